@@ -1,0 +1,265 @@
+"""Generate golden vectors from the REAL reference package (run in the build
+container only; /root/reference does not exist on the GPU box).
+
+    python tools/make_golden.py            # writes tests/golden/*.npz
+
+The reference ``pyrstereo`` is imported from /root/reference/pkg/src.  Its
+prior window is hard-coded to +-1 (matcher.py:280,294); for the BASELINE
+radii (2, 3) this script drives the reference's own stage functions
+(CostEngine.at / dsi_rows, refine_level, selective_median, upsample_prior,
+build_pyramid) with a radius-generalised copy of select_with_prior's control
+flow, and checks at radius 1 that this driver reproduces run_pipeline
+bit-for-bit.
+"""
+
+from __future__ import annotations
+
+import os
+import sys
+import time
+
+import numpy as np
+
+REF = "/root/reference/pkg/src"
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+OUT = os.path.join(ROOT, "tests", "golden")
+sys.path.insert(0, REF)
+sys.path.insert(0, ROOT)
+
+import pyrstereo as ref  # noqa: E402
+from pyrstereo import matcher as ref_matcher  # noqa: E402
+from paper_1901_09593_b200.synthetic import CONFIGS, make_pair  # noqa: E402
+
+COUNT_KEYS = ("trusted", "trusted_evals", "trusted_window_max",
+              "full_search_pixels", "selection_evals", "refined",
+              "refine_evals", "median_replaced")
+
+
+def select_r(engine, d_hat, c_hat, beta, r):
+    """matcher.py:263-320 with offsets range(-r, r+1)."""
+    h, w = c_hat.shape
+    d_max = engine.d_max
+    finite = np.isfinite(d_hat)
+    center = np.where(finite, d_hat, 0.0).astype(np.intp)
+    window_ok = finite & (center + r >= 0) & (center - r <= d_max)
+    trusted = (c_hat > beta) & window_ok
+    disparity = np.empty((h, w))
+    cost = np.empty((h, w))
+    stats = ref_matcher.SelectionStats(trusted=int(trusted.sum()))
+    before = engine.counter.count
+    if stats.trusted:
+        ti, tj = np.nonzero(trusted)
+        tz = center[ti, tj]
+        best_c = np.full(ti.shape[0], -2.0)
+        best_z = np.zeros(ti.shape[0], dtype=np.intp)
+        ws = np.zeros(ti.shape[0], dtype=np.intp)
+        for off in range(-r, r + 1):
+            z = tz + off
+            legal = (z >= 0) & (z <= d_max)
+            if not legal.any():
+                continue
+            ws[legal] += 1
+            c = engine.at(ti[legal], tj[legal], z[legal])
+            improve = c > best_c[legal]
+            sel = np.nonzero(legal)[0][improve]
+            best_c[sel] = c[improve]
+            best_z[sel] = z[legal][improve]
+        disparity[ti, tj] = best_z.astype(np.float64)
+        cost[ti, tj] = best_c
+        stats.window_max = int(ws.max())
+        stats.trusted_evals = engine.counter.count - before
+    full = ~trusted
+    stats.full_search_pixels = int(full.sum())
+    if stats.full_search_pixels:
+        fi, fj = np.nonzero(full)
+        rows = engine.dsi_rows(fi, fj)
+        best = np.argmax(rows, axis=1)
+        disparity[fi, fj] = best.astype(np.float64)
+        cost[fi, fj] = rows[np.arange(fi.shape[0]), best]
+    stats.evals = engine.counter.count - before
+    return disparity, cost, stats
+
+
+def pipeline_r(left, right, config, r):
+    """run_pipeline (matcher.py:398-466) with select_r at finer levels."""
+    pyr = ref.build_pyramid(left, right, config.d_max, levels=config.levels,
+                            base_block=config.block)
+    counter = ref.EvalCounter()
+    trace = ref.PipelineTrace()
+
+    def mk(level):
+        return ref.LevelTrace(level=level.index, height=level.shape[0],
+                              width=level.shape[1], d_max=level.d_max,
+                              block=level.block)
+
+    coarse = pyr.coarsest
+    eng = ref.CostEngine(coarse.left, coarse.right, coarse.block, coarse.d_max,
+                         sigma_eps=config.sigma_eps, sign=config.sign,
+                         counter=counter)
+    lt = mk(coarse)
+    d, c = ref_matcher._process_level(eng, lt, config.alpha,
+                                      lambda: ref.match_coarsest(eng))
+    lt.full_search_pixels = lt.pixels
+    lt.selection_evals = lt.pixels * (coarse.d_max + 1)
+    trace.levels.append(lt)
+    for k in range(len(pyr) - 2, -1, -1):
+        lv = pyr[k]
+        eng = ref.CostEngine(lv.left, lv.right, lv.block, lv.d_max,
+                             sigma_eps=config.sigma_eps, sign=config.sign,
+                             counter=counter)
+        lt = mk(lv)
+        d_hat, c_hat = ref.upsample_prior(d, c, lv.shape)
+        box = []
+
+        def sel():
+            dd, cc, st = select_r(eng, d_hat, c_hat, config.beta, r)
+            box.append(st)
+            return dd, cc
+
+        d, c = ref_matcher._process_level(eng, lt, config.alpha, sel)
+        st = box[0]
+        lt.trusted = st.trusted
+        lt.trusted_evals = st.trusted_evals
+        lt.trusted_window_max = st.window_max
+        lt.full_search_pixels = st.full_search_pixels
+        lt.selection_evals = st.evals
+        trace.levels.append(lt)
+    return d, c, trace
+
+
+def counts_array(trace):
+    return np.array([[lt.level, lt.height, lt.width, lt.d_max, lt.block]
+                     + [getattr(lt, k) for k in COUNT_KEYS]
+                     for lt in trace.levels], dtype=np.int64)
+
+
+def save(name, **arrays):
+    path = os.path.join(OUT, name)
+    np.savez_compressed(path, **arrays)
+    print(f"wrote {path} ({os.path.getsize(path) / 1e6:.2f} MB)")
+
+
+def pipeline_case(name, left, right, d_max, levels, block, r, sign="middlebury",
+                  alpha=0.9, beta=0.9):
+    cfg = ref.MatchConfig(d_max=d_max, levels=levels, block=block, alpha=alpha,
+                          beta=beta, sign=sign)
+    t0 = time.perf_counter()
+    if r == 1:
+        d, c, tr = ref.run_pipeline(left, right, cfg)
+        d2, c2, tr2 = pipeline_r(left, right, cfg, 1)
+        assert np.array_equal(d, d2) and np.array_equal(c, c2)
+        assert tr.counts_dict() == tr2.counts_dict()
+    else:
+        d, c, tr = pipeline_r(left, right, cfg, r)
+    dt = time.perf_counter() - t0
+    print(f"{name}: {left.shape} D={d_max} K={levels} b={block} r={r} "
+          f"{dt:.1f}s total_evals={tr.total_evals}")
+    save(f"pipe_{name}.npz", left=left, right=right, disparity=d.astype(np.int16),
+         cost=c, counts=counts_array(tr),
+         params=np.array([d_max, levels, block, r, 1 if sign == "paper" else 0]),
+         gates=np.array([alpha, beta]), ref_seconds=np.array(dt))
+
+
+def stage_cases():
+    rng = np.random.default_rng(20261019)
+    out = {}
+    # gaussian_downsample (pyramid.py:71-81)
+    for i, shp in enumerate([(8, 8), (7, 9), (31, 17), (64, 48)]):
+        img = rng.random(shp) * 255.0
+        out[f"down_in_{i}"] = img
+        out[f"down_out_{i}"] = ref.gaussian_downsample(img)
+    # CostEngine stats (zncc.py:185-189)
+    for i, (shp, b) in enumerate([((12, 15), 3), ((20, 17), 5), ((16, 16), 9)]):
+        img = rng.random(shp) * 255.0
+        e = ref.CostEngine(img, img, b, 4)
+        out[f"stats_in_{i}"] = img
+        out[f"stats_b_{i}"] = np.array(b)
+        out[f"stats_mean_{i}"] = e.mean_l
+        out[f"stats_sigma_{i}"] = e.sigma_l
+    # upsample_prior incl. the scipy cubic B-spline (matcher.py:236-260)
+    for i, (ch, cw, h, w) in enumerate([(4, 5, 8, 10), (5, 6, 9, 11),
+                                        (47, 57, 94, 113), (94, 113, 188, 225)]):
+        dc = rng.integers(0, 40, size=(ch, cw)).astype(np.float64)
+        cc = np.clip(rng.normal(0.7, 0.4, size=(ch, cw)), -1, 1)
+        dh, chat = ref.upsample_prior(dc, cc, (h, w))
+        out[f"up_d_{i}"] = dc
+        out[f"up_c_{i}"] = cc
+        out[f"up_shape_{i}"] = np.array([h, w])
+        out[f"up_dhat_{i}"] = dh
+        out[f"up_chat_{i}"] = chat
+    # selective_median (criterion-7 style, matcher.py:323-359)
+    med_d, med_c, med_a, med_out = [], [], [], []
+    mrng = np.random.default_rng(1007)
+    for _ in range(100):
+        dd = mrng.integers(0, 20, size=(9, 9)).astype(float)
+        cc = mrng.uniform(-1.0, 1.0, size=(9, 9))
+        a = float(mrng.uniform(0.2, 0.95))
+        med_d.append(dd), med_c.append(cc), med_a.append(a)
+        med_out.append(ref.selective_median(dd, cc, a))
+    out["med_d"] = np.array(med_d)
+    out["med_c"] = np.array(med_c)
+    out["med_alpha"] = np.array(med_a)
+    out["med_out"] = np.array(med_out)
+    # coarse full search (criterion-1 style, matcher.py:184-193)
+    frng = np.random.default_rng(1001)
+    for i in range(24):
+        h = int(frng.integers(16, 33))
+        w = int(frng.integers(16, 33))
+        d_max = int(frng.integers(4, 11))
+        block = int(frng.choice([3, 5]))
+        left, right = frng.random((h, w)), frng.random((h, w))
+        sign = "paper" if i % 4 == 3 else "middlebury"
+        e = ref.CostEngine(left, right, block=block, d_max=d_max, sign=sign)
+        d, c = ref.match_coarsest(e)
+        out[f"full_l_{i}"] = left
+        out[f"full_r_{i}"] = right
+        out[f"full_p_{i}"] = np.array([d_max, block, 1 if sign == "paper" else 0])
+        out[f"full_d_{i}"] = d
+        out[f"full_c_{i}"] = c
+    # select_with_prior r=1 and refine_level on a shifted pair
+    srng = np.random.default_rng(7)
+    left, right = ref.shifted_pair(24, 40, 5, srng, cutoff=0.1)
+    e = ref.CostEngine(left, right, block=5, d_max=12)
+    d_hat = np.clip(np.round(5 + srng.normal(0, 2, size=(24, 40))), -3, 15)
+    d_hat[3, 4] = np.nan
+    c_hat = srng.uniform(0.5, 1.0, size=(24, 40))
+    d, c, st = ref.select_with_prior(e, d_hat, c_hat, 0.9)
+    out.update(sel_l=left, sel_r=right, sel_dhat=d_hat, sel_chat=c_hat,
+               sel_d=d, sel_c=c,
+               sel_stats=np.array([st.trusted, st.trusted_evals, st.window_max,
+                                   st.full_search_pixels, st.evals]))
+    e2 = ref.CostEngine(left, right, block=5, d_max=12)
+    rd, rc = ref.refine_level(e2, d, c, 0.9)
+    out.update(ref_d=rd, ref_c=rc, ref_evals=np.array(e2.counter.count))
+    save("stages.npz", **out)
+
+
+def main():
+    os.makedirs(OUT, exist_ok=True)
+    stage_cases()
+    rng = np.random.default_rng(16)
+    left, right = ref.shifted_pair(64, 64, 6, rng, cutoff=0.05)
+    pipeline_case("shift64_b11", left, right, 16, 2, 11, 1)
+    rng = np.random.default_rng(20)
+    r_, l_ = ref.shifted_pair(64, 64, 5, rng, cutoff=0.05)
+    pipeline_case("paper64_b11", l_, r_, 16, 2, 11, 1, sign="paper")
+    rng = np.random.default_rng(19)
+    left, right = ref.shifted_pair(48, 56, 4, rng, cutoff=0.05)
+    pipeline_case("shift48_k0", left, right, 12, 0, 5, 1)
+    # BASELINE C1 at full size: r=1 (reference run_pipeline) and r=2
+    l1, r1, _ = make_pair(CONFIGS["C1"])
+    pipeline_case("C1_r1", l1, r1, 64, 2, 5, 1)
+    pipeline_case("C1_r2", l1, r1, 64, 2, 5, 2)
+    # parity-size crops of the other configs at their own parameters
+    crops = {"C2": (248, 368), "C3": (248, 368), "C4": (180, 320),
+             "C5": (384, 512)}
+    for name, (h, w) in crops.items():
+        cfg = CONFIGS[name]
+        lc, rc, _ = make_pair(cfg, height=h, width=w)
+        pipeline_case(f"{name}crop", lc, rc, cfg.d_max, cfg.levels, cfg.block,
+                      cfg.radius)
+
+
+if __name__ == "__main__":
+    main()
