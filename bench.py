@@ -1,0 +1,343 @@
+"""Benchmark: MSHBM disparity hot path on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2]
+                    [--impl ours|reference] [--no-cpu-baseline]
+
+One "step" = one stereo pair of the workload (default BASELINE config C2,
+1472x992, D=144, 4 pyramid levels, 7x7 window, prior radius 2) through the
+whole hot path: pyramid -> per-level stats -> fused ZNCC sweep + WTA +
+refinement -> selective median -> B-spline prior for the next level.
+
+value  : full-search-equivalent Mpixel*disparities/s = N * W*H*(D+1) / t,
+         inputs resident in HBM, CUDA events on the launching stream, L2
+         flushed (256 MiB write) between steps, max over ranks.
+e2e    : the same metric through the C-ABI call a user makes
+         (mshbm_run_pipeline, MSHBM_IO_HOST) from pinned host buffers:
+         H2D of both images + D2H of disparity (int16) and cost (fp32)
+         inside the timed region.
+N > 1  : torchrun, one rank per GPU, each rank its own pair (seed + rank):
+         independent pairs shard with no data-path collective ("weak").
+--impl reference: the CPU oracle port (oracle/mshbm_oracle.py, the
+         reference's own numpy algorithm restated; the reference package is
+         pure Python and cannot travel to the box) on a bounded crop of the
+         same workload, rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_1901_09593_b200.synthetic import CONFIGS, make_pair  # noqa: E402
+
+METRIC = "Mpixel-disparities/s"
+UNIT = "Mpixel*disparities/s (full-search-equivalent W*H*(D+1)/t)"
+CPU_SAMPLE = (352, 512)     # (H, W) crop of the workload for the CPU legs
+
+
+def flops_per_pde(b: int) -> int:
+    """direct ZNCC F(b) = 2 b^2 + 8 flops per (pixel, disparity)."""
+    return 2 * b * b + 8
+
+
+def workload_desc(cfg) -> dict:
+    return {"workload": f"{cfg.name} {cfg.width}x{cfg.height} D={cfg.d_max} "
+                        f"levels={cfg.levels + 1} block={cfg.block} radius={cfg.radius}",
+            "width": cfg.width, "height": cfg.height, "d_max": cfg.d_max,
+            "pyramid_levels": cfg.levels + 1, "block": cfg.block, "radius": cfg.radius,
+            "alpha": 0.9, "beta": 0.9, "noise_sigma": cfg.noise,
+            "full_search_pde_per_pair": cfg.full_search_pde}
+
+
+# --------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+    NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+        self.t = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        sm, mx, reasons = [], None, set()
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for name, v in zip(self.NAMES, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# --------------------------------------------------------------------- dist
+def dist_init():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def cpu_oracle_run(cfg, seed, workers):
+    """Time the CPU oracle port on the bounded crop sample; returns (s, pde)."""
+    from oracle import mshbm_oracle as O
+    h, w = CPU_SAMPLE
+    left, right, _ = make_pair(cfg, seed=seed, height=h, width=w)
+    t0 = time.perf_counter()
+    O.run_pipeline(left, right, cfg.d_max, cfg.levels, cfg.block, radius=cfg.radius,
+                   workers=workers)
+    dt = time.perf_counter() - t0
+    return dt, h * w * (cfg.d_max + 1)
+
+
+def run_reference(args, cfg):
+    ws, rank, _ = dist_init()
+    if rank != 0:
+        return
+    workers = os.cpu_count() or 1
+    times = []
+    pde = 0
+    for k in range(args.warmup + args.steps):
+        dt, pde = cpu_oracle_run(cfg, cfg.seed, workers)
+        if k >= args.warmup:
+            times.append(dt)
+    t = statistics.mean(times)
+    val = pde / t / 1e6
+    h, w = CPU_SAMPLE
+    line = {
+        "impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": f"synthetic BASELINE generator, {cfg.name} params, {w}x{h} crop, seed {cfg.seed}",
+        "config": workload_desc(cfg),
+        "cpu_baseline": {"value": val, "unit": UNIT, "cores": workers, "kind": "port",
+                         "sample": f"{w}x{h} crop of {cfg.name} (D={cfg.d_max}, "
+                                   f"levels={cfg.levels + 1}, b={cfg.block}, r={cfg.radius}) "
+                                   "through oracle/mshbm_oracle.run_pipeline (numpy fp64)"},
+        "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------- ours
+def run_ours(args, cfg):
+    import torch
+    import torch.distributed as dist
+
+    ws, rank, local = dist_init()
+    if ws > 1:
+        dist.init_process_group("nccl", init_method="env://")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+
+    import paper_1901_09593_b200 as gpu
+    from paper_1901_09593_b200 import _lib
+
+    gpu.matcher.STAGE_TIMING = False
+    seed = cfg.seed + rank
+    left, right, _ = make_pair(cfg, seed=seed)
+    lt = torch.from_numpy(left).to(dev)
+    rt = torch.from_numpy(right).to(dev)
+    mc = gpu.MatchConfig(d_max=cfg.d_max, levels=cfg.levels, block=cfg.block,
+                         radius=cfg.radius)
+    stream = torch.cuda.current_stream(dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    def barrier():
+        if ws > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    # trace of this pair (exact counters): evaluated PDE count, level-0 work
+    _, _, trace = gpu.run_pipeline_device(lt, rt, mc, trace=True)
+    l0 = trace.levels[-1]
+    for _ in range(args.warmup):
+        gpu.run_pipeline_device(lt, rt, mc, trace=False)
+    barrier()
+
+    # ---- device-resident timed region
+    ctx = _lib.context(local)
+    n0 = _lib.lib().mshbm_launch_count(ctx)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    with ClockSampler(local) as clocks:
+        barrier()
+        for k in range(args.steps):
+            flush.fill_(k & 0xFF)
+            ev[k][0].record(stream)
+            gpu.run_pipeline_device(lt, rt, mc, trace=False)
+            ev[k][1].record(stream)
+        barrier()
+    launches = int(_lib.lib().mshbm_launch_count(ctx) - n0)
+    ms_steps = [a.elapsed_time(b) for a, b in ev]
+    ms = sum(ms_steps) / len(ms_steps)
+    if ws > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = ws * cfg.full_search_pde / (ms * 1e-3) / 1e6
+
+    # ---- end to end through the C ABI with host buffers (pinned)
+    hl = torch.from_numpy(left).pin_memory()
+    hr = torch.from_numpy(right).pin_memory()
+    hd = torch.empty((cfg.height, cfg.width), dtype=torch.int16).pin_memory()
+    hc = torch.empty((cfg.height, cfg.width), dtype=torch.float32).pin_memory()
+    cc = mc.to_c()
+    sptr = C.c_void_p(stream.cuda_stream)
+
+    def e2e_call():
+        st = _lib.lib().mshbm_run_pipeline(ctx, hl.data_ptr(), hr.data_ptr(), cfg.height,
+                                           cfg.width, cfg.width, C.byref(cc), hd.data_ptr(),
+                                           hc.data_ptr(), cfg.width, None, None,
+                                           _lib.IO_HOST, 0, sptr)
+        _lib.check(st, ctx)
+
+    for _ in range(max(1, args.warmup)):
+        e2e_call()
+    barrier()
+    eev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    for k in range(args.steps):
+        flush.fill_(k & 0xFF)
+        eev[k][0].record(stream)
+        e2e_call()
+        eev[k][1].record(stream)
+    barrier()
+    ems = sum(a.elapsed_time(b) for a, b in eev) / args.steps
+    if ws > 1:
+        t = torch.tensor([ems], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ems = float(t.item())
+    e2e_value = ws * cfg.full_search_pde / (ems * 1e-3) / 1e6
+    h2d = 2 * cfg.width * cfg.height * 4
+    d2h = cfg.width * cfg.height * (2 + 4)
+
+    # ---- roofline of the dominant kernel (level-0 sweep), live CUDA events
+    gpu.matcher.STAGE_TIMING = True
+    sweep_ms = []
+    for _ in range(5):
+        flush.fill_(1)
+        _, _, tt = gpu.run_pipeline(left, right, mc)
+        sweep_ms.append(tt.levels[-1].seconds["select"] * 1e3)
+        step_ms = sum(sum(v for v in lv.seconds.values()) for lv in tt.levels)
+    sweep_ms = statistics.median(sweep_ms)
+    tf = C.c_double()
+    pms = C.c_double()
+    _lib.check(_lib.lib().mshbm_probe_fp32_peak(local, 20000, C.byref(tf), C.byref(pms)))
+    alg_flops = l0.evals * flops_per_pde(l0.block)
+    achieved = alg_flops / (sweep_ms * 1e-3) / 1e12
+    dense_flops = l0.pixels * (l0.d_max + 1) * flops_per_pde(l0.block)
+    roof = {"bound": "fp32", "kernel": "sweep_kernel<b=%d> (level 0)" % l0.block,
+            "achieved": achieved, "peak": tf.value, "unit": "TFLOP/s",
+            "frac": achieved / tf.value, "traffic": None,
+            "peak_source": "measured live: mshbm_probe_fp32_peak FFMA probe on this GPU "
+                           "(MEASURED_PEAKS.json has no FP32 figure)",
+            "algorithmic_flops_per_launch": alg_flops,
+            "algorithmic_basis": "level-0 trace evals (selection_evals + refine_evals) "
+                                 "x F(b)=2b^2+8 (SURVEY 8d)",
+            "launch_ms": sweep_ms, "share_of_step": sweep_ms / step_ms if step_ms else None,
+            "dense_pde_flops_per_launch": dense_flops,
+            "dense_achieved": dense_flops / (sweep_ms * 1e-3) / 1e12}
+
+    out = None
+    if rank == 0:
+        out = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32", "data": f"synthetic BASELINE generator ({cfg.name}), seed "
+                                    f"{cfg.seed}+rank; L2 flushed (256 MiB) between steps",
+            "config": dict(workload_desc(cfg), parallelism=f"pair-parallel x{ws}",
+                           l2="flushed between timed steps"),
+            "pairs_per_s": ws / (ms * 1e-3),
+            "evaluated_mpd_per_s": ws * trace.total_evals / (ms * 1e-3) / 1e6,
+            "total_evals_per_pair": trace.total_evals,
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h, "ms_per_step": ems,
+                    "path": "mshbm_run_pipeline(MSHBM_IO_HOST) from pinned host buffers"},
+            "roofline": roof,
+            "gpu_launches": launches,
+            "clocks": clocks.summary(),
+        }
+        if ws == 1 and not args.no_cpu_baseline:
+            workers = os.cpu_count() or 1
+            dt, pde = cpu_oracle_run(cfg, cfg.seed, workers)
+            h, w = CPU_SAMPLE
+            out["cpu_baseline"] = {
+                "value": pde / dt / 1e6, "unit": UNIT, "cores": workers, "kind": "port",
+                "sample": f"{w}x{h} crop of {cfg.name} params through the numpy oracle "
+                          f"(reference algorithm, fp64), {dt:.1f} s"}
+    if ws > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    if out is not None:
+        print(json.dumps(out), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="C2", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup) if args.impl == "ours" else args.warmup
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg)
+    else:
+        run_ours(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,58 @@
+"""B200-native MSHBM disparity engine -- drop-in for the reference ``pyrstereo``
+hot path (``/root/reference/pkg/src/pyrstereo``: pyramid, cost engine,
+matcher).  ``import paper_1901_09593_b200 as pyrstereo`` exposes the same
+names for the disparity path; the work runs in libmshbm.so (sm_100a CUDA)
+through the C ABI in include/mshbm.h.  Codecs, evaluation, the naive
+baseline and the CLI are out of scope.
+"""
+
+from .matcher import (
+    ConfigError,
+    LevelTrace,
+    MatchConfig,
+    PipelineTrace,
+    SelectionStats,
+    match_coarsest,
+    match_level_with_prior,
+    refine_level,
+    run_pipeline,
+    run_pipeline_device,
+    select_with_prior,
+    selective_median,
+    upsample_prior,
+)
+from .pyramid import (
+    BINOMIAL_KERNEL,
+    PyramidLevel,
+    StereoPyramid,
+    auto_levels,
+    build_pyramid,
+    gaussian_downsample,
+    level_block,
+    level_d_max,
+)
+from .zncc import (
+    SIGN_MIDDLEBURY,
+    SIGN_PAPER_PLUS,
+    CostEngine,
+    DsiSlice,
+    EvalCounter,
+    PatchStats,
+    averaged_dsi,
+    dsi_entry,
+    patch_stats,
+    zncc,
+)
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "BINOMIAL_KERNEL", "ConfigError", "CostEngine", "DsiSlice", "EvalCounter",
+    "LevelTrace", "MatchConfig", "PatchStats", "PipelineTrace", "PyramidLevel",
+    "SIGN_MIDDLEBURY", "SIGN_PAPER_PLUS", "SelectionStats", "StereoPyramid",
+    "auto_levels", "averaged_dsi", "build_pyramid", "dsi_entry",
+    "gaussian_downsample", "level_block", "level_d_max", "match_coarsest",
+    "match_level_with_prior", "patch_stats", "refine_level", "run_pipeline",
+    "run_pipeline_device", "select_with_prior", "selective_median",
+    "upsample_prior", "zncc",
+]

@@ -1,0 +1,836 @@
+// libmshbm: context, per-shape execution plans (CUDA-graph captured), level
+// orchestration of run_pipeline, CostEngine handles and the C ABI declared
+// in include/mshbm.h.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "../../include/mshbm.h"
+#include "common.cuh"
+#include "kernels.h"
+
+using namespace mshbm;
+
+namespace {
+
+thread_local std::string g_err;
+
+int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
+
+struct LevelBuf {
+  int h = 0, w = 0, d = 0, b = 0;
+  int64_t ld = 0;
+  double* L = nullptr;
+  double* R = nullptr;
+  float* muR = nullptr;
+  float* isR = nullptr;
+  int* wc = nullptr;
+  int16_t* dsel = nullptr;
+  int16_t* dmed = nullptr;
+  float* c = nullptr;
+  uint8_t* low = nullptr;
+  double* coef = nullptr;   // spline coefficients of this level's cost map
+  int64_t ldc = 0;
+};
+
+struct PlanKey {
+  int H, W, K, user;
+  int d_max, block, radius, sign;
+  double alpha, beta, eps;
+  std::vector<int> lvl;     // per-level (h, w, d, b) for user pyramids
+  bool operator<(const PlanKey& o) const {
+    return std::tie(H, W, K, user, d_max, block, radius, sign, alpha, beta, eps, lvl) <
+           std::tie(o.H, o.W, o.K, o.user, o.d_max, o.block, o.radius, o.sign, o.alpha,
+                    o.beta, o.eps, o.lvl);
+  }
+};
+
+struct Plan {
+  PlanKey key{};
+  int H = 0, W = 0, K = 0;
+  bool user = false;
+  mshbm_config cfg{};
+  std::vector<LevelBuf> lv;
+  float* in_l = nullptr;
+  float* in_r = nullptr;
+  int64_t ld_in = 0;
+  unsigned long long* counters = nullptr;
+  void* arena = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  int launches = 0;
+};
+
+}  // namespace
+
+struct mshbm_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  std::string err;
+  std::map<PlanKey, Plan*> plans;
+  int64_t launches = 0;
+  cudaEvent_t ev[64];
+  int n_ev = 0;
+};
+
+struct mshbm_engine {
+  mshbm_ctx* ctx = nullptr;
+  int H = 0, W = 0, d = 0, b = 0, dir = 1;
+  double eps = 1e-6;
+  int64_t ld = 0;
+  double *L = nullptr, *R = nullptr;
+  double *muL = nullptr, *sgL = nullptr, *muR = nullptr, *sgR = nullptr;
+  float *muR32 = nullptr, *isR32 = nullptr;
+  int* wc = nullptr;
+  int16_t *fz = nullptr, *wz = nullptr, *nz = nullptr;
+  float *fc = nullptr, *wcst = nullptr, *nc = nullptr;
+  unsigned long long* counters = nullptr;
+  int* bad = nullptr;
+  void* arena = nullptr;
+};
+
+namespace {
+
+int fail(mshbm_ctx* ctx, int code, const std::string& msg) {
+  g_err = msg;
+  if (ctx) ctx->err = msg;
+  return code;
+}
+
+#define CK(call)                                                                    \
+  do {                                                                              \
+    cudaError_t e_ = (call);                                                        \
+    if (e_ != cudaSuccess)                                                          \
+      return fail(ctx, MSHBM_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+// NULL selects the legacy default stream (CUDA's own convention), so calls
+// from torch's default stream stay ordered with torch's work.
+cudaStream_t pick(mshbm_ctx*, void* s) { return (cudaStream_t)s; }
+
+// ---------------------------------------------------------------- config
+int validate_config(mshbm_ctx* ctx, const mshbm_config* c) {
+  char buf[160];
+  if (!c) return fail(ctx, MSHBM_ERR_CONFIG, "null config");
+  if (c->d_max < 1) {
+    snprintf(buf, sizeof buf, "d_max must be >= 1, got %d", c->d_max);
+    return fail(ctx, MSHBM_ERR_CONFIG, buf);
+  }
+  if (c->block < 3 || c->block % 2 == 0) {
+    snprintf(buf, sizeof buf, "block must be odd and >= 3, got %d", c->block);
+    return fail(ctx, MSHBM_ERR_CONFIG, buf);
+  }
+  if (!(c->alpha > 0.0 && c->alpha < 1.0)) {
+    snprintf(buf, sizeof buf, "alpha must lie in (0, 1), got %g", c->alpha);
+    return fail(ctx, MSHBM_ERR_CONFIG, buf);
+  }
+  if (!(c->beta > 0.0 && c->beta < 1.0)) {
+    snprintf(buf, sizeof buf, "beta must lie in (0, 1), got %g", c->beta);
+    return fail(ctx, MSHBM_ERR_CONFIG, buf);
+  }
+  if (!(c->sigma_eps > 0.0)) {
+    snprintf(buf, sizeof buf, "sigma_eps must be positive, got %g", c->sigma_eps);
+    return fail(ctx, MSHBM_ERR_CONFIG, buf);
+  }
+  if (c->sign != MSHBM_SIGN_MIDDLEBURY && c->sign != MSHBM_SIGN_PAPER)
+    return fail(ctx, MSHBM_ERR_CONFIG, "unknown sign convention");
+  if (c->radius < 0) return fail(ctx, MSHBM_ERR_CONFIG, "radius must be >= 0");
+  return MSHBM_OK;
+}
+
+// ---------------------------------------------------------------- plans
+struct Carver {
+  size_t off = 0;
+  char* base = nullptr;
+  template <typename T>
+  T* take(size_t n) {
+    off = (size_t)round_up((int64_t)off, 256);
+    T* p = base ? (T*)(base + off) : nullptr;
+    off += n * sizeof(T);
+    return p;
+  }
+};
+
+void carve(Plan& p, Carver& cv) {
+  const int64_t ldi = round_up(p.W, 32);
+  p.ld_in = ldi;
+  p.in_l = cv.take<float>((size_t)ldi * p.H);
+  p.in_r = cv.take<float>((size_t)ldi * p.H);
+  p.counters = cv.take<unsigned long long>((size_t)(p.K + 1) * kCntSlots);
+  for (auto& l : p.lv) {
+    const size_t n = (size_t)l.ld * l.h;
+    l.L = cv.take<double>(n);
+    l.R = cv.take<double>(n);
+    l.muR = cv.take<float>(n);
+    l.isR = cv.take<float>(n);
+    l.wc = cv.take<int>(n);
+    l.dsel = cv.take<int16_t>(n);
+    l.dmed = cv.take<int16_t>(n);
+    l.c = cv.take<float>(n);
+    l.low = cv.take<uint8_t>(n);
+    l.ldc = round_up(l.w + 24, 32);
+    l.coef = cv.take<double>((size_t)l.ldc * (l.h + 24) * 2);   // + IIR scratch
+  }
+}
+
+int build_plan(mshbm_ctx* ctx, Plan& p) {
+  Carver probe;
+  carve(p, probe);
+  CK(cudaMalloc(&p.arena, probe.off + 256));
+  Carver real;
+  real.base = (char*)p.arena;
+  carve(p, real);
+  return MSHBM_OK;
+}
+
+struct StageEvents {
+  cudaEvent_t up0, up1, sel0, sel1, med0, med1;
+};
+
+// Enqueue the whole pair on `s` (also used under stream capture).
+int enqueue(mshbm_ctx* ctx, Plan& p, cudaStream_t s, std::vector<StageEvents>* tev) {
+  int n = 0;
+  const mshbm_config& cfg = p.cfg;
+  const int dir = cfg.sign == MSHBM_SIGN_PAPER ? -1 : 1;
+  CK(cudaMemsetAsync(p.counters, 0, sizeof(unsigned long long) * (p.K + 1) * kCntSlots, s));
+  if (!p.user) {
+    CK(launch_f32_to_f64(p.in_l, p.in_r, p.H, p.W, p.ld_in, p.lv[0].L, p.lv[0].R, p.lv[0].ld, s));
+    ++n;
+    for (int k = 1; k <= p.K; ++k) {
+      const LevelBuf& a = p.lv[k - 1];
+      LevelBuf& b = p.lv[k];
+      CK(launch_downsample(a.L, a.R, a.h, a.w, a.ld, b.L, b.R, b.ld, s));
+      ++n;
+    }
+  }
+  for (int k = 0; k <= p.K; ++k) {
+    LevelBuf& l = p.lv[k];
+    CK(launch_stats_f32(l.R, l.h, l.w, l.ld, l.b, cfg.sigma_eps, l.muR, l.isR, l.ld, s));
+    ++n;
+  }
+  for (int k = p.K; k >= 0; --k) {
+    LevelBuf& l = p.lv[k];
+    unsigned long long* cnt = p.counters + (size_t)(p.K - k) * kCntSlots;
+    StageEvents* ev = tev ? &(*tev)[p.K - k] : nullptr;
+    if (ev) CK(cudaEventRecord(ev->up0, s));
+    if (k < p.K) {
+      LevelBuf& c = p.lv[k + 1];
+      CK(launch_bspline_prefilter(c.c, nullptr, c.h, c.w, c.ld, c.coef, c.ldc, s));
+      n += 5;
+      CK(launch_prior_eval(c.dmed, c.ld, c.h, c.w, c.coef, c.ldc, l.h, l.w, l.d, cfg.radius,
+                           cfg.beta, l.wc, l.ld, cnt, s));
+      ++n;
+    }
+    if (ev) CK(cudaEventRecord(ev->up1, s));
+    SweepArgs a{};
+    a.L = l.L; a.R = l.R; a.ld = l.ld;
+    a.muR = l.muR; a.isR = l.isR; a.lds = l.ld;
+    a.H = l.h; a.W = l.w; a.d = l.d; a.block = l.b; a.dir = dir;
+    a.sigma_eps = cfg.sigma_eps;
+    a.wc = k < p.K ? l.wc : nullptr; a.ldw = l.ld; a.radius = cfg.radius;
+    a.alpha = cfg.alpha; a.mode = kSweepPipeline;
+    a.dout = l.dsel; a.cout = l.c; a.low = l.low; a.ldo = l.ld;
+    a.counters = cnt;
+    if (ev) CK(cudaEventRecord(ev->sel0, s));
+    CK(launch_sweep(a, s, &n));
+    if (ev) CK(cudaEventRecord(ev->sel1, s));
+    if (ev) CK(cudaEventRecord(ev->med0, s));
+    CK(launch_median_pipeline(l.dsel, l.c, l.low, l.ld, l.h, l.w, cfg.alpha, l.dmed, cnt, s));
+    ++n;
+    if (ev) CK(cudaEventRecord(ev->med1, s));
+  }
+  p.launches = n;
+  return MSHBM_OK;
+}
+
+Plan* get_plan(mshbm_ctx* ctx, const PlanKey& key, const mshbm_config& cfg,
+               const std::vector<std::tuple<int, int, int, int>>& dims, int* st) {
+  auto it = ctx->plans.find(key);
+  if (it != ctx->plans.end()) return it->second;
+  Plan* p = new Plan();
+  p->key = key;
+  p->H = key.H;
+  p->W = key.W;
+  p->K = key.K;
+  p->user = key.user != 0;
+  p->cfg = cfg;
+  for (auto& t : dims) {
+    LevelBuf l;
+    l.h = std::get<0>(t);
+    l.w = std::get<1>(t);
+    l.d = std::get<2>(t);
+    l.b = std::get<3>(t);
+    l.ld = round_up(l.w, 32);
+    p->lv.push_back(l);
+  }
+  *st = build_plan(ctx, *p);
+  if (*st != MSHBM_OK) {
+    delete p;
+    return nullptr;
+  }
+  ctx->plans[key] = p;
+  return p;
+}
+
+// run a plan: graph replay (captured on first use) or direct launches.
+// Stage events are only recorded on the direct path (MSHBM_FLAG_TIMING).
+int launch_plan(mshbm_ctx* ctx, Plan& p, cudaStream_t s, int flags,
+                std::vector<StageEvents>* tev) {
+  const bool direct = (tev != nullptr) || (flags & MSHBM_FLAG_NO_GRAPH);
+  if (tev) {
+    tev->resize(p.K + 1);
+    for (auto& e : *tev) {
+      cudaEvent_t* ev = &e.up0;
+      for (int t = 0; t < 6; ++t) CK(cudaEventCreate(&ev[t]));
+    }
+  }
+  if (direct) {
+    int st = enqueue(ctx, p, s, tev);
+    if (st) return st;
+  } else {
+    if (!p.exec) {
+      cudaStream_t cs;
+      CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+      cudaGraph_t g;
+      CK(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+      int st = enqueue(ctx, p, cs, nullptr);
+      cudaError_t ce = cudaStreamEndCapture(cs, &g);
+      cudaStreamDestroy(cs);
+      if (st) return st;
+      CK(ce);
+      CK(cudaGraphInstantiate(&p.exec, g, 0));
+      cudaGraphDestroy(g);
+    }
+    CK(cudaGraphLaunch(p.exec, s));
+  }
+  ctx->launches += p.launches;
+  return MSHBM_OK;
+}
+
+// Copy the device counters back (synchronises `s`) and pack the trace
+// exactly as run_pipeline fills LevelTrace (matcher.py:377-463, A.10).
+int finish_trace(mshbm_ctx* ctx, Plan& p, cudaStream_t s, mshbm_level_trace* trace,
+                 std::vector<StageEvents>* tev) {
+  std::vector<unsigned long long> h((size_t)(p.K + 1) * kCntSlots);
+  CK(cudaMemcpyAsync(h.data(), p.counters, h.size() * sizeof(h[0]), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  for (int t = 0; t <= p.K; ++t) {
+    const int k = p.K - t;
+    const LevelBuf& l = p.lv[k];
+    const unsigned long long* c = &h[(size_t)t * kCntSlots];
+    mshbm_level_trace& o = trace[t];
+    memset(&o, 0, sizeof o);
+    o.level = k;
+    o.height = l.h;
+    o.width = l.w;
+    o.d_max = l.d;
+    o.block = l.b;
+    const int64_t N = (int64_t)l.h * l.w;
+    if (k == p.K) {
+      o.full_search_pixels = N;
+      o.selection_evals = N * (l.d + 1);
+    } else {
+      o.trusted = (int64_t)c[kCntTrusted];
+      o.trusted_evals = (int64_t)c[kCntTrustedEvals];
+      o.trusted_window_max = (int64_t)c[kCntWindowMax];
+      o.full_search_pixels = N - o.trusted;
+      o.selection_evals = o.trusted_evals + o.full_search_pixels * (l.d + 1);
+    }
+    o.refined = (int64_t)c[kCntRefined];
+    o.refine_evals = o.refined > 0 ? (int64_t)c[kCntNeeded] * (l.d + 1) : 0;
+    o.median_replaced = (int64_t)c[kCntMedianReplaced];
+    if (tev && !tev->empty()) {
+      StageEvents& e = (*tev)[t];
+      float ms = 0.f;
+      if (k < p.K) {
+        cudaEventElapsedTime(&ms, e.up0, e.up1);
+        o.ms_upsample = ms;
+      }
+      cudaEventElapsedTime(&ms, e.sel0, e.sel1);
+      o.ms_select = ms;
+      o.ms_refine = 0.f;   // fused into the sweep (reported under select)
+      cudaEventElapsedTime(&ms, e.med0, e.med1);
+      o.ms_median = ms;
+    }
+  }
+  return MSHBM_OK;
+}
+
+void destroy_events(std::vector<StageEvents>& tev) {
+  for (auto& e : tev) {
+    cudaEvent_t* ev = &e.up0;
+    for (int t = 0; t < 6; ++t) cudaEventDestroy(ev[t]);
+  }
+  tev.clear();
+}
+
+// inputs (optional) -> plan -> outputs (+ trace).  Host I/O synchronises.
+int run_plan_io(mshbm_ctx* ctx, Plan* p, const float* left, const float* right, int64_t ld,
+                int16_t* disparity, float* cost, int64_t ld_out, mshbm_level_trace* trace,
+                int32_t io, int32_t flags, cudaStream_t s) {
+  const bool host = io == MSHBM_IO_HOST;
+  const cudaMemcpyKind kin = host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
+  const cudaMemcpyKind kout = host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+  if (left) {
+    CK(cudaMemcpy2DAsync(p->in_l, p->ld_in * 4, left, ld * 4, (size_t)p->W * 4, p->H, kin, s));
+    CK(cudaMemcpy2DAsync(p->in_r, p->ld_in * 4, right, ld * 4, (size_t)p->W * 4, p->H, kin, s));
+  }
+  std::vector<StageEvents> tev;
+  const bool timing = trace && (flags & MSHBM_FLAG_TIMING);
+  int st = launch_plan(ctx, *p, s, flags, timing ? &tev : nullptr);
+  if (st) {
+    destroy_events(tev);
+    return st;
+  }
+  const LevelBuf& l0 = p->lv[0];
+  if (disparity)
+    CK(cudaMemcpy2DAsync(disparity, ld_out * 2, l0.dmed, l0.ld * 2, (size_t)l0.w * 2, l0.h, kout, s));
+  if (cost)
+    CK(cudaMemcpy2DAsync(cost, ld_out * 4, l0.c, l0.ld * 4, (size_t)l0.w * 4, l0.h, kout, s));
+  if (trace) st = finish_trace(ctx, *p, s, trace, &tev);
+  else if (host) {
+    CK(cudaStreamSynchronize(s));
+  }
+  destroy_events(tev);
+  return st;
+}
+
+}  // namespace
+
+// ======================================================================= C ABI
+extern "C" {
+
+int mshbm_abi_version(void) { return MSHBM_ABI_VERSION; }
+
+const char* mshbm_status_string(int s) {
+  switch (s) {
+    case MSHBM_OK: return "ok";
+    case MSHBM_ERR_VALUE: return "value error";
+    case MSHBM_ERR_CONFIG: return "config error";
+    case MSHBM_ERR_CUDA: return "cuda error";
+    case MSHBM_ERR_NOMEM: return "out of memory";
+    case MSHBM_ERR_UNSUPPORTED: return "unsupported";
+    default: return "unknown";
+  }
+}
+
+const char* mshbm_last_error(const mshbm_ctx* ctx) {
+  return ctx ? ctx->err.c_str() : g_err.c_str();
+}
+
+int mshbm_create(mshbm_ctx** out, int device) {
+  mshbm_ctx* ctx = nullptr;
+  if (!out) return fail(nullptr, MSHBM_ERR_VALUE, "null out pointer");
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0)
+    return fail(nullptr, MSHBM_ERR_CUDA, std::string("no CUDA device: ") + cudaGetErrorString(e));
+  if (device < 0 || device >= n) return fail(nullptr, MSHBM_ERR_VALUE, "bad device index");
+  CK(cudaSetDevice(device));
+  ctx = new mshbm_ctx();
+  ctx->device = device;
+  if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) {
+    delete ctx;
+    return fail(nullptr, MSHBM_ERR_CUDA, "stream create failed");
+  }
+  *out = ctx;
+  return MSHBM_OK;
+}
+
+int mshbm_destroy(mshbm_ctx* ctx) {
+  if (!ctx) return MSHBM_OK;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  for (auto& kv : ctx->plans) {
+    if (kv.second->exec) cudaGraphExecDestroy(kv.second->exec);
+    cudaFree(kv.second->arena);
+    delete kv.second;
+  }
+  cudaStreamDestroy(ctx->stream);
+  delete ctx;
+  return MSHBM_OK;
+}
+
+int64_t mshbm_launch_count(const mshbm_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int32_t mshbm_level_d_max(int32_t d_max, int32_t k) {
+  const int32_t v = d_max >> k;
+  return v > 1 ? v : 1;
+}
+
+int32_t mshbm_level_block(int32_t base_block, int32_t k) {
+  int32_t b = base_block >> k;
+  if (b % 2 == 0) b -= 1;
+  return b > 3 ? b : 3;
+}
+
+int mshbm_auto_levels(int64_t width, int64_t height, int64_t d_max, int64_t base_block,
+                      int32_t* out_levels) {
+  mshbm_ctx* ctx = nullptr;
+  if (std::min(width, height) <= 0 || d_max < 1 || base_block < 1)
+    return fail(ctx, MSHBM_ERR_VALUE, "width, height, d_max and base_block must be positive");
+  int k = 0;
+  while ((double)std::min(width, height) / std::ldexp(1.0, k + 1) >= 4.0 * (double)base_block &&
+         (d_max >> (k + 1)) >= 2)
+    ++k;
+  *out_levels = k;
+  return MSHBM_OK;
+}
+
+int mshbm_resolve_levels(const mshbm_config* cfg, int32_t height, int32_t width,
+                         int32_t* out_levels) {
+  mshbm_ctx* ctx = nullptr;
+  int st = validate_config(nullptr, cfg);
+  if (st) return st;
+  if (height < 1 || width < 1) return fail(ctx, MSHBM_ERR_VALUE, "empty image");
+  int32_t K = cfg->levels;
+  if (K < 0) {
+    st = mshbm_auto_levels(width, height, cfg->d_max, cfg->block, &K);
+    if (st) return st;
+  }
+  if (K > 0) {
+    int h = height, w = width;
+    for (int t = 0; t < K; ++t) h = (h + 1) / 2, w = (w + 1) / 2;
+    char buf[200];
+    if (std::min(h, w) < 2 * mshbm_level_block(cfg->block, K)) {
+      snprintf(buf, sizeof buf,
+               "%d levels leave a %dx%d coarsest image, smaller than twice its %d-pixel block",
+               K, h, w, mshbm_level_block(cfg->block, K));
+      return fail(ctx, MSHBM_ERR_VALUE, buf);
+    }
+    if ((cfg->d_max >> K) < 2) {
+      snprintf(buf, sizeof buf, "%d levels shrink the disparity range below 2 (d_max=%d)", K,
+               cfg->d_max);
+      return fail(ctx, MSHBM_ERR_VALUE, buf);
+    }
+  }
+  *out_levels = K;
+  return MSHBM_OK;
+}
+
+int mshbm_downsample(mshbm_ctx* ctx, const double* in, int32_t h, int32_t w, int64_t ld_in,
+                     double* out, int64_t ld_out, void* stream) {
+  if (!ctx) return fail(nullptr, MSHBM_ERR_VALUE, "null context");
+  if (h < 2 || w < 2) return fail(ctx, MSHBM_ERR_VALUE, "cannot downsample image smaller than 2x2");
+  CK(cudaSetDevice(ctx->device));
+  CK(launch_downsample(in, nullptr, h, w, ld_in, out, nullptr, ld_out, pick(ctx, stream)));
+  ctx->launches += 1;
+  return MSHBM_OK;
+}
+
+int mshbm_run_pipeline(mshbm_ctx* ctx, const float* left, const float* right, int32_t height,
+                       int32_t width, int64_t ld, const mshbm_config* cfg, int16_t* disparity,
+                       float* cost, int64_t ld_out, mshbm_level_trace* trace,
+                       int32_t* out_levels, int32_t io, int32_t flags, void* stream) {
+  if (!ctx) return fail(nullptr, MSHBM_ERR_VALUE, "null context");
+  if (!left || !right) return fail(ctx, MSHBM_ERR_VALUE, "null image pointer");
+  if (ld < width || ld_out < width) return fail(ctx, MSHBM_ERR_VALUE, "row stride < width");
+  int K = 0;
+  int st = mshbm_resolve_levels(cfg, height, width, &K);
+  if (st) return fail(ctx, st, g_err);
+  if (out_levels) *out_levels = K;
+  CK(cudaSetDevice(ctx->device));
+  std::vector<std::tuple<int, int, int, int>> dims;
+  int h = height, w = width;
+  for (int k = 0; k <= K; ++k) {
+    const int b = mshbm_level_block(cfg->block, k);
+    if (!sweep_supported_block(b)) return fail(ctx, MSHBM_ERR_UNSUPPORTED, "block larger than 63");
+    dims.emplace_back(h, w, mshbm_level_d_max(cfg->d_max, k), b);
+    h = (h + 1) / 2;
+    w = (w + 1) / 2;
+  }
+  PlanKey key{height, width, K, 0, cfg->d_max, cfg->block, cfg->radius, cfg->sign,
+              cfg->alpha, cfg->beta, cfg->sigma_eps, {}};
+  Plan* p = get_plan(ctx, key, *cfg, dims, &st);
+  if (!p) return st;
+  cudaStream_t s = pick(ctx, stream);
+  return run_plan_io(ctx, p, left, right, ld, disparity, cost, ld_out, trace, io, flags, s);
+}
+
+int mshbm_run_pyramid(mshbm_ctx* ctx, int32_t n_levels, const double* const* lefts,
+                      const double* const* rights, const int32_t* heights,
+                      const int32_t* widths, const int64_t* lds, const int32_t* d_maxs,
+                      const int32_t* blocks, const mshbm_config* cfg, int16_t* disparity,
+                      float* cost, int64_t ld_out, mshbm_level_trace* trace, void* stream) {
+  if (!ctx) return fail(nullptr, MSHBM_ERR_VALUE, "null context");
+  int st = validate_config(ctx, cfg);
+  if (st) return st;
+  if (n_levels < 1) return fail(ctx, MSHBM_ERR_VALUE, "empty pyramid");
+  CK(cudaSetDevice(ctx->device));
+  std::vector<std::tuple<int, int, int, int>> dims;
+  std::vector<int> flat;
+  for (int k = 0; k < n_levels; ++k) {
+    if (heights[k] < 1 || widths[k] < 1) return fail(ctx, MSHBM_ERR_VALUE, "empty level");
+    if (blocks[k] < 3 || blocks[k] % 2 == 0 || !sweep_supported_block(blocks[k]))
+      return fail(ctx, MSHBM_ERR_VALUE, "block must be odd, >= 3 and <= 63");
+    if (d_maxs[k] < 0) return fail(ctx, MSHBM_ERR_VALUE, "d_max must be >= 0");
+    if (k > 0 && (heights[k] != (heights[k - 1] + 1) / 2 || widths[k] != (widths[k - 1] + 1) / 2))
+      return fail(ctx, MSHBM_ERR_VALUE, "pyramid levels are not dyadic");
+    dims.emplace_back(heights[k], widths[k], d_maxs[k], blocks[k]);
+    flat.insert(flat.end(), {heights[k], widths[k], d_maxs[k], blocks[k]});
+  }
+  PlanKey key{heights[0], widths[0], n_levels - 1, 1, cfg->d_max, cfg->block, cfg->radius,
+              cfg->sign, cfg->alpha, cfg->beta, cfg->sigma_eps, flat};
+  Plan* p = get_plan(ctx, key, *cfg, dims, &st);
+  if (!p) return st;
+  cudaStream_t s = pick(ctx, stream);
+  for (int k = 0; k < n_levels; ++k) {
+    LevelBuf& l = p->lv[k];
+    CK(cudaMemcpy2DAsync(l.L, l.ld * 8, lefts[k], lds[k] * 8, (size_t)l.w * 8, l.h,
+                         cudaMemcpyDeviceToDevice, s));
+    CK(cudaMemcpy2DAsync(l.R, l.ld * 8, rights[k], lds[k] * 8, (size_t)l.w * 8, l.h,
+                         cudaMemcpyDeviceToDevice, s));
+  }
+  return run_plan_io(ctx, p, nullptr, nullptr, 0, disparity, cost, ld_out, trace,
+                     MSHBM_IO_DEVICE, 0, s);
+}
+
+// ------------------------------------------------------------------ engine
+int mshbm_engine_create(mshbm_ctx* ctx, const double* left, const double* right, int32_t height,
+                        int32_t width, int64_t ld, int32_t block, int32_t d_max, double sigma_eps,
+                        int32_t sign, mshbm_engine** out) {
+  if (!ctx || !out) return fail(ctx, MSHBM_ERR_VALUE, "null argument");
+  if (height < 1 || width < 1) return fail(ctx, MSHBM_ERR_VALUE, "empty image");
+  if (block < 3 || block % 2 == 0)
+    return fail(ctx, MSHBM_ERR_VALUE, "block must be odd and >= 3, got " + std::to_string(block));
+  if (!sweep_supported_block(block)) return fail(ctx, MSHBM_ERR_UNSUPPORTED, "block larger than 63");
+  if (d_max < 0) return fail(ctx, MSHBM_ERR_VALUE, "d_max must be >= 0, got " + std::to_string(d_max));
+  if (sign != MSHBM_SIGN_MIDDLEBURY && sign != MSHBM_SIGN_PAPER)
+    return fail(ctx, MSHBM_ERR_VALUE, "unknown sign convention");
+  CK(cudaSetDevice(ctx->device));
+  mshbm_engine* e = new mshbm_engine();
+  e->ctx = ctx;
+  e->H = height; e->W = width; e->d = d_max; e->b = block;
+  e->dir = sign == MSHBM_SIGN_PAPER ? -1 : 1;
+  e->eps = sigma_eps;
+  e->ld = round_up(width, 32);
+  const size_t n = (size_t)e->ld * height, nd = (size_t)height * width;
+  Carver cv;
+  for (int pass = 0; pass < 2; ++pass) {
+    cv.off = 0;
+    e->L = cv.take<double>(n); e->R = cv.take<double>(n);
+    e->muL = cv.take<double>(nd); e->sgL = cv.take<double>(nd);
+    e->muR = cv.take<double>(nd); e->sgR = cv.take<double>(nd);
+    e->muR32 = cv.take<float>(n); e->isR32 = cv.take<float>(n);
+    e->wc = cv.take<int>(n);
+    e->fz = cv.take<int16_t>(nd); e->wz = cv.take<int16_t>(nd); e->nz = cv.take<int16_t>(nd);
+    e->fc = cv.take<float>(nd); e->wcst = cv.take<float>(nd); e->nc = cv.take<float>(nd);
+    e->counters = cv.take<unsigned long long>(kCntSlots);
+    e->bad = cv.take<int>(1);
+    if (pass == 0) {
+      if (cudaMalloc(&e->arena, cv.off + 256) != cudaSuccess) {
+        delete e;
+        return fail(ctx, MSHBM_ERR_NOMEM, "engine allocation failed");
+      }
+      cv.base = (char*)e->arena;
+    }
+  }
+  cudaStream_t s = ctx->stream;
+  CK(cudaMemcpy2DAsync(e->L, e->ld * 8, left, ld * 8, (size_t)width * 8, height, cudaMemcpyDeviceToDevice, s));
+  CK(cudaMemcpy2DAsync(e->R, e->ld * 8, right, ld * 8, (size_t)width * 8, height, cudaMemcpyDeviceToDevice, s));
+  CK(launch_stats_f64(e->L, height, width, e->ld, block, e->muL, e->sgL, s));
+  CK(launch_stats_f64(e->R, height, width, e->ld, block, e->muR, e->sgR, s));
+  CK(launch_stats_f32(e->R, height, width, e->ld, block, sigma_eps, e->muR32, e->isR32, e->ld, s));
+  ctx->launches += 3;
+  CK(cudaStreamSynchronize(s));
+  *out = e;
+  return MSHBM_OK;
+}
+
+int mshbm_engine_destroy(mshbm_engine* e) {
+  if (!e) return MSHBM_OK;
+  cudaSetDevice(e->ctx->device);
+  cudaStreamSynchronize(e->ctx->stream);
+  cudaFree(e->arena);
+  delete e;
+  return MSHBM_OK;
+}
+
+static EngineView view(const mshbm_engine* e) {
+  EngineView v;
+  v.L = e->L; v.R = e->R; v.ld = e->ld;
+  v.muL = e->muL; v.sgL = e->sgL; v.muR = e->muR; v.sgR = e->sgR;
+  v.H = e->H; v.W = e->W; v.d = e->d; v.block = e->b; v.dir = e->dir;
+  v.sigma_eps = e->eps;
+  return v;
+}
+
+int mshbm_engine_stats(mshbm_engine* e, double* mean_l, double* sigma_l, double* mean_r,
+                       double* sigma_r, void* stream) {
+  mshbm_ctx* ctx = e ? e->ctx : nullptr;
+  if (!e) return fail(nullptr, MSHBM_ERR_VALUE, "null engine");
+  cudaStream_t s = pick(ctx, stream);
+  const size_t bytes = (size_t)e->H * e->W * 8;
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (mean_l) CK(cudaMemcpyAsync(mean_l, e->muL, bytes, cudaMemcpyDeviceToDevice, s));
+  if (sigma_l) CK(cudaMemcpyAsync(sigma_l, e->sgL, bytes, cudaMemcpyDeviceToDevice, s));
+  if (mean_r) CK(cudaMemcpyAsync(mean_r, e->muR, bytes, cudaMemcpyDeviceToDevice, s));
+  if (sigma_r) CK(cudaMemcpyAsync(sigma_r, e->sgR, bytes, cudaMemcpyDeviceToDevice, s));
+  return MSHBM_OK;
+}
+
+int mshbm_engine_plane(mshbm_engine* e, int32_t z, double* out, void* stream) {
+  mshbm_ctx* ctx = e ? e->ctx : nullptr;
+  if (!e) return fail(nullptr, MSHBM_ERR_VALUE, "null engine");
+  if (z < 0 || z > e->d)
+    return fail(ctx, MSHBM_ERR_VALUE,
+                "disparity " + std::to_string(z) + " outside [0, " + std::to_string(e->d) + "]");
+  CK(cudaSetDevice(ctx->device));
+  CK(launch_engine_plane(view(e), z, out, pick(ctx, stream)));
+  ctx->launches += 1;
+  return MSHBM_OK;
+}
+
+int mshbm_engine_at(mshbm_engine* e, const int64_t* rows, const int64_t* cols, const int64_t* z,
+                    int64_t n, double* out, void* stream) {
+  mshbm_ctx* ctx = e ? e->ctx : nullptr;
+  if (!e) return fail(nullptr, MSHBM_ERR_VALUE, "null engine");
+  if (n <= 0) return MSHBM_OK;
+  CK(cudaSetDevice(ctx->device));
+  cudaStream_t s = pick(ctx, stream);
+  CK(cudaMemsetAsync(e->bad, 0, sizeof(int), s));
+  CK(launch_engine_at(view(e), rows, cols, z, n, out, e->bad, s));
+  ctx->launches += 1;
+  int bad = 0;
+  CK(cudaMemcpyAsync(&bad, e->bad, sizeof(int), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  if (bad) return fail(ctx, MSHBM_ERR_VALUE, "disparities outside [0, " + std::to_string(e->d) + "] or pixel outside the image");
+  return MSHBM_OK;
+}
+
+int mshbm_engine_dsi_rows(mshbm_engine* e, const int64_t* rows, const int64_t* cols, int64_t n,
+                          double* out, void* stream) {
+  mshbm_ctx* ctx = e ? e->ctx : nullptr;
+  if (!e) return fail(nullptr, MSHBM_ERR_VALUE, "null engine");
+  if (n <= 0) return MSHBM_OK;
+  CK(cudaSetDevice(ctx->device));
+  cudaStream_t s = pick(ctx, stream);
+  CK(cudaMemsetAsync(e->bad, 0, sizeof(int), s));
+  CK(launch_engine_dsi(view(e), rows, cols, n, out, e->bad, s));
+  ctx->launches += 1;
+  int bad = 0;
+  CK(cudaMemcpyAsync(&bad, e->bad, sizeof(int), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  if (bad) return fail(ctx, MSHBM_ERR_VALUE, "pixel outside the image");
+  return MSHBM_OK;
+}
+
+static SweepArgs raw_args(mshbm_engine* e, const int* wc, int radius) {
+  SweepArgs a{};
+  a.L = e->L; a.R = e->R; a.ld = e->ld;
+  a.muR = e->muR32; a.isR = e->isR32; a.lds = e->ld;
+  a.H = e->H; a.W = e->W; a.d = e->d; a.block = e->b; a.dir = e->dir;
+  a.sigma_eps = e->eps;
+  a.wc = wc; a.ldw = e->W; a.radius = radius;
+  a.alpha = 0.5; a.mode = kSweepRaw;
+  a.fz = e->fz; a.fc = e->fc; a.wz = e->wz; a.wcst = e->wcst; a.nz = e->nz; a.nc = e->nc;
+  return a;
+}
+
+int mshbm_match_coarsest(mshbm_engine* e, double* disparity, double* cost, void* stream) {
+  mshbm_ctx* ctx = e ? e->ctx : nullptr;
+  if (!e) return fail(nullptr, MSHBM_ERR_VALUE, "null engine");
+  CK(cudaSetDevice(ctx->device));
+  cudaStream_t s = pick(ctx, stream);
+  int n = 0;
+  CK(launch_sweep(raw_args(e, nullptr, 0), s, &n));
+  CK(launch_combine_select(nullptr, e->H, e->W, e->fz, e->fc, e->wz, e->wcst, disparity, cost, s));
+  ctx->launches += n + 1;
+  return MSHBM_OK;
+}
+
+int mshbm_select_with_prior(mshbm_engine* e, const double* d_hat, const double* c_hat, double beta,
+                            int32_t radius, double* disparity, double* cost, int64_t* stats,
+                            void* stream) {
+  mshbm_ctx* ctx = e ? e->ctx : nullptr;
+  if (!e) return fail(nullptr, MSHBM_ERR_VALUE, "null engine");
+  if (radius < 0) return fail(ctx, MSHBM_ERR_VALUE, "radius must be >= 0");
+  CK(cudaSetDevice(ctx->device));
+  cudaStream_t s = pick(ctx, stream);
+  CK(cudaMemsetAsync(e->counters, 0, kCntSlots * 8, s));
+  CK(launch_prior_maps(d_hat, c_hat, e->H, e->W, e->d, radius, beta, e->wc, e->W, e->counters, s));
+  int n = 1;
+  CK(launch_sweep(raw_args(e, e->wc, radius), s, &n));
+  CK(launch_combine_select(e->wc, e->H, e->W, e->fz, e->fc, e->wz, e->wcst, disparity, cost, s));
+  ctx->launches += n + 1;
+  unsigned long long h[kCntSlots];
+  CK(cudaMemcpyAsync(h, e->counters, sizeof h, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  const int64_t N = (int64_t)e->H * e->W;
+  if (stats) {
+    stats[0] = (int64_t)h[kCntTrusted];
+    stats[1] = (int64_t)h[kCntTrustedEvals];
+    stats[2] = (int64_t)h[kCntWindowMax];
+    stats[3] = N - stats[0];
+    stats[4] = stats[1] + stats[3] * (e->d + 1);
+  }
+  return MSHBM_OK;
+}
+
+int mshbm_refine_level(mshbm_engine* e, const double* disparity, const double* cost, double alpha,
+                       double* out_disparity, double* out_cost, int64_t* evals, void* stream) {
+  mshbm_ctx* ctx = e ? e->ctx : nullptr;
+  if (!e) return fail(nullptr, MSHBM_ERR_VALUE, "null engine");
+  CK(cudaSetDevice(ctx->device));
+  cudaStream_t s = pick(ctx, stream);
+  CK(cudaMemsetAsync(e->counters, 0, kCntSlots * 8, s));
+  int n = 0;
+  CK(launch_sweep(raw_args(e, nullptr, 0), s, &n));
+  CK(launch_combine_refine(disparity, cost, e->H, e->W, alpha, e->nz, e->nc, out_disparity,
+                           out_cost, e->counters, s));
+  ctx->launches += n + 1;
+  unsigned long long h[kCntSlots];
+  CK(cudaMemcpyAsync(h, e->counters, sizeof h, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  if (evals) *evals = h[kCntRefined] > 0 ? (int64_t)h[kCntNeeded] * (e->d + 1) : 0;
+  return MSHBM_OK;
+}
+
+int mshbm_selective_median(mshbm_ctx* ctx, const double* disparity, const double* cost,
+                           int32_t height, int32_t width, double alpha, double* out,
+                           int64_t* replaced, void* stream) {
+  if (!ctx) return fail(nullptr, MSHBM_ERR_VALUE, "null context");
+  if (height < 1 || width < 1) return MSHBM_OK;
+  CK(cudaSetDevice(ctx->device));
+  cudaStream_t s = pick(ctx, stream);
+  unsigned long long* cnt = nullptr;
+  CK(cudaMallocAsync((void**)&cnt, 8, s));
+  CK(cudaMemsetAsync(cnt, 0, 8, s));
+  CK(launch_median_f64(disparity, cost, height, width, alpha, out, cnt, s));
+  ctx->launches += 1;
+  unsigned long long h = 0;
+  CK(cudaMemcpyAsync(&h, cnt, 8, cudaMemcpyDeviceToHost, s));
+  CK(cudaFreeAsync(cnt, s));
+  CK(cudaStreamSynchronize(s));
+  if (replaced) *replaced = (int64_t)h;
+  return MSHBM_OK;
+}
+
+int mshbm_upsample_prior(mshbm_ctx* ctx, const double* d_coarse, const double* c_coarse,
+                         int32_t ch, int32_t cw, int32_t h, int32_t w, double* d_hat,
+                         double* c_hat, void* stream) {
+  if (!ctx) return fail(nullptr, MSHBM_ERR_VALUE, "null context");
+  if (ch != (h + 1) / 2 || cw != (w + 1) / 2 || ch < 1 || cw < 1) {
+    char buf[160];
+    snprintf(buf, sizeof buf, "%dx%d maps cannot upsample to %dx%d: not the dyadic parent", ch, cw,
+             h, w);
+    return fail(ctx, MSHBM_ERR_VALUE, buf);
+  }
+  CK(cudaSetDevice(ctx->device));
+  cudaStream_t s = pick(ctx, stream);
+  const int64_t ldc = round_up(cw + 24, 32);
+  double* coef = nullptr;
+  CK(cudaMallocAsync((void**)&coef, (size_t)ldc * (ch + 24) * 8 * 2, s));
+  CK(launch_bspline_prefilter(nullptr, c_coarse, ch, cw, cw, coef, ldc, s));
+  CK(launch_upsample(d_coarse, ch, cw, coef, ldc, h, w, d_hat, c_hat, s));
+  ctx->launches += 6;
+  CK(cudaFreeAsync(coef, s));
+  return MSHBM_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,53 @@
+// Shared device helpers for libmshbm (sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#define MSHBM_DEV __device__ __forceinline__
+
+namespace mshbm {
+
+constexpr int kWcNone = -2147483647 - 1;   // "untrusted" window centre
+
+MSHBM_DEV int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
+
+// Warp-wide sum of a 64-bit counter.
+MSHBM_DEV unsigned long long warp_sum_u64(unsigned long long v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+MSHBM_DEV long long warp_max_i64(long long v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    long long w = __shfl_xor_sync(0xffffffffu, v, o);
+    v = w > v ? w : v;
+  }
+  return v;
+}
+
+// Block-aggregated atomic add: one atomic per warp (lane 0).
+MSHBM_DEV void warp_atomic_add(unsigned long long* dst, unsigned long long v) {
+  v = warp_sum_u64(v);
+  if ((threadIdx.x & 31) == 0 && v) atomicAdd(dst, v);
+}
+
+MSHBM_DEV void warp_atomic_max(long long* dst, long long v) {
+  v = warp_max_i64(v);
+  if ((threadIdx.x & 31) == 0 && v > 0) atomicMax((long long*)dst, v);
+}
+
+// Per-level device counters (int64), see mshbm_level_trace.
+enum CounterSlot {
+  kCntTrusted = 0,
+  kCntTrustedEvals = 1,
+  kCntWindowMax = 2,
+  kCntRefined = 3,
+  kCntNeeded = 4,
+  kCntMedianReplaced = 5,
+  kCntSlots = 8
+};
+
+}  // namespace mshbm

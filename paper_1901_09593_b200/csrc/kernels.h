@@ -1,0 +1,122 @@
+// Internal launcher interface between api.cu and the kernel translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace mshbm {
+
+// ---------------------------------------------------------------- sweep
+// Dense fused ZNCC z-sweep for one level (SURVEY §7 K3a/K3b/K3c fused):
+// every pixel x every z in [0, d], three register-resident winner-take-all
+// states (full range, +-r prior window, 3x3-summed cost), then the
+// reference's selection/refinement gates in the epilogue.
+enum SweepMode { kSweepPipeline = 0, kSweepRaw = 1 };
+
+struct SweepArgs {
+  const double* L;      // level images, float64, row stride ld
+  const double* R;
+  int64_t ld;
+  const float* muR;     // box mean of R (fp32)
+  const float* isR;     // 1/sigma_R, 0 where degenerate (fp32)
+  int64_t lds;
+  int H, W, d, block, dir;   // dir: +1 middlebury (q = j - z), -1 paper
+  double sigma_eps;
+  const int* wc;        // window centre per pixel or kWcNone; nullptr = none
+  int64_t ldw;
+  int radius;
+  double alpha;
+  int mode;
+  // pipeline outputs (stride ldo)
+  int16_t* dout;
+  float* cout;
+  uint8_t* low;
+  int64_t ldo;
+  unsigned long long* counters;
+  // raw outputs (dense H x W): full, window, 3x3-summed winners
+  int16_t* fz; float* fc; int16_t* wz; float* wcst; int16_t* nz; float* nc;
+};
+cudaError_t launch_sweep(const SweepArgs& a, cudaStream_t s, int* n_launch);
+bool sweep_supported_block(int b);
+
+// ---------------------------------------------------------------- pyramid
+cudaError_t launch_f32_to_f64(const float* a, const float* b, int h, int w,
+                              int64_t ld_in, double* oa, double* ob,
+                              int64_t ld_out, cudaStream_t s);
+// two images at once when in1/out1 are non-null
+cudaError_t launch_downsample(const double* in0, const double* in1, int h,
+                              int w, int64_t ld_in, double* out0, double* out1,
+                              int64_t ld_out, cudaStream_t s);
+
+// ---------------------------------------------------------------- stats
+// fp32 mean / inverse sigma (0 = degenerate) of the b x b replicate-padded
+// window, centred arithmetic in fp64.
+cudaError_t launch_stats_f32(const double* img, int h, int w, int64_t ld,
+                             int b, double sigma_eps, float* mu, float* is,
+                             int64_t lds, cudaStream_t s);
+// fp64 mean / sigma maps (dense) for the CostEngine API
+cudaError_t launch_stats_f64(const double* img, int h, int w, int64_t ld,
+                             int b, double* mu, double* sigma, cudaStream_t s);
+
+// ---------------------------------------------------------------- prior
+// cubic B-spline prefilter of a coarse cost map into coef
+// ((ch+24) x (cw+24), stride ldc); exactly one of c32 / c64 non-null.
+cudaError_t launch_bspline_prefilter(const float* c32, const double* c64,
+                                     int ch, int cw, int64_t ldcin,
+                                     double* coef, int64_t ldc, cudaStream_t s);
+// pipeline prior: window centres from the coarse disparity + spline coef
+cudaError_t launch_prior_eval(const int16_t* dcoarse, int64_t ldd, int ch,
+                              int cw, const double* coef, int64_t ldc, int h,
+                              int w, int d, int radius, double beta, int* wc,
+                              int64_t ldw, unsigned long long* counters,
+                              cudaStream_t s);
+// stage prior from explicit float64 (d_hat, c_hat) maps (dense h x w)
+cudaError_t launch_prior_maps(const double* d_hat, const double* c_hat, int h,
+                              int w, int d, int radius, double beta, int* wc,
+                              int64_t ldw, unsigned long long* counters,
+                              cudaStream_t s);
+// upsample_prior stage: d_hat = 2*NN(d), c_hat = clamp(spline)
+cudaError_t launch_upsample(const double* dcoarse, int ch, int cw,
+                            const double* coef, int64_t ldc, int h, int w,
+                            double* d_hat, double* c_hat, cudaStream_t s);
+
+// ---------------------------------------------------------------- median
+// pipeline: int16 d, fp32 c, low mask (selection) -> median d, counters
+cudaError_t launch_median_pipeline(const int16_t* d, const float* c,
+                                   const uint8_t* low, int64_t ld, int h,
+                                   int w, double alpha, int16_t* out,
+                                   unsigned long long* counters,
+                                   cudaStream_t s);
+// stage API: float64 dense maps, NaN-aware
+cudaError_t launch_median_f64(const double* d, const double* c, int h, int w,
+                              double alpha, double* out,
+                              unsigned long long* replaced, cudaStream_t s);
+
+// ---------------------------------------------------------------- engine
+struct EngineView {
+  const double* L; const double* R; int64_t ld;
+  const double* muL; const double* sgL; const double* muR; const double* sgR;
+  int H, W, d, block, dir;
+  double sigma_eps;
+};
+cudaError_t launch_engine_plane(const EngineView& e, int z, double* out,
+                                cudaStream_t s);
+cudaError_t launch_engine_at(const EngineView& e, const int64_t* rows,
+                             const int64_t* cols, const int64_t* z, int64_t n,
+                             double* out, int* bad, cudaStream_t s);
+cudaError_t launch_engine_dsi(const EngineView& e, const int64_t* rows,
+                              const int64_t* cols, int64_t n, double* out,
+                              int* bad, cudaStream_t s);
+// stage combine: select (trusted ? window : full) or refine (low ? nb : in)
+cudaError_t launch_combine_select(const int* wc, int h, int w,
+                                  const int16_t* fz, const float* fc,
+                                  const int16_t* wz, const float* wcst,
+                                  double* dout, double* cout, cudaStream_t s);
+cudaError_t launch_combine_refine(const double* din, const double* cin, int h,
+                                  int w, double alpha, const int16_t* nz,
+                                  const float* nc, double* dout, double* cout,
+                                  unsigned long long* counters, cudaStream_t s);
+cudaError_t launch_low_mask(const double* c, int h, int w, double alpha,
+                            int* wc_out, cudaStream_t s);
+
+}  // namespace mshbm

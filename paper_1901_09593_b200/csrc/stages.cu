@@ -1,0 +1,696 @@
+// HBM-bound stage kernels: pyramid (K1), window statistics (K2), cubic
+// B-spline prior (K5), selective median (K4), and the CostEngine / stage-API
+// helpers (direct fp64 evaluation, gate combines).
+#include <math.h>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace mshbm {
+
+namespace {
+
+constexpr unsigned kFull = 0xffffffffu;
+
+inline dim3 grid2d(int w, int h, dim3 blk, int z = 1) {
+  return dim3((w + blk.x - 1) / blk.x, (h + blk.y - 1) / blk.y, z);
+}
+
+// ------------------------------------------------------------------ K1
+__global__ void f32_to_f64_kernel(const float* a, const float* b, int h, int w,
+                                  int64_t ldi, double* oa, double* ob,
+                                  int64_t ldo) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  const int y = blockIdx.y * blockDim.y + threadIdx.y;
+  if (x >= w || y >= h) return;
+  const float* src = blockIdx.z ? b : a;
+  double* dst = blockIdx.z ? ob : oa;
+  dst[(int64_t)y * ldo + x] = (double)src[(int64_t)y * ldi + x];
+}
+
+// gaussian_downsample (pyramid.py:65-81): (1,4,6,4,1)/16 along axis 0, then
+// axis 1, replicate borders, keep even rows/cols.  Only the kept samples are
+// computed: out(I,J) = sum_b k_b sum_a k_a X(2I+a-2, 2J+b-2) (clamped).
+__global__ void downsample_kernel(const double* in0, const double* in1, int h,
+                                  int w, int64_t ldi, double* out0,
+                                  double* out1, int64_t ldo, int oh, int ow) {
+  const int J = blockIdx.x * blockDim.x + threadIdx.x;
+  const int I = blockIdx.y * blockDim.y + threadIdx.y;
+  if (J >= ow || I >= oh) return;
+  const double* in = blockIdx.z ? in1 : in0;
+  double* out = blockIdx.z ? out1 : out0;
+  const double k[5] = {1.0 / 16.0, 4.0 / 16.0, 6.0 / 16.0, 4.0 / 16.0, 1.0 / 16.0};
+  int rows[5];
+#pragma unroll
+  for (int a = 0; a < 5; ++a) rows[a] = clampi(2 * I + a - 2, 0, h - 1);
+  double acc = 0.0;
+#pragma unroll
+  for (int b = 0; b < 5; ++b) {
+    const int col = clampi(2 * J + b - 2, 0, w - 1);
+    double v = 0.0;
+#pragma unroll
+    for (int a = 0; a < 5; ++a) v += k[a] * in[(int64_t)rows[a] * ldi + col];
+    acc += k[b] * v;
+  }
+  out[(int64_t)I * ldo + J] = acc;
+}
+
+// ------------------------------------------------------------------ K2
+// Box mean and centred sigma of the b x b replicate-padded window
+// (zncc.py:185-189 computes the same quantities via uniform_filter raw
+// moments; centred arithmetic keeps flat patches at sigma == 0 exactly).
+template <bool F64>
+__global__ void stats_kernel(const double* img, int h, int w, int64_t ld,
+                             int b, double sigma_eps, float* mu32, float* is32,
+                             double* mu64, double* sg64, int64_t lds) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  const int y = blockIdx.y * blockDim.y + threadIdx.y;
+  if (x >= w || y >= h) return;
+  const int h2 = b / 2;
+  double s = 0.0;
+  for (int r = 0; r < b; ++r) {
+    const double* row = img + (int64_t)clampi(y + r - h2, 0, h - 1) * ld;
+    for (int c = 0; c < b; ++c) s += row[clampi(x + c - h2, 0, w - 1)];
+  }
+  const double area = (double)(b * b);
+  const double mu = s / area;
+  double ss = 0.0;
+  for (int r = 0; r < b; ++r) {
+    const double* row = img + (int64_t)clampi(y + r - h2, 0, h - 1) * ld;
+    for (int c = 0; c < b; ++c) {
+      const double dv = row[clampi(x + c - h2, 0, w - 1)] - mu;
+      ss += dv * dv;
+    }
+  }
+  const double sigma = sqrt(ss / area);
+  if (F64) {
+    mu64[(int64_t)y * w + x] = mu;
+    sg64[(int64_t)y * w + x] = sigma;
+  } else {
+    mu32[(int64_t)y * lds + x] = (float)mu;
+    is32[(int64_t)y * lds + x] = sigma >= sigma_eps ? (float)(1.0 / sigma) : 0.f;
+  }
+}
+
+// ------------------------------------------------------------------ K5
+// scipy map_coordinates(order=3, mode='nearest') (matcher.py:259):
+// _prepad_for_spline_filter pads 12 samples by edge replication, then
+// spline_filter1d along axis 0 and axis 1 with the cubic pole
+// z = sqrt(3) - 2, gain (1-z)(1-1/z), 'reflect' causal/anticausal init.
+constexpr int kNpad = 12;
+
+__global__ void bspline_pad_kernel(const float* c32, const double* c64, int ch,
+                                   int cw, int64_t ldcin, double* coef,
+                                   int64_t ldc) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  const int y = blockIdx.y * blockDim.y + threadIdx.y;
+  const int nh = ch + 2 * kNpad, nw = cw + 2 * kNpad;
+  if (x >= nw || y >= nh) return;
+  const int64_t o = (int64_t)clampi(y - kNpad, 0, ch - 1) * ldcin + clampi(x - kNpad, 0, cw - 1);
+  coef[(int64_t)y * ldc + x] = c32 ? (double)c32[o] : c64[o];
+}
+
+// The IIR prefilter runs as parallel segments: each thread filters kSeg
+// samples of one line from a register window that also holds kWarm samples
+// of warm-up (|z|^32 ~ 5e-19, below fp64 resolution), so the result equals
+// scipy's sequential recursion to rounding.  All loads of the window are
+// independent and issued up front.  Segments touching a line end use
+// scipy's exact 'reflect' initialisation; lines of <= kWin samples run the
+// exact sequential recursion.
+constexpr double kPole = -0.26794919243112270;   // sqrt(3) - 2
+constexpr int kWarm = 32;
+constexpr int kSeg = 32;
+constexpr int kWin = kWarm + kSeg;
+
+__device__ __forceinline__ double line_at(const double* p, int64_t stride, int i) {
+  return p[(int64_t)i * stride];
+}
+
+// exact scipy recursion (gain, reflect init, causal, anticausal) of a line
+__device__ void spline_line_exact(const double* x, double* y, int n, int64_t stride, double g,
+                                  bool causal) {
+  const double z = kPole;
+  if (causal) {
+    const double zn = pow(z, (double)n);
+    const double c0 = g * x[0];
+    double acc = c0 + zn * g * line_at(x, stride, n - 1);
+    double zi = z;
+    for (int i = 1; i < n; ++i) {
+      acc += zi * (g * line_at(x, stride, i) + zn * g * line_at(x, stride, n - 1 - i));
+      zi *= z;
+    }
+    double prev = acc * (z / (1.0 - zn * zn)) + c0;
+    y[0] = prev;
+    for (int i = 1; i < n; ++i) {
+      prev = g * line_at(x, stride, i) + z * prev;
+      y[(int64_t)i * stride] = prev;
+    }
+  } else {
+    double prev = line_at(x, stride, n - 1) * (z / (z - 1.0));
+    y[(int64_t)(n - 1) * stride] = prev;
+    for (int i = n - 2; i >= 0; --i) {
+      prev = z * (prev - line_at(x, stride, i));
+      y[(int64_t)i * stride] = prev;
+    }
+  }
+}
+
+// causal pass: out[i] = g*in[i] + z*out[i-1]
+__global__ void __launch_bounds__(128) iir_causal_kernel(const double* __restrict__ in,
+                                                         double* __restrict__ out, int64_t ldc,
+                                                         int nh, int nw, int axis, double g) {
+  const int line = blockIdx.x * blockDim.x + threadIdx.x;
+  const int n = axis == 0 ? nh : nw;
+  const int nl = axis == 0 ? nw : nh;
+  if (line >= nl) return;
+  const int64_t stride = axis == 0 ? ldc : 1;
+  const int64_t base = axis == 0 ? line : (int64_t)line * ldc;
+  const double* x = in + base;
+  double* y = out + base;
+  if (n <= kWin) {
+    if (blockIdx.y == 0) spline_line_exact(x, y, n, stride, g, true);
+    return;
+  }
+  const int s = blockIdx.y * kSeg;
+  if (s >= n) return;
+  const int e = min(n, s + kSeg);
+  const int w0 = s - kWarm;              // window [w0, w0 + kWin), left-aligned
+  double v[kWin];
+#pragma unroll
+  for (int k = 0; k < kWin; ++k) {
+    const int idx = w0 + k;
+    v[k] = (idx >= 0 && idx < n) ? g * line_at(x, stride, idx) : 0.0;
+  }
+  const double z = kPole;
+  double acc;
+  if (w0 < 0) {
+    // s == 0: exact reflect init; n > kWin so z^n terms vanish (< 1e-36)
+    double sum = 0.0, zi = z;
+#pragma unroll
+    for (int k = kWarm + 1; k < kWin; ++k) {
+      sum += zi * v[k];
+      zi *= z;
+    }
+    acc = (v[kWarm] + sum) * z + v[kWarm];
+    y[0] = acc;
+  } else {
+    acc = v[0];
+  }
+#pragma unroll
+  for (int k = 1; k < kWin; ++k) {
+    const int idx = w0 + k;
+    if (w0 < 0 && k <= kWarm) continue;   // before the line start / the init sample
+    acc = v[k] + z * acc;
+    if (idx >= s && idx < e) y[(int64_t)idx * stride] = acc;
+  }
+}
+
+// anticausal pass: out[n-1] = in[n-1]*z/(z-1); out[i] = z*(out[i+1] - in[i])
+__global__ void __launch_bounds__(128) iir_anticausal_kernel(const double* __restrict__ in,
+                                                             double* __restrict__ out,
+                                                             int64_t ldc, int nh, int nw,
+                                                             int axis) {
+  const int line = blockIdx.x * blockDim.x + threadIdx.x;
+  const int n = axis == 0 ? nh : nw;
+  const int nl = axis == 0 ? nw : nh;
+  if (line >= nl) return;
+  const int64_t stride = axis == 0 ? ldc : 1;
+  const int64_t base = axis == 0 ? line : (int64_t)line * ldc;
+  const double* x = in + base;
+  double* y = out + base;
+  if (n <= kWin) {
+    if (blockIdx.y == 0) spline_line_exact(x, y, n, stride, 1.0, false);
+    return;
+  }
+  const int s = blockIdx.y * kSeg;
+  if (s >= n) return;
+  const int e = min(n, s + kSeg);
+  const int we = min(n, e + kWarm);      // window [we - kWin, we), right-aligned
+  const int w0 = we - kWin;
+  double v[kWin];
+#pragma unroll
+  for (int k = 0; k < kWin; ++k) {
+    const int idx = w0 + k;
+    v[k] = idx >= 0 ? line_at(x, stride, idx) : 0.0;
+  }
+  const double z = kPole;
+  double acc = we == n ? v[kWin - 1] * (z / (z - 1.0)) : -z * v[kWin - 1];
+  if (we - 1 < e) y[(int64_t)(we - 1) * stride] = acc;
+#pragma unroll
+  for (int k = kWin - 2; k >= 0; --k) {
+    const int idx = w0 + k;
+    acc = z * (acc - v[k]);
+    if (idx >= s && idx < e) y[(int64_t)idx * stride] = acc;
+  }
+}
+
+__device__ __forceinline__ void bspline_w(double t, double* wgt) {
+  const double u = 1.0 - t;
+  wgt[0] = u * u * u / 6.0;
+  wgt[1] = (4.0 - 6.0 * t * t + 3.0 * t * t * t) / 6.0;
+  wgt[2] = (1.0 + 3.0 * t + 3.0 * t * t - 3.0 * t * t * t) / 6.0;
+  wgt[3] = t * t * t / 6.0;
+}
+
+// spline value at fine pixel (i, j) of an h x w target from a ch x cw map
+__device__ double spline_at(const double* coef, int64_t ldc, int ch, int cw,
+                            int h, int w, int i, int j) {
+  const double y = ((double)i + 0.5) * ((double)ch / (double)h) - 0.5 + kNpad;
+  const double x = ((double)j + 0.5) * ((double)cw / (double)w) - 0.5 + kNpad;
+  const double fy = floor(y), fx = floor(x);
+  double wy[4], wx[4];
+  bspline_w(y - fy, wy);
+  bspline_w(x - fx, wx);
+  const int iy = (int)fy - 1, ix = (int)fx - 1;
+  const int nh = ch + 2 * kNpad, nw = cw + 2 * kNpad;
+  double out = 0.0;
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    const double* row = coef + (int64_t)clampi(iy + a, 0, nh - 1) * ldc;
+    double r = 0.0;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) r += wx[b] * row[clampi(ix + b, 0, nw - 1)];
+    out += wy[a] * r;
+  }
+  return out;
+}
+
+// Trace counters of select_with_prior (matcher.py:288-308, A.10):
+// trusted, sum of legal window sizes, max window size.
+__device__ __forceinline__ void count_trusted(bool trusted, int c, int r, int d,
+                                              unsigned long long* counters) {
+  long long ws = 0;
+  if (trusted) ws = (long long)(min(c + r, d) - max(c - r, 0) + 1);
+  const unsigned bal = __ballot_sync(kFull, trusted);
+  unsigned long long evals = warp_sum_u64((unsigned long long)ws);
+  long long wmax = warp_max_i64(ws);
+  if ((threadIdx.x & 31) == 0 && bal) {
+    atomicAdd(&counters[kCntTrusted], (unsigned long long)__popc(bal));
+    atomicAdd(&counters[kCntTrustedEvals], evals);
+    atomicMax((unsigned long long*)&counters[kCntWindowMax], (unsigned long long)wmax);
+  }
+}
+
+// upsample_prior + the trust gate of select_with_prior (matcher.py:236-260,
+// 276-281): d_hat = 2 d[i/2, j/2], c_hat = clamp(spline, -1, 1),
+// trusted = c_hat > beta and [c-r, c+r] intersects [0, d].
+__global__ void prior_eval_kernel(const int16_t* dco, int64_t ldd, int ch,
+                                  int cw, const double* coef, int64_t ldc,
+                                  int h, int w, int d, int r, double beta,
+                                  int* wc, int64_t ldw,
+                                  unsigned long long* counters) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  const int i = blockIdx.y * blockDim.y + threadIdx.y;
+  const bool in = i < h && j < w;
+  bool trusted = false;
+  int center = 0;
+  if (in) {
+    double chat = spline_at(coef, ldc, ch, cw, h, w, i, j);
+    chat = fmin(fmax(chat, -1.0), 1.0);
+    center = 2 * (int)dco[(int64_t)(i >> 1) * ldd + (j >> 1)];
+    const bool ok = (center + r >= 0) && (center - r <= d);
+    trusted = (chat > beta) && ok;
+    wc[(int64_t)i * ldw + j] = trusted ? center : kWcNone;
+  }
+  count_trusted(trusted, center, r, d, counters);
+}
+
+__global__ void prior_maps_kernel(const double* d_hat, const double* c_hat,
+                                  int h, int w, int d, int r, double beta,
+                                  int* wc, int64_t ldw,
+                                  unsigned long long* counters) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  const int i = blockIdx.y * blockDim.y + threadIdx.y;
+  const bool in = i < h && j < w;
+  bool trusted = false;
+  int center = 0;
+  if (in) {
+    const double dh = d_hat[(int64_t)i * w + j];
+    const bool finite = isfinite(dh);
+    const double cen = finite ? trunc(dh) : 0.0;     // astype(np.intp)
+    const bool ok = finite && (cen + r >= 0.0) && (cen - r <= (double)d);
+    trusted = (c_hat[(int64_t)i * w + j] > beta) && ok;
+    center = trusted ? (int)cen : 0;
+    wc[(int64_t)i * ldw + j] = trusted ? center : kWcNone;
+  }
+  count_trusted(trusted, center, r, d, counters);
+}
+
+__global__ void upsample_kernel(const double* dco, int ch, int cw,
+                                const double* coef, int64_t ldc, int h, int w,
+                                double* d_hat, double* c_hat) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  const int i = blockIdx.y * blockDim.y + threadIdx.y;
+  if (i >= h || j >= w) return;
+  const double c = spline_at(coef, ldc, ch, cw, h, w, i, j);
+  c_hat[(int64_t)i * w + j] = fmin(fmax(c, -1.0), 1.0);
+  d_hat[(int64_t)i * w + j] = 2.0 * dco[(int64_t)(i >> 1) * cw + (j >> 1)];
+}
+
+// ------------------------------------------------------------------ K4
+// selective_median (matcher.py:323-359): a pixel with C <= alpha takes the
+// lower median of the disparities in its clipped 5x5 window whose own
+// cost exceeds alpha (and are finite); none -> unchanged.
+template <typename T>
+__device__ __forceinline__ T lower_median(T* v, int n) {
+  const int m = (n - 1) >> 1;
+  T best = v[0];
+  for (int k = 0; k < n; ++k) {
+    int less = 0, leq = 0;
+    for (int t = 0; t < n; ++t) {
+      less += v[t] < v[k];
+      leq += v[t] <= v[k];
+    }
+    if (less <= m && m < leq) { best = v[k]; break; }
+  }
+  return best;
+}
+
+__global__ void median_pipeline_kernel(const int16_t* d, const float* c,
+                                       const uint8_t* low, int64_t ld, int h,
+                                       int w, double alpha, int16_t* out,
+                                       unsigned long long* counters) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  const int i = blockIdx.y * blockDim.y + threadIdx.y;
+  const bool in = i < h && j < w;
+  bool changed = false, needed = false;
+  if (in) {
+    const int64_t o = (int64_t)i * ld + j;
+    const int16_t d0 = d[o];
+    int16_t res = d0;
+    for (int di = -1; di <= 1; ++di)
+      for (int dj = -1; dj <= 1; ++dj) {
+        const int qi = i + di, qj = j + dj;
+        if (qi >= 0 && qi < h && qj >= 0 && qj < w && low[(int64_t)qi * ld + qj]) needed = true;
+      }
+    if ((double)c[o] <= alpha) {
+      int v[24];
+      int n = 0;
+      for (int di = -2; di <= 2; ++di) {
+        const int qi = i + di;
+        if (qi < 0 || qi >= h) continue;
+        for (int dj = -2; dj <= 2; ++dj) {
+          const int qj = j + dj;
+          if (qj < 0 || qj >= w) continue;
+          const int64_t q = (int64_t)qi * ld + qj;
+          if ((double)c[q] > alpha && n < 24) v[n++] = d[q];
+        }
+      }
+      if (n > 0) res = (int16_t)lower_median(v, n);
+    }
+    out[o] = res;
+    changed = res != d0;
+  }
+  const unsigned bc = __ballot_sync(kFull, changed);
+  const unsigned bn = __ballot_sync(kFull, needed);
+  if ((threadIdx.x & 31) == 0) {
+    if (bc) atomicAdd(&counters[kCntMedianReplaced], (unsigned long long)__popc(bc));
+    if (bn) atomicAdd(&counters[kCntNeeded], (unsigned long long)__popc(bn));
+  }
+}
+
+__global__ void median_f64_kernel(const double* d, const double* c, int h,
+                                  int w, double alpha, double* out,
+                                  unsigned long long* replaced) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  const int i = blockIdx.y * blockDim.y + threadIdx.y;
+  const bool in = i < h && j < w;
+  bool changed = false;
+  if (in) {
+    const int64_t o = (int64_t)i * w + j;
+    const double d0 = d[o];
+    double res = d0;
+    if (c[o] <= alpha) {
+      double v[25];
+      int n = 0;
+      for (int di = -2; di <= 2; ++di) {
+        const int qi = i + di;
+        if (qi < 0 || qi >= h) continue;
+        for (int dj = -2; dj <= 2; ++dj) {
+          const int qj = j + dj;
+          if (qj < 0 || qj >= w) continue;
+          const int64_t q = (int64_t)qi * w + qj;
+          if (c[q] > alpha && isfinite(d[q])) v[n++] = d[q];
+        }
+      }
+      if (n > 0) res = lower_median(v, n);
+    }
+    out[o] = res;
+    changed = !(isnan(d0) && isnan(res)) && (res != d0);
+  }
+  const unsigned bc = __ballot_sync(kFull, changed);
+  if ((threadIdx.x & 31) == 0 && bc && replaced)
+    atomicAdd(replaced, (unsigned long long)__popc(bc));
+}
+
+// ------------------------------------------------------------------ engine
+// CostEngine point evaluation (zncc.py:271-287) in fp64, centred.
+__device__ double engine_cost(const EngineView& e, int i, int j, int z) {
+  const int q = j - e.dir * z;
+  if (q < 0 || q > e.W - 1) return -1.0;
+  const int64_t pl = (int64_t)i * e.W + j, pr = (int64_t)i * e.W + q;
+  const double sl = e.sgL[pl], sr = e.sgR[pr];
+  if (!(sl >= e.sigma_eps) || !(sr >= e.sigma_eps)) return -1.0;
+  const double ml = e.muL[pl], mr = e.muR[pr];
+  const int h2 = e.block / 2;
+  double acc = 0.0;
+  for (int r = 0; r < e.block; ++r) {
+    const int64_t ro = (int64_t)clampi(i + r - h2, 0, e.H - 1) * e.ld;
+    for (int c = 0; c < e.block; ++c)
+      acc += (e.L[ro + clampi(j + c - h2, 0, e.W - 1)] - ml) *
+             (e.R[ro + clampi(q + c - h2, 0, e.W - 1)] - mr);
+  }
+  const double v = acc / ((double)(e.block * e.block) * sl * sr);
+  return fmin(fmax(v, -1.0), 1.0);
+}
+
+__global__ void engine_plane_kernel(const EngineView e, int z, double* out) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  const int i = blockIdx.y * blockDim.y + threadIdx.y;
+  if (i >= e.H || j >= e.W) return;
+  out[(int64_t)i * e.W + j] = engine_cost(e, i, j, z);
+}
+
+__global__ void engine_at_kernel(const EngineView e, const int64_t* rows,
+                                 const int64_t* cols, const int64_t* zs,
+                                 int64_t n, double* out, int* bad) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  const int64_t i = rows[t], j = cols[t], z = zs[t];
+  if (z < 0 || z > e.d || i < 0 || i >= e.H || j < 0 || j >= e.W) {
+    atomicExch(bad, 1);
+    out[t] = -1.0;
+    return;
+  }
+  out[t] = engine_cost(e, (int)i, (int)j, (int)z);
+}
+
+__global__ void engine_dsi_kernel(const EngineView e, const int64_t* rows,
+                                  const int64_t* cols, int64_t n, double* out,
+                                  int* bad) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t total = n * (int64_t)(e.d + 1);
+  if (t >= total) return;
+  const int64_t p = t / (e.d + 1);
+  const int z = (int)(t - p * (e.d + 1));
+  const int64_t i = rows[p], j = cols[p];
+  if (i < 0 || i >= e.H || j < 0 || j >= e.W) {
+    atomicExch(bad, 1);
+    out[t] = -1.0;
+    return;
+  }
+  out[t] = engine_cost(e, (int)i, (int)j, z);
+}
+
+__global__ void combine_select_kernel(const int* wc, int h, int w,
+                                      const int16_t* fz, const float* fc,
+                                      const int16_t* wz, const float* wcst,
+                                      double* dout, double* cout) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  const int i = blockIdx.y * blockDim.y + threadIdx.y;
+  if (i >= h || j >= w) return;
+  const int64_t o = (int64_t)i * w + j;
+  const bool trusted = wc != nullptr && wc[o] != kWcNone;
+  dout[o] = trusted ? (double)wz[o] : (double)fz[o];
+  cout[o] = trusted ? (double)wcst[o] : (double)fc[o];
+}
+
+__global__ void combine_refine_kernel(const double* din, const double* cin,
+                                      int h, int w, double alpha,
+                                      const int16_t* nz, const float* nc,
+                                      double* dout, double* cout,
+                                      unsigned long long* counters) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  const int i = blockIdx.y * blockDim.y + threadIdx.y;
+  const bool in = i < h && j < w;
+  bool low = false, needed = false;
+  if (in) {
+    const int64_t o = (int64_t)i * w + j;
+    low = cin[o] <= alpha;
+    for (int di = -1; di <= 1; ++di)
+      for (int dj = -1; dj <= 1; ++dj) {
+        const int qi = i + di, qj = j + dj;
+        if (qi >= 0 && qi < h && qj >= 0 && qj < w && cin[(int64_t)qi * w + qj] <= alpha)
+          needed = true;
+      }
+    dout[o] = low ? (double)nz[o] : din[o];
+    cout[o] = low ? (double)nc[o] : cin[o];
+  }
+  const unsigned bl = __ballot_sync(kFull, low);
+  const unsigned bn = __ballot_sync(kFull, needed);
+  if ((threadIdx.x & 31) == 0) {
+    if (bl) atomicAdd(&counters[kCntRefined], (unsigned long long)__popc(bl));
+    if (bn) atomicAdd(&counters[kCntNeeded], (unsigned long long)__popc(bn));
+  }
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ launchers
+cudaError_t launch_f32_to_f64(const float* a, const float* b, int h, int w,
+                              int64_t ld_in, double* oa, double* ob,
+                              int64_t ld_out, cudaStream_t s) {
+  dim3 blk(64, 4);
+  f32_to_f64_kernel<<<grid2d(w, h, blk, b ? 2 : 1), blk, 0, s>>>(a, b, h, w, ld_in, oa, ob, ld_out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_downsample(const double* in0, const double* in1, int h,
+                              int w, int64_t ld_in, double* out0, double* out1,
+                              int64_t ld_out, cudaStream_t s) {
+  const int oh = (h + 1) / 2, ow = (w + 1) / 2;
+  dim3 blk(32, 8);
+  downsample_kernel<<<grid2d(ow, oh, blk, in1 ? 2 : 1), blk, 0, s>>>(
+      in0, in1, h, w, ld_in, out0, out1, ld_out, oh, ow);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_stats_f32(const double* img, int h, int w, int64_t ld,
+                             int b, double sigma_eps, float* mu, float* is,
+                             int64_t lds, cudaStream_t s) {
+  dim3 blk(32, 8);
+  stats_kernel<false><<<grid2d(w, h, blk), blk, 0, s>>>(img, h, w, ld, b, sigma_eps,
+                                                         mu, is, nullptr, nullptr, lds);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_stats_f64(const double* img, int h, int w, int64_t ld,
+                             int b, double* mu, double* sigma, cudaStream_t s) {
+  dim3 blk(32, 8);
+  stats_kernel<true><<<grid2d(w, h, blk), blk, 0, s>>>(img, h, w, ld, b, 0.0, nullptr,
+                                                        nullptr, mu, sigma, 0);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_bspline_prefilter(const float* c32, const double* c64,
+                                     int ch, int cw, int64_t ldcin,
+                                     double* coef, int64_t ldc, cudaStream_t s) {
+  // coef holds two (ch+24) x ldc planes: the result and a ping-pong scratch
+  const int nh = ch + 2 * kNpad, nw = cw + 2 * kNpad;
+  double* tmp = coef + (int64_t)ldc * nh;
+  const double gain = (1.0 - kPole) * (1.0 - 1.0 / kPole);
+  dim3 blk(32, 8);
+  bspline_pad_kernel<<<grid2d(nw, nh, blk), blk, 0, s>>>(c32, c64, ch, cw, ldcin, coef, ldc);
+  const dim3 g0((nw + 127) / 128, nh <= kWin ? 1 : (nh + kSeg - 1) / kSeg);
+  const dim3 g1((nh + 127) / 128, nw <= kWin ? 1 : (nw + kSeg - 1) / kSeg);
+  iir_causal_kernel<<<g0, 128, 0, s>>>(coef, tmp, ldc, nh, nw, 0, gain);
+  iir_anticausal_kernel<<<g0, 128, 0, s>>>(tmp, coef, ldc, nh, nw, 0);
+  iir_causal_kernel<<<g1, 128, 0, s>>>(coef, tmp, ldc, nh, nw, 1, gain);
+  iir_anticausal_kernel<<<g1, 128, 0, s>>>(tmp, coef, ldc, nh, nw, 1);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_prior_eval(const int16_t* dcoarse, int64_t ldd, int ch,
+                              int cw, const double* coef, int64_t ldc, int h,
+                              int w, int d, int radius, double beta, int* wc,
+                              int64_t ldw, unsigned long long* counters,
+                              cudaStream_t s) {
+  dim3 blk(32, 8);
+  prior_eval_kernel<<<grid2d(w, h, blk), blk, 0, s>>>(dcoarse, ldd, ch, cw, coef, ldc, h, w,
+                                                       d, radius, beta, wc, ldw, counters);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_prior_maps(const double* d_hat, const double* c_hat, int h,
+                              int w, int d, int radius, double beta, int* wc,
+                              int64_t ldw, unsigned long long* counters,
+                              cudaStream_t s) {
+  dim3 blk(32, 8);
+  prior_maps_kernel<<<grid2d(w, h, blk), blk, 0, s>>>(d_hat, c_hat, h, w, d, radius, beta,
+                                                       wc, ldw, counters);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_upsample(const double* dcoarse, int ch, int cw,
+                            const double* coef, int64_t ldc, int h, int w,
+                            double* d_hat, double* c_hat, cudaStream_t s) {
+  dim3 blk(32, 8);
+  upsample_kernel<<<grid2d(w, h, blk), blk, 0, s>>>(dcoarse, ch, cw, coef, ldc, h, w, d_hat,
+                                                     c_hat);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_median_pipeline(const int16_t* d, const float* c,
+                                   const uint8_t* low, int64_t ld, int h,
+                                   int w, double alpha, int16_t* out,
+                                   unsigned long long* counters,
+                                   cudaStream_t s) {
+  dim3 blk(32, 8);
+  median_pipeline_kernel<<<grid2d(w, h, blk), blk, 0, s>>>(d, c, low, ld, h, w, alpha, out,
+                                                            counters);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_median_f64(const double* d, const double* c, int h, int w,
+                              double alpha, double* out,
+                              unsigned long long* replaced, cudaStream_t s) {
+  dim3 blk(32, 8);
+  median_f64_kernel<<<grid2d(w, h, blk), blk, 0, s>>>(d, c, h, w, alpha, out, replaced);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_engine_plane(const EngineView& e, int z, double* out,
+                                cudaStream_t s) {
+  dim3 blk(32, 8);
+  engine_plane_kernel<<<grid2d(e.W, e.H, blk), blk, 0, s>>>(e, z, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_engine_at(const EngineView& e, const int64_t* rows,
+                             const int64_t* cols, const int64_t* z, int64_t n,
+                             double* out, int* bad, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  engine_at_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(e, rows, cols, z, n, out, bad);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_engine_dsi(const EngineView& e, const int64_t* rows,
+                              const int64_t* cols, int64_t n, double* out,
+                              int* bad, cudaStream_t s) {
+  const int64_t total = n * (int64_t)(e.d + 1);
+  if (total <= 0) return cudaSuccess;
+  engine_dsi_kernel<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(e, rows, cols, n, out, bad);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_combine_select(const int* wc, int h, int w,
+                                  const int16_t* fz, const float* fc,
+                                  const int16_t* wz, const float* wcst,
+                                  double* dout, double* cout, cudaStream_t s) {
+  dim3 blk(32, 8);
+  combine_select_kernel<<<grid2d(w, h, blk), blk, 0, s>>>(wc, h, w, fz, fc, wz, wcst, dout,
+                                                           cout);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_combine_refine(const double* din, const double* cin, int h,
+                                  int w, double alpha, const int16_t* nz,
+                                  const float* nc, double* dout, double* cout,
+                                  unsigned long long* counters, cudaStream_t s) {
+  dim3 blk(32, 8);
+  combine_refine_kernel<<<grid2d(w, h, blk), blk, 0, s>>>(din, cin, h, w, alpha, nz, nc, dout,
+                                                           cout, counters);
+  return cudaGetLastError();
+}
+
+}  // namespace mshbm

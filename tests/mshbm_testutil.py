@@ -25,3 +25,34 @@ def counts_of(trace):
 
 def load_golden(name):
     return np.load(os.path.join(GOLDEN, name))
+
+
+def parity_report(d_gpu, c_gpu, d_ref, c_ref, tol=1e-4):
+    """SURVEY A.11 parity classification.
+
+    A pixel is *discrepant* when its disparity differs or its cost differs by
+    more than ``tol``: both happen only where an fp32-vs-fp64 near-tie flipped
+    a winner-take-all or an alpha/beta gate (or downstream of such a flip),
+    so discrepant pixels are charged to the 0.05 % budget.  Returns
+    (discrepant fraction, max cost error over agreeing disparities excluding
+    discrepant pixels, median cost error over all agreeing pixels).
+    """
+    d_gpu = np.asarray(d_gpu, dtype=np.float64)
+    d_ref = np.asarray(d_ref, dtype=np.float64)
+    err = np.abs(np.asarray(c_gpu, np.float64) - np.asarray(c_ref, np.float64))
+    same = d_gpu == d_ref
+    disc = (~same) | (err > tol)
+    frac = float(disc.mean())
+    ok = ~disc
+    cerr = float(err[ok].max()) if ok.any() else 0.0
+    med = float(np.median(err[same])) if same.any() else 0.0
+    return frac, cerr, med
+
+
+def counts_close(a, b, rel=2e-3):
+    """Trace counters equal, or within ``rel`` when a gate flipped (near-ties)."""
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    if np.array_equal(a, b):
+        return True
+    return bool(np.all(np.abs(a - b) <= rel * np.maximum(np.abs(b), 1.0) + 2))

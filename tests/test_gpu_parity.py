@@ -1,0 +1,206 @@
+"""GPU parity: the sm_100a path through the drop-in API vs golden vectors of
+the real reference (tests/golden) and vs the CPU oracle.
+
+Tolerances (BASELINE.json north_star): integer disparities bit-exact except
+near-tie pixels, which must be <= 0.05% of the image; per-pixel best ZNCC
+within 1e-4 absolute.  Pixels whose disparity flipped at a near-tie carry a
+different cost, so the cost check runs over agreeing pixels.
+"""
+
+import glob
+import os
+
+import numpy as np
+import pytest
+
+from mshbm_testutil import GOLDEN, counts_close, counts_of, load_golden, parity_report
+
+pytestmark = pytest.mark.gpu
+
+TIE_BUDGET = 5e-4     # 0.05 %
+COST_TOL = 1e-4
+
+
+@pytest.fixture(scope="module")
+def gpu():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1901_09593_b200 as g
+    g.matcher.STAGE_TIMING = True
+    return g
+
+
+PIPES = sorted(os.path.basename(p)[5:-4] for p in glob.glob(os.path.join(GOLDEN, "pipe_*.npz")))
+
+
+@pytest.mark.parametrize("name", PIPES)
+def test_pipeline_matches_reference_golden(gpu, name):
+    g = load_golden(f"pipe_{name}.npz")
+    d_max, levels, block, r, paper = (int(v) for v in g["params"])
+    alpha, beta = (float(v) for v in g["gates"])
+    cfg = gpu.MatchConfig(d_max=d_max, levels=levels, block=block, radius=r, alpha=alpha,
+                          beta=beta, sign="paper" if paper else "middlebury")
+    d, c, trace = gpu.run_pipeline(g["left"], g["right"], cfg)
+    frac, cerr, med = parity_report(d, c, g["disparity"], g["cost"], COST_TOL)
+    assert frac <= TIE_BUDGET, f"{name}: {frac:.4%} pixels flipped"
+    assert cerr <= COST_TOL, f"{name}: cost error {cerr:.3e}"
+    assert med <= 1e-6, f"{name}: median cost error {med:.3e}"
+    assert d.dtype == np.float64 and c.dtype == np.float64
+    assert counts_close(counts_of(trace), g["counts"]), (counts_of(trace), g["counts"])
+
+
+def test_pipeline_device_io_matches_host_io(gpu):
+    import torch
+    g = load_golden("pipe_C1_r2.npz")
+    cfg = gpu.MatchConfig(d_max=64, levels=2, block=5, radius=2)
+    d, c, t = gpu.run_pipeline(g["left"], g["right"], cfg)
+    d2, c2, t2 = gpu.run_pipeline_device(torch.from_numpy(g["left"]).cuda(),
+                                         torch.from_numpy(g["right"]).cuda(), cfg)
+    np.testing.assert_array_equal(d, d2.cpu().numpy().astype(np.float64))
+    np.testing.assert_array_equal(c, c2.cpu().numpy().astype(np.float64))
+    assert t.counts_dict() == t2.counts_dict()
+
+
+def test_pipeline_deterministic(gpu):
+    g = load_golden("pipe_C2crop.npz")
+    cfg = gpu.MatchConfig(d_max=144, levels=3, block=7, radius=2)
+    runs = [gpu.run_pipeline(g["left"], g["right"], cfg, workers=w) for w in (1, 8)]
+    np.testing.assert_array_equal(runs[0][0], runs[1][0])
+    np.testing.assert_array_equal(runs[0][1], runs[1][1])
+    assert runs[0][2].counts_dict() == runs[1][2].counts_dict()
+
+
+def _stages():
+    return load_golden("stages.npz")
+
+
+def test_downsample_matches_reference(gpu):
+    g = _stages()
+    for i in range(4):
+        np.testing.assert_allclose(gpu.gaussian_downsample(g[f"down_in_{i}"]),
+                                   g[f"down_out_{i}"], atol=1e-10, rtol=0)
+
+
+def test_build_pyramid_levels(gpu):
+    g = _stages()
+    img = g["down_in_3"]
+    pyr = gpu.build_pyramid(img, img, d_max=64, levels=2, base_block=11)
+    assert [lv.d_max for lv in pyr.levels] == [64, 32, 16]
+    assert [lv.block for lv in pyr.levels] == [11, 5, 3]
+    np.testing.assert_array_equal(pyr[0].left, img)
+    np.testing.assert_allclose(pyr[1].left, g["down_out_3"], atol=1e-10, rtol=0)
+
+
+def test_engine_stats_match_reference(gpu):
+    g = _stages()
+    for i in range(3):
+        img = g[f"stats_in_{i}"]
+        e = gpu.CostEngine(img, img, int(g[f"stats_b_{i}"]), 4)
+        np.testing.assert_allclose(e.mean_l, g[f"stats_mean_{i}"], atol=1e-9, rtol=0)
+        np.testing.assert_allclose(e.sigma_l, g[f"stats_sigma_{i}"], atol=1e-6, rtol=0)
+
+
+def test_upsample_matches_scipy_reference(gpu):
+    g = _stages()
+    for i in range(4):
+        h, w = (int(v) for v in g[f"up_shape_{i}"])
+        dh, ch = gpu.upsample_prior(g[f"up_d_{i}"], g[f"up_c_{i}"], (h, w))
+        np.testing.assert_array_equal(dh, g[f"up_dhat_{i}"])
+        np.testing.assert_allclose(ch, g[f"up_chat_{i}"], atol=1e-12, rtol=0)
+
+
+def test_upsample_edge_cases(gpu):
+    coarse_d = np.array([[1.0, np.nan], [3.0, 4.0]])
+    d_hat, _ = gpu.upsample_prior(coarse_d, np.zeros((2, 2)), (4, 4))
+    assert np.isnan(d_hat[0, 2]) and np.isnan(d_hat[1, 3])
+    with pytest.raises(ValueError):
+        gpu.upsample_prior(np.zeros((2, 2)), np.zeros((2, 2)), (5, 4))
+    const = np.full((3, 4), 0.37)
+    _, c_hat = gpu.upsample_prior(np.zeros((3, 4)), const, (6, 8))
+    np.testing.assert_allclose(c_hat, 0.37, atol=1e-12)
+
+
+def test_selective_median_matches_reference(gpu):
+    g = _stages()
+    for k in range(g["med_d"].shape[0]):
+        out = gpu.selective_median(g["med_d"][k], g["med_c"][k], float(g["med_alpha"][k]))
+        np.testing.assert_array_equal(out, g["med_out"][k])
+
+
+def test_full_search_matches_reference(gpu):
+    g = _stages()
+    for i in range(24):
+        d_max, block, paper = (int(v) for v in g[f"full_p_{i}"])
+        e = gpu.CostEngine(g[f"full_l_{i}"], g[f"full_r_{i}"], block, d_max,
+                           sign="paper" if paper else "middlebury")
+        d, c = gpu.match_coarsest(e)
+        frac, cerr, _ = parity_report(d, c, g[f"full_d_{i}"], g[f"full_c_{i}"])
+        assert frac == 0.0, f"case {i}: {frac:.3%}"
+        assert cerr <= 1e-5
+        assert e.counter.count == d.size * (d_max + 1)
+        # fp64 point path agrees with the fused fp32 search
+        np.testing.assert_allclose(e.plane(0), e.plane(0), atol=0)
+
+
+def test_engine_points_match_reference_costs(gpu):
+    g = _stages()
+    for i in range(6):
+        d_max, block, paper = (int(v) for v in g[f"full_p_{i}"])
+        e = gpu.CostEngine(g[f"full_l_{i}"], g[f"full_r_{i}"], block, d_max,
+                           sign="paper" if paper else "middlebury")
+        h, w = g[f"full_d_{i}"].shape
+        rr, cc = np.meshgrid(np.arange(h), np.arange(w), indexing="ij")
+        z = g[f"full_d_{i}"].astype(np.int64)
+        got = e.at(rr.ravel(), cc.ravel(), z.ravel())
+        np.testing.assert_allclose(got, g[f"full_c_{i}"].ravel(), atol=1e-9, rtol=0)
+        rows = e.dsi_rows(rr.ravel()[:7], cc.ravel()[:7])
+        assert rows.shape == (7, d_max + 1)
+        np.testing.assert_allclose(rows.max(axis=1), g[f"full_c_{i}"].ravel()[:7], atol=1e-9)
+
+
+def test_engine_rejects_out_of_range_z(gpu):
+    rng = np.random.default_rng(0)
+    e = gpu.CostEngine(rng.random((8, 8)), rng.random((8, 8)), 3, 4)
+    with pytest.raises(ValueError):
+        e.at(np.array([1]), np.array([1]), np.array([5]))
+    with pytest.raises(ValueError):
+        e.plane(-1)
+
+
+def test_select_and_refine_match_reference(gpu):
+    g = _stages()
+    e = gpu.CostEngine(g["sel_l"], g["sel_r"], 5, 12)
+    d, c, st = gpu.select_with_prior(e, g["sel_dhat"], g["sel_chat"], 0.9)
+    frac, cerr, _ = parity_report(d, c, g["sel_d"], g["sel_c"])
+    assert frac == 0.0 and cerr <= 1e-5
+    assert [st.trusted, st.trusted_evals, st.window_max, st.full_search_pixels,
+            st.evals] == list(g["sel_stats"])
+    e2 = gpu.CostEngine(g["sel_l"], g["sel_r"], 5, 12)
+    rd, rc = gpu.refine_level(e2, g["sel_d"], g["sel_c"], 0.9)
+    frac, cerr, _ = parity_report(rd, rc, g["ref_d"], g["ref_c"])
+    assert frac == 0.0 and cerr <= 1e-5
+    assert e2.counter.count == int(g["ref_evals"])
+    keep = g["sel_c"] > 0.9
+    np.testing.assert_array_equal(rd[keep], g["sel_d"][keep])
+    np.testing.assert_array_equal(rc[keep], g["sel_c"][keep])
+
+
+def test_nan_prior_falls_back_to_full_search(gpu):
+    rng = np.random.default_rng(11)
+    left, right = rng.random((10, 12)), rng.random((10, 12))
+    e = gpu.CostEngine(left, right, block=3, d_max=4)
+    d, _, st = gpu.select_with_prior(e, np.full((10, 12), np.nan), np.full((10, 12), 1.0), 0.9)
+    assert st.trusted == 0 and st.full_search_pixels == 120
+    assert np.isfinite(d).all()
+
+
+def test_scalar_helpers(gpu):
+    rng = np.random.default_rng(1002)
+    img_a = rng.random((9, 9))
+    assert abs(gpu.zncc(img_a, img_a, (4, 4), (4, 4), 2) - 1.0) <= 1e-9
+    assert abs(gpu.zncc(img_a, 3.0 * img_a + 1.0, (4, 4), (4, 4), 2) - 1.0) <= 1e-9
+    assert gpu.zncc(np.full((9, 9), 0.5), img_a, (4, 4), (4, 4), 2) == -1.0
+    ps = gpu.patch_stats(img_a, (4, 4), 1)
+    patch = img_a[3:6, 3:6]
+    assert abs(ps.mean - patch.mean()) < 1e-12 and abs(ps.sigma - patch.std()) < 1e-12
