@@ -186,6 +186,8 @@ int mshbm_upsample_prior(mshbm_ctx* ctx, const double* d_coarse,
  * FMA chains per thread, `iters` x 128 FMAs): the roofline denominator of
  * the ZNCC sweep (not part of the reference interface). */
 int mshbm_probe_fp32_peak(int device, int iters, double* tflops, double* ms);
+/* FP64 DFMA throughput, same shape (diagnostics). */
+int mshbm_probe_fp64_peak(int device, int iters, double* tflops, double* ms);
 
 #ifdef __cplusplus
 }

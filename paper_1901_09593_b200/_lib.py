@@ -73,6 +73,7 @@ SIGNATURES = {
     "mshbm_selective_median": (C.c_int, [P, P, P, I32, I32, D, P, P, P]),
     "mshbm_upsample_prior": (C.c_int, [P, P, P, I32, I32, I32, I32, P, P, P]),
     "mshbm_probe_fp32_peak": (C.c_int, [C.c_int, C.c_int, C.POINTER(D), C.POINTER(D)]),
+    "mshbm_probe_fp64_peak": (C.c_int, [C.c_int, C.c_int, C.POINTER(D), C.POINTER(D)]),
 }
 
 _lock = threading.Lock()

@@ -38,7 +38,8 @@ template <int B, int DIR, int ZC, int NR, int NZ>
 __device__ __forceinline__ void sweep_chunk(
     const float (&Rs)[NR + B - 1][30 + B + ZC], const float2 (&Ms)[NR][31 + ZC],
     float (&Hs)[ZC][NR][32], const float (&Lt)[B][B], float sumLt, int z0, int zoff,
-    int zend, bool inimg, int lane, int wp, float& bF, int& zF) {
+    int zend, bool inimg, int lane, int wp, float& bF, int& zF, bool wchunk, int wlo,
+    int whi, float& bW, int& zW) {
   float S[NZ];
 #pragma unroll
   for (int zz = 0; zz < NZ; ++zz) S[zz] = 0.f;
@@ -70,6 +71,9 @@ __device__ __forceinline__ void sweep_chunk(
     rho = fminf(fmaxf(rho, -1.f), 1.f);            // fmaxf(NaN, -1) = -1
     if (NZ < ZC && z > zend) rho = -3.f;           // masked tail slot
     if (rho > bF) { bF = rho; zF = z; }
+    if (wchunk) {   // warp-uniform: some lane's prior window meets this chunk
+      if (z >= wlo && z <= whi && rho > bW) { bW = rho; zW = z; }
+    }
     const float o = inimg ? rho : 0.f;
     const float hl = __shfl_up_sync(kFull, o, 1);
     const float hr = __shfl_down_sync(kFull, o, 1);
@@ -164,77 +168,65 @@ sweep_kernel(const SweepArgs a) {
   };
   fetch(0);
 
+  // ---- left tile (fp64) through shared memory, aliasing the Hs buffers
+  // (first written after the barrier that follows store(0))
+  constexpr int LC = 31 + B;
+  using LtT = double[RR][LC];
+  static_assert(sizeof(LtT) <= 2 * sizeof(HsT), "left tile must fit in Hs");
+  LtT& Ls = *reinterpret_cast<LtT*>(Hs);
+  for (int t = threadIdx.x; t < RR * LC; t += NT) {
+    const int rr = t / LC, e = t - rr * LC;
+    Ls[rr][e] = a.L[(int64_t)clampi(y0 - 1 - H2 + rr, 0, H - 1) * a.ld +
+                    clampi(x0 - 1 - H2 + e, 0, W - 1)];
+  }
+  __syncthreads();
+
   // ---- left window: centred in fp64, scaled by 1/(b^2 sigma_L), rounded once
+  // (replicate padding comes from the clamped tile rows/cols; halo lanes at
+  // the image border see clamped duplicates and are never outputs)
   float Lt[B][B];
   float sumLt;
-  const int ic = clampi(i, 0, H - 1), jc = clampi(j, 0, W - 1);
   {
     double s = 0.0;
 #pragma unroll
-    for (int r = 0; r < B; ++r) {
-      const double* row = a.L + (int64_t)clampi(ic + r - H2, 0, H - 1) * a.ld;
+    for (int r = 0; r < B; ++r)
 #pragma unroll
-      for (int c = 0; c < B; ++c) s += row[clampi(jc + c - H2, 0, W - 1)];
-    }
+      for (int c = 0; c < B; ++c) s += Ls[wp + r][lane + c];
     const double mu = s / (double)(B * B);
     double ss = 0.0;
 #pragma unroll
-    for (int r = 0; r < B; ++r) {
-      const double* row = a.L + (int64_t)clampi(ic + r - H2, 0, H - 1) * a.ld;
+    for (int r = 0; r < B; ++r)
 #pragma unroll
       for (int c = 0; c < B; ++c) {
-        const double dv = row[clampi(jc + c - H2, 0, W - 1)] - mu;
-        ss += dv * dv;
+        const double dv = Ls[wp + r][lane + c] - mu;
+        ss = fma(dv, dv, ss);
       }
-    }
     const double sigma = sqrt(ss / (double)(B * B));
     const bool okL = inimg && sigma >= a.sigma_eps;
     const double kL = okL ? 1.0 / ((double)(B * B) * sigma) : 0.0;
-    double sl = 0.0;
+    float sl = 0.f;
 #pragma unroll
-    for (int r = 0; r < B; ++r) {
-      const double* row = a.L + (int64_t)clampi(ic + r - H2, 0, H - 1) * a.ld;
+    for (int r = 0; r < B; ++r)
 #pragma unroll
       for (int c = 0; c < B; ++c) {
-        const float f = (float)((row[clampi(jc + c - H2, 0, W - 1)] - mu) * kL);
+        const float f = (float)((Ls[wp + r][lane + c] - mu) * kL);
         Lt[r][c] = f;
-        sl += (double)f;
+        sl += f;
       }
-    }
-    sumLt = okL ? (float)sl : qnan;   // NaN: every cost of a flat block is -1
+    sumLt = okL ? sl : qnan;   // NaN: every cost of a flat block is -1
   }
 
-  // ---- prior window: <= 2r+1 candidates evaluated once, ascending, strict '>'
+  // ---- prior window (candidates in ascending z, strict '>', init -2)
   bool trusted = false;
-  int zW = 0;
+  int wlo = 1, whi = 0, zW = 0;
   float bW = -2.f;
   if (a.wc != nullptr && inner) {
     const int c = a.wc[(int64_t)i * a.ldw + j];
     if (c != kWcNone) {
       trusted = true;
-      const int wlo = max(c - a.radius, 0), whi = min(c + a.radius, d);
+      wlo = max(c - a.radius, 0);
+      whi = min(c + a.radius, d);
       zW = wlo;
-      for (int z = wlo; z <= whi; ++z) {
-        const int q = j - DIR * z;
-        float rho = -1.f;
-        if (q >= 0 && q < W) {
-          const int64_t so = (int64_t)i * a.lds + q;
-          const float is = a.isR[so];
-          if (is > 0.f) {
-            float acc = 0.f;
-#pragma unroll
-            for (int r = 0; r < B; ++r) {
-              const double* row = a.R + (int64_t)clampi(i + r - H2, 0, H - 1) * a.ld;
-#pragma unroll
-              for (int cc = 0; cc < B; ++cc)
-                acc = fmaf(Lt[r][cc], (float)(row[clampi(q + cc - H2, 0, W - 1)] - cR), acc);
-            }
-            rho = fmaf(-(a.muR[so] - cRf), sumLt, acc) * is;
-            rho = fminf(fmaxf(rho, -1.f), 1.f);
-          }
-        }
-        if (rho > bW) { bW = rho; zW = z; }
-      }
     }
   }
 
@@ -250,30 +242,32 @@ sweep_kernel(const SweepArgs a) {
   for (int z0 = 0; z0 <= zmax; z0 += ZC, cur ^= 1) {
     const bool more = z0 + ZC <= zmax;
     if (more) fetch(z0 + ZC);   // in flight during this chunk's math
+    const bool wchunk = __any_sync(kFull, trusted && wlo <= z0 + ZC - 1 && whi >= z0);
     int nz;
     if (z0 + ZC - 1 <= zmax) {
       sweep_chunk<B, DIR, ZC, NR, ZC>(Rs[cur], Ms[cur], Hs[cur], Lt, sumLt, z0, 0, zmax,
-                                      inimg, lane, wp, bF, zF);
+                                      inimg, lane, wp, bF, zF, wchunk, wlo, whi, bW, zW);
       nz = ZC;
     } else {
       nz = zmax - z0 + 1;
       for (int zo = 0; zo < nz; zo += 4)
         sweep_chunk<B, DIR, ZC, NR, 4>(Rs[cur], Ms[cur], Hs[cur], Lt, sumLt, z0, zo, zmax,
-                                       inimg, lane, wp, bF, zF);
+                                       inimg, lane, wp, bF, zF, wchunk, wlo, whi, bW, zW);
     }
     if (more) store(cur ^ 1);
     __syncthreads();
     if (inner) {
       const HsT& hs = Hs[cur];
-#pragma unroll 4
-      for (int zz = 0; zz < nz; ++zz) {
+#pragma unroll
+      for (int zz = 0; zz < ZC; ++zz) {
         const float nb = (hs[zz][wp - 1][lane] + hs[zz][wp][lane]) + hs[zz][wp + 1][lane];
-        if (nb > bN) { bN = nb; zN = z0 + zz; }
+        if (zz < nz && nb > bN) { bN = nb; zN = z0 + zz; }
       }
     }
   }
 
   // ---- epilogue: the reference's gates
+  if (trusted && bW == -2.f) { bW = -1.f; zW = wlo; }  // window beyond zmax: all -1
   const int members = ((i > 0) + 1 + (i < H - 1)) * ((j > 0) + 1 + (j < W - 1));
   bool low = false;
   if (a.mode == kSweepPipeline) {

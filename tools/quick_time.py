@@ -43,3 +43,5 @@ for name in sys.argv[1:] or ["C2"]:
 tf, ms = C.c_double(), C.c_double()
 _lib.lib().mshbm_probe_fp32_peak(0, 20000, C.byref(tf), C.byref(ms))
 print(f"fp32 FFMA probe: {tf.value:.1f} TFLOP/s ({ms.value:.2f} ms)")
+_lib.lib().mshbm_probe_fp64_peak(0, 4000, C.byref(tf), C.byref(ms))
+print(f"fp64 DFMA probe: {tf.value:.1f} TFLOP/s ({ms.value:.2f} ms)")
