@@ -221,7 +221,7 @@ int enqueue(mshbm_ctx* ctx, Plan& p, cudaStream_t s, std::vector<StageEvents>* t
     if (k < p.K) {
       LevelBuf& c = p.lv[k + 1];
       CK(launch_bspline_prefilter(c.c, nullptr, c.h, c.w, c.ld, c.coef, c.ldc, s));
-      n += 5;
+      n += 1;
       CK(launch_prior_eval(c.dmed, c.ld, c.h, c.w, c.coef, c.ldc, l.h, l.w, l.d, cfg.radius,
                            cfg.beta, l.wc, l.ld, cnt, s));
       ++n;
@@ -828,7 +828,7 @@ int mshbm_upsample_prior(mshbm_ctx* ctx, const double* d_coarse, const double* c
   CK(cudaMallocAsync((void**)&coef, (size_t)ldc * (ch + 24) * 8 * 2, s));
   CK(launch_bspline_prefilter(nullptr, c_coarse, ch, cw, cw, coef, ldc, s));
   CK(launch_upsample(d_coarse, ch, cw, coef, ldc, h, w, d_hat, c_hat, s));
-  ctx->launches += 6;
+  ctx->launches += 2;
   CK(cudaFreeAsync(coef, s));
   return MSHBM_OK;
 }

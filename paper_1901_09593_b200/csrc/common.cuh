@@ -39,6 +39,36 @@ MSHBM_DEV void warp_atomic_max(long long* dst, long long v) {
   if ((threadIdx.x & 31) == 0 && v > 0) atomicMax((long long*)dst, v);
 }
 
+// Block-level counter accumulation: warp shuffles, one shared-memory atomic
+// per warp, one global atomic per block (same-address global atomics from
+// every warp serialise in L2).  Every thread of the block must call it.
+template <int NSLOT>
+MSHBM_DEV void block_accumulate(unsigned long long* __restrict__ gdst, const int (&slot)[NSLOT],
+                                const unsigned long long (&val)[NSLOT], const bool (&is_max)[NSLOT]) {
+  __shared__ unsigned long long acc[NSLOT];
+  const int tid = threadIdx.x + blockDim.x * (threadIdx.y + blockDim.y * threadIdx.z);
+  if (tid < NSLOT) acc[tid] = 0ull;
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < NSLOT; ++k) {
+    unsigned long long x = val[k];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const unsigned long long y = __shfl_xor_sync(0xffffffffu, x, o);
+      x = is_max[k] ? (y > x ? y : x) : x + y;
+    }
+    if ((tid & 31) == 0 && x) {
+      if (is_max[k]) atomicMax(&acc[k], x);
+      else atomicAdd(&acc[k], x);
+    }
+  }
+  __syncthreads();
+  if (tid < NSLOT && acc[tid]) {
+    if (is_max[tid]) atomicMax(&gdst[slot[tid]], acc[tid]);
+    else atomicAdd(&gdst[slot[tid]], acc[tid]);
+  }
+}
+
 // Per-level device counters (int64), see mshbm_level_trace.
 enum CounterSlot {
   kCntTrusted = 0,

@@ -38,6 +38,9 @@ struct SweepArgs {
 };
 cudaError_t launch_sweep(const SweepArgs& a, cudaStream_t s, int* n_launch);
 bool sweep_supported_block(int b);
+// two-pixels-per-thread variant (sweep2.cu) for b in {3,5,7,9,11}
+bool sweep2_supported(int b);
+cudaError_t launch_sweep2(const SweepArgs& a, cudaStream_t s);
 
 // ---------------------------------------------------------------- pyramid
 cudaError_t launch_f32_to_f64(const float* a, const float* b, int h, int w,

@@ -244,6 +244,104 @@ __global__ void __launch_bounds__(128) iir_anticausal_kernel(const double* __res
   }
 }
 
+// Fused prefilter: one block per 32x32 tile of the padded coefficient array.
+// The block stages the (32+64)^2 padded input region (edge-replicated coarse
+// costs, i.e. scipy's 12-sample prepad) in shared memory, filters axis 0
+// (causal then anticausal per column) and axis 1 (per row) in place, and
+// writes the inner 32x32.  Lines are exact where the tile reaches a line end
+// (scipy init) and warmed up over 32 samples elsewhere (|z|^32 ~ 5e-19).
+constexpr int kTile = 32, kWU = 32, kExt = kTile + 2 * kWU;   // 96
+
+__device__ __forceinline__ void iir_line_smem(double* x, int stride, int lo, int hi, bool exact_lo,
+                                              bool exact_hi, int n_full, double g) {
+  // x[lo .. hi) is the part of the line inside the tile (tile-local indices);
+  // exact_lo: x[lo] is element 0 of the line; exact_hi: x[hi-1] is element n-1.
+  const double z = kPole;
+  const int n = hi - lo;
+  if (n <= 0) return;
+  for (int k = lo; k < hi; ++k) x[k * stride] *= g;
+  double acc;
+  if (exact_lo) {
+    if (exact_hi && n_full == n) {
+      // whole line present: scipy's full reflect init
+      const double zn = pow(z, (double)n);
+      const double c0 = x[lo * stride];
+      double s = c0 + zn * x[(hi - 1) * stride];
+      double zi = z;
+      for (int i = 1; i < n; ++i) {
+        s += zi * (x[(lo + i) * stride] + zn * x[(hi - 1 - i) * stride]);
+        zi *= z;
+      }
+      acc = s * (z / (1.0 - zn * zn)) + c0;
+    } else {
+      // line longer than the warm-up: z^n terms vanish (n > 64)
+      double s = 0.0, zi = z;
+      const int m = min(n, kWU);
+      for (int i = 1; i < m; ++i) {
+        s += zi * x[(lo + i) * stride];
+        zi *= z;
+      }
+      const double c0 = x[lo * stride];
+      acc = (c0 + s) * z + c0;
+    }
+  } else {
+    acc = x[lo * stride];
+  }
+  x[lo * stride] = acc;
+  for (int k = lo + 1; k < hi; ++k) {
+    acc = x[k * stride] + z * acc;
+    x[k * stride] = acc;
+  }
+  acc = exact_hi ? x[(hi - 1) * stride] * (z / (z - 1.0)) : -z * x[(hi - 1) * stride];
+  x[(hi - 1) * stride] = acc;
+  for (int k = hi - 2; k >= lo; --k) {
+    acc = z * (acc - x[k * stride]);
+    x[k * stride] = acc;
+  }
+}
+
+__global__ void __launch_bounds__(128) bspline_tile_kernel(const float* c32, const double* c64,
+                                                           int ch, int cw, int64_t ldcin,
+                                                           double* coef, int64_t ldc) {
+  extern __shared__ double S[];   // [kExt][kExt + 1]
+  constexpr int SP = kExt + 1;
+  const int nh = ch + 2 * kNpad, nw = cw + 2 * kNpad;
+  const int y0 = blockIdx.y * kTile, x0 = blockIdx.x * kTile;
+  const int gy0 = y0 - kWU, gx0 = x0 - kWU;
+  for (int t = threadIdx.x; t < kExt * kExt; t += blockDim.x) {
+    const int r = t / kExt, c = t - r * kExt;
+    const int gy = gy0 + r, gx = gx0 + c;
+    double v = 0.0;
+    if (gy >= 0 && gy < nh && gx >= 0 && gx < nw) {
+      const int64_t o = (int64_t)clampi(gy - kNpad, 0, ch - 1) * ldcin + clampi(gx - kNpad, 0, cw - 1);
+      v = c32 ? (double)c32[o] : c64[o];
+    }
+    S[r * SP + c] = v;
+  }
+  __syncthreads();
+  const double gain = (1.0 - kPole) * (1.0 - 1.0 / kPole);
+  // rows of the tile that lie in the array
+  const int rlo = max(0, -gy0), rhi = min(kExt, nh - gy0);
+  const int clo = max(0, -gx0), chi = min(kExt, nw - gx0);
+  // axis 0: one thread per column
+  for (int c = threadIdx.x; c < kExt; c += blockDim.x) {
+    if (c < clo || c >= chi) continue;
+    iir_line_smem(S + c, SP, rlo, rhi, gy0 + rlo == 0, gy0 + rhi == nh, nh, gain);
+  }
+  __syncthreads();
+  // axis 1: one thread per output row of the tile
+  for (int r = kWU + threadIdx.x; r < kWU + kTile; r += blockDim.x) {
+    if (r < rlo || r >= rhi) continue;
+    iir_line_smem(S + r * SP, 1, clo, chi, gx0 + clo == 0, gx0 + chi == nw, nw, gain);
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < kTile * kTile; t += blockDim.x) {
+    const int r = t / kTile, c = t - r * kTile;
+    const int gy = y0 + r, gx = x0 + c;
+    if (gy < nh && gx < nw) coef[(int64_t)gy * ldc + gx] = S[(kWU + r) * SP + kWU + c];
+  }
+}
+
 __device__ __forceinline__ void bspline_w(double t, double* wgt) {
   const double u = 1.0 - t;
   wgt[0] = u * u * u / 6.0;
@@ -281,14 +379,11 @@ __device__ __forceinline__ void count_trusted(bool trusted, int c, int r, int d,
                                               unsigned long long* counters) {
   long long ws = 0;
   if (trusted) ws = (long long)(min(c + r, d) - max(c - r, 0) + 1);
-  const unsigned bal = __ballot_sync(kFull, trusted);
-  unsigned long long evals = warp_sum_u64((unsigned long long)ws);
-  long long wmax = warp_max_i64(ws);
-  if ((threadIdx.x & 31) == 0 && bal) {
-    atomicAdd(&counters[kCntTrusted], (unsigned long long)__popc(bal));
-    atomicAdd(&counters[kCntTrustedEvals], evals);
-    atomicMax((unsigned long long*)&counters[kCntWindowMax], (unsigned long long)wmax);
-  }
+  const int slot[3] = {kCntTrusted, kCntTrustedEvals, kCntWindowMax};
+  const unsigned long long val[3] = {trusted ? 1ull : 0ull, (unsigned long long)ws,
+                                     (unsigned long long)ws};
+  const bool mx[3] = {false, false, true};
+  block_accumulate<3>(counters, slot, val, mx);
 }
 
 // upsample_prior + the trust gate of select_with_prior (matcher.py:236-260,
@@ -544,6 +639,154 @@ __global__ void combine_refine_kernel(const double* din, const double* cin,
   }
 }
 
+// ---- shared-memory tiled versions of the per-pixel stage kernels --------
+constexpr int kTX = 32, kTY = 8;
+
+// K2 for b <= 15: window tile in smem; mean via separable row sums,
+// centred sigma from the tile (fp64), 1/sigma or 0 (degenerate) in fp32.
+template <int B>
+__global__ void __launch_bounds__(kTX * kTY) stats_tiled_kernel(const double* img, int h, int w,
+                                                              int64_t ld, double sigma_eps,
+                                                              float* mu32, float* is32,
+                                                              int64_t lds) {
+  constexpr int H2 = B / 2, TR = kTY + B - 1, TC = kTX + B - 1;
+  __shared__ double T[TR][TC];
+  __shared__ double Hs[TR][kTX];
+  const int x0 = blockIdx.x * kTX, y0 = blockIdx.y * kTY;
+  const int tid = threadIdx.y * kTX + threadIdx.x;
+  for (int t = tid; t < TR * TC; t += kTX * kTY) {
+    const int r = t / TC, c = t - r * TC;
+    T[r][c] = img[(int64_t)clampi(y0 - H2 + r, 0, h - 1) * ld + clampi(x0 - H2 + c, 0, w - 1)];
+  }
+  __syncthreads();
+  for (int t = tid; t < TR * kTX; t += kTX * kTY) {
+    const int r = t / kTX, c = t - r * kTX;
+    double s = 0.0;
+#pragma unroll
+    for (int k = 0; k < B; ++k) s += T[r][c + k];
+    Hs[r][c] = s;
+  }
+  __syncthreads();
+  const int x = x0 + threadIdx.x, y = y0 + threadIdx.y;
+  if (x >= w || y >= h) return;
+  double s = 0.0;
+#pragma unroll
+  for (int k = 0; k < B; ++k) s += Hs[threadIdx.y + k][threadIdx.x];
+  const double mu = s / (double)(B * B);
+  double ss = 0.0;
+#pragma unroll
+  for (int r = 0; r < B; ++r)
+#pragma unroll
+    for (int c = 0; c < B; ++c) {
+      const double dv = T[threadIdx.y + r][threadIdx.x + c] - mu;
+      ss = fma(dv, dv, ss);
+    }
+  const double sigma = sqrt(ss / (double)(B * B));
+  mu32[(int64_t)y * lds + x] = (float)mu;
+  is32[(int64_t)y * lds + x] = sigma >= sigma_eps ? (float)(1.0 / sigma) : 0.f;
+}
+
+// prior_eval with the 4x4 spline support of the block staged in smem
+__global__ void __launch_bounds__(kTX * kTY) prior_eval_tiled_kernel(
+    const int16_t* dco, int64_t ldd, int ch, int cw, const double* coef, int64_t ldc, int h,
+    int w, int d, int r, double beta, int* wc, int64_t ldw, unsigned long long* counters) {
+  constexpr int CR = 12, CC = 24;
+  __shared__ double Cs[CR][CC];
+  const int nh = ch + 2 * kNpad, nw = cw + 2 * kNpad;
+  const double ry = (double)ch / (double)h, rx = (double)cw / (double)w;
+  const int i0 = blockIdx.y * kTY, j0 = blockIdx.x * kTX;
+  const int ylo = (int)floor(((double)i0 + 0.5) * ry - 0.5 + kNpad) - 1;
+  const int xlo = (int)floor(((double)j0 + 0.5) * rx - 0.5 + kNpad) - 1;
+  const int tid = threadIdx.y * kTX + threadIdx.x;
+  for (int t = tid; t < CR * CC; t += kTX * kTY) {
+    const int a = t / CC, b = t - a * CC;
+    Cs[a][b] = coef[(int64_t)clampi(ylo + a, 0, nh - 1) * ldc + clampi(xlo + b, 0, nw - 1)];
+  }
+  __syncthreads();
+  const int i = i0 + threadIdx.y, j = j0 + threadIdx.x;
+  const bool in = i < h && j < w;
+  bool trusted = false;
+  int center = 0;
+  if (in) {
+    const double y = ((double)i + 0.5) * ry - 0.5 + kNpad;
+    const double x = ((double)j + 0.5) * rx - 0.5 + kNpad;
+    const double fy = floor(y), fx = floor(x);
+    double wy[4], wx[4];
+    bspline_w(y - fy, wy);
+    bspline_w(x - fx, wx);
+    const int iy = (int)fy - 1 - ylo, ix = (int)fx - 1 - xlo;   // within the tile
+    double chat = 0.0;
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      double rr = 0.0;
+#pragma unroll
+      for (int b = 0; b < 4; ++b) rr += wx[b] * Cs[iy + a][ix + b];
+      chat += wy[a] * rr;
+    }
+    chat = fmin(fmax(chat, -1.0), 1.0);
+    center = 2 * (int)dco[(int64_t)(i >> 1) * ldd + (j >> 1)];
+    const bool ok = (center + r >= 0) && (center - r <= d);
+    trusted = (chat > beta) && ok;
+    wc[(int64_t)i * ldw + j] = trusted ? center : kWcNone;
+  }
+  count_trusted(trusted, center, r, d, counters);
+}
+
+// selective median (pipeline) with the 5x5 neighbourhood staged in smem
+__global__ void __launch_bounds__(kTX * kTY) median_tiled_kernel(
+    const int16_t* d, const float* c, const uint8_t* low, int64_t ld, int h, int w,
+    double alpha, int16_t* out, unsigned long long* counters) {
+  constexpr int TR = kTY + 4, TC = kTX + 4;
+  __shared__ float Cs[TR][TC];
+  __shared__ int16_t Ds[TR][TC];
+  __shared__ uint8_t Lw[TR][TC];
+  const int x0 = blockIdx.x * kTX, y0 = blockIdx.y * kTY;
+  const int tid = threadIdx.y * kTX + threadIdx.x;
+  for (int t = tid; t < TR * TC; t += kTX * kTY) {
+    const int a = t / TC, b = t - a * TC;
+    const int gy = y0 - 2 + a, gx = x0 - 2 + b;
+    if (gy >= 0 && gy < h && gx >= 0 && gx < w) {
+      const int64_t o = (int64_t)gy * ld + gx;
+      Cs[a][b] = c[o];
+      Ds[a][b] = d[o];
+      Lw[a][b] = low[o];
+    } else {
+      Cs[a][b] = -2.f;     // below any legal alpha: never qualifies (matcher.py:345)
+      Ds[a][b] = 0;
+      Lw[a][b] = 0;
+    }
+  }
+  __syncthreads();
+  const int i = y0 + threadIdx.y, j = x0 + threadIdx.x;
+  const bool in = i < h && j < w;
+  bool changed = false, needed = false;
+  if (in) {
+    const int ty = threadIdx.y + 2, tx = threadIdx.x + 2;
+#pragma unroll
+    for (int di = -1; di <= 1; ++di)
+#pragma unroll
+      for (int dj = -1; dj <= 1; ++dj) needed |= Lw[ty + di][tx + dj] != 0;
+    const int16_t d0 = Ds[ty][tx];
+    int16_t res = d0;
+    if ((double)Cs[ty][tx] <= alpha) {
+      int v[24];
+      int n = 0;
+#pragma unroll
+      for (int di = -2; di <= 2; ++di)
+#pragma unroll
+        for (int dj = -2; dj <= 2; ++dj)
+          if ((di | dj) != 0 && (double)Cs[ty + di][tx + dj] > alpha) v[n++] = Ds[ty + di][tx + dj];
+      if (n > 0) res = (int16_t)lower_median(v, n);
+    }
+    out[(int64_t)i * ld + j] = res;
+    changed = res != d0;
+  }
+  const int slot[2] = {kCntMedianReplaced, kCntNeeded};
+  const unsigned long long val[2] = {changed ? 1ull : 0ull, needed ? 1ull : 0ull};
+  const bool mx[2] = {false, false};
+  block_accumulate<2>(counters, slot, val, mx);
+}
+
 }  // namespace
 
 // ------------------------------------------------------------------ launchers
@@ -569,6 +812,15 @@ cudaError_t launch_stats_f32(const double* img, int h, int w, int64_t ld,
                              int b, double sigma_eps, float* mu, float* is,
                              int64_t lds, cudaStream_t s) {
   dim3 blk(32, 8);
+  const dim3 g = grid2d(w, h, blk);
+  switch (b) {
+    case 3: stats_tiled_kernel<3><<<g, blk, 0, s>>>(img, h, w, ld, sigma_eps, mu, is, lds); return cudaGetLastError();
+    case 5: stats_tiled_kernel<5><<<g, blk, 0, s>>>(img, h, w, ld, sigma_eps, mu, is, lds); return cudaGetLastError();
+    case 7: stats_tiled_kernel<7><<<g, blk, 0, s>>>(img, h, w, ld, sigma_eps, mu, is, lds); return cudaGetLastError();
+    case 9: stats_tiled_kernel<9><<<g, blk, 0, s>>>(img, h, w, ld, sigma_eps, mu, is, lds); return cudaGetLastError();
+    case 11: stats_tiled_kernel<11><<<g, blk, 0, s>>>(img, h, w, ld, sigma_eps, mu, is, lds); return cudaGetLastError();
+    default: break;
+  }
   stats_kernel<false><<<grid2d(w, h, blk), blk, 0, s>>>(img, h, w, ld, b, sigma_eps,
                                                          mu, is, nullptr, nullptr, lds);
   return cudaGetLastError();
@@ -585,18 +837,17 @@ cudaError_t launch_stats_f64(const double* img, int h, int w, int64_t ld,
 cudaError_t launch_bspline_prefilter(const float* c32, const double* c64,
                                      int ch, int cw, int64_t ldcin,
                                      double* coef, int64_t ldc, cudaStream_t s) {
-  // coef holds two (ch+24) x ldc planes: the result and a ping-pong scratch
   const int nh = ch + 2 * kNpad, nw = cw + 2 * kNpad;
-  double* tmp = coef + (int64_t)ldc * nh;
-  const double gain = (1.0 - kPole) * (1.0 - 1.0 / kPole);
-  dim3 blk(32, 8);
-  bspline_pad_kernel<<<grid2d(nw, nh, blk), blk, 0, s>>>(c32, c64, ch, cw, ldcin, coef, ldc);
-  const dim3 g0((nw + 127) / 128, nh <= kWin ? 1 : (nh + kSeg - 1) / kSeg);
-  const dim3 g1((nh + 127) / 128, nw <= kWin ? 1 : (nw + kSeg - 1) / kSeg);
-  iir_causal_kernel<<<g0, 128, 0, s>>>(coef, tmp, ldc, nh, nw, 0, gain);
-  iir_anticausal_kernel<<<g0, 128, 0, s>>>(tmp, coef, ldc, nh, nw, 0);
-  iir_causal_kernel<<<g1, 128, 0, s>>>(coef, tmp, ldc, nh, nw, 1, gain);
-  iir_anticausal_kernel<<<g1, 128, 0, s>>>(tmp, coef, ldc, nh, nw, 1);
+  constexpr size_t smem = sizeof(double) * kExt * (kExt + 1);
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(bspline_tile_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  const dim3 grid((nw + kTile - 1) / kTile, (nh + kTile - 1) / kTile);
+  bspline_tile_kernel<<<grid, 128, smem, s>>>(c32, c64, ch, cw, ldcin, coef, ldc);
   return cudaGetLastError();
 }
 
@@ -606,6 +857,12 @@ cudaError_t launch_prior_eval(const int16_t* dcoarse, int64_t ldd, int ch,
                               int64_t ldw, unsigned long long* counters,
                               cudaStream_t s) {
   dim3 blk(32, 8);
+  if (2 * ch <= h + 2 && 2 * cw <= w + 2) {   // dyadic parent: the tile covers the support
+    prior_eval_tiled_kernel<<<grid2d(w, h, blk), blk, 0, s>>>(dcoarse, ldd, ch, cw, coef, ldc, h,
+                                                               w, d, radius, beta, wc, ldw,
+                                                               counters);
+    return cudaGetLastError();
+  }
   prior_eval_kernel<<<grid2d(w, h, blk), blk, 0, s>>>(dcoarse, ldd, ch, cw, coef, ldc, h, w,
                                                        d, radius, beta, wc, ldw, counters);
   return cudaGetLastError();
@@ -636,6 +893,8 @@ cudaError_t launch_median_pipeline(const int16_t* d, const float* c,
                                    unsigned long long* counters,
                                    cudaStream_t s) {
   dim3 blk(32, 8);
+  median_tiled_kernel<<<grid2d(w, h, blk), blk, 0, s>>>(d, c, low, ld, h, w, alpha, out, counters);
+  return cudaGetLastError();
   median_pipeline_kernel<<<grid2d(w, h, blk), blk, 0, s>>>(d, c, low, ld, h, w, alpha, out,
                                                             counters);
   return cudaGetLastError();

@@ -462,6 +462,12 @@ bool sweep_supported_block(int b) { return b >= 3 && (b & 1) && b <= 63; }
 
 cudaError_t launch_sweep(const SweepArgs& a, cudaStream_t s, int* n_launch) {
   if (n_launch) ++*n_launch;
+  static int impl = -1;
+  if (impl < 0) {
+    const char* v = getenv("MSHBM_SWEEP_IMPL");   // 1 = one pixel per thread
+    impl = v ? atoi(v) : 2;
+  }
+  if (impl == 2 && sweep2_supported(a.block)) return launch_sweep2(a, s);
   return a.dir > 0 ? launch_dir<1>(a, s) : launch_dir<-1>(a, s);
 }
 

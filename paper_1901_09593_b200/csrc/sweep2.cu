@@ -1,0 +1,393 @@
+// Dense fused ZNCC z-sweep, two vertically adjacent pixels per thread.
+//
+// Same contract as sweep.cu (one launch per level; full-range, prior-window
+// and 3x3-summed winner-take-all fused; gates in the epilogue), but each
+// thread owns pixels A = (i, j) and B = (i+1, j).  Their windows share b-1
+// rows, so with P(z) = sum over the shared rows of (L - muA)(R - c):
+//   S_A(z) = P(z) + row_top(z)
+//   S_B(z) = P(z) + row_bottom(z) + b^2 (muA - muB) * (muR_B(q) - c)
+// where both extra rows are centred by muA; the last term re-centres B's
+// whole window from muA to muB exactly (sum over a window of (R - c) is
+// b^2 (muR - c)).  That is b^2 + b + 1 FMAs per two pixels instead of 2 b^2,
+// and every staged right-image row feeds both pixels.
+//
+// Reference semantics: matcher.py:184-193 (full search), 263-320 (prior
+// window), 196-233 (3x3-summed refinement); zncc.py:271-287 (cost).
+#include <stdlib.h>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace mshbm {
+
+namespace {
+
+constexpr unsigned kFull = 0xffffffffu;
+
+template <int B, int ZC, int NR>
+struct Sweep2Smem {
+  static constexpr int NROW = 2 * NR;
+  static constexpr int RW = 30 + B + ZC;
+  static constexpr int RR = NROW + B - 1;
+  static constexpr int SW = 31 + ZC;
+  static constexpr int LC = 31 + B;
+  using RsT = float[RR][RW];
+  using MsT = float2[NROW][SW];
+  using HxT = float[ZC][2][NR][32];   // [0] hsA, [1] hsB (horizontal 3-sums)
+  using LsT = double[RR][LC];
+  static constexpr size_t bytes() {
+    return 2 * sizeof(RsT) + 2 * sizeof(MsT) + 2 * sizeof(HxT);
+  }
+};
+
+// One chunk of NZ disparities (NZ == ZC, or 4 for the tail) for pixels A, B.
+template <int B, int DIR, int ZC, int NR, int NZ>
+__device__ __forceinline__ void chunk2(
+    const typename Sweep2Smem<B, ZC, NR>::RsT& Rs, const typename Sweep2Smem<B, ZC, NR>::MsT& Ms,
+    typename Sweep2Smem<B, ZC, NR>::HxT& Hx, const float (&Lt)[B][B], const float (&Lb)[B],
+    float kLA, float kLB, float dW, int z0, int zoff, int zend, bool inA, bool inB, int lane,
+    int wp, float (&best)[4], int (&bestz)[4], bool wchunk, const int (&wlo)[2],
+    const int (&whi)[2]) {
+  float SA[NZ], P[NZ];
+#pragma unroll
+  for (int zz = 0; zz < NZ; ++zz) SA[zz] = 0.f, P[zz] = 0.f;
+  // window rows r = 0 (A only), 1..B-1 (shared), B (B's bottom)
+#pragma unroll
+  for (int r = 0; r <= B; ++r) {
+    const float* rp = &Rs[2 * wp + r][lane];
+#pragma unroll
+    for (int e = 0; e < NZ + B - 1; ++e) {
+      const int eo = DIR > 0 ? (ZC - NZ - zoff) + e : zoff + e;
+      const float v = rp[eo];
+#pragma unroll
+      for (int c = 0; c < B; ++c) {
+        const int g = e - c;
+        if (g >= 0 && g < NZ) {
+          const int zz = DIR > 0 ? (NZ - 1 - g) : g;
+          if (r == 0) SA[zz] = fmaf(Lt[0][c], v, SA[zz]);
+          else if (r < B) P[zz] = fmaf(Lt[r][c], v, P[zz]);
+          else P[zz] = fmaf(Lb[c], v, P[zz]);
+        }
+      }
+    }
+    if (r == B - 1) {
+#pragma unroll
+      for (int zz = 0; zz < NZ; ++zz) SA[zz] += P[zz];   // S_A complete
+    }
+  }
+#pragma unroll
+  for (int zz = 0; zz < NZ; ++zz) {
+    const int z = z0 + zoff + zz;
+    const int g = DIR > 0 ? (ZC - 1 - (zoff + zz)) : (zoff + zz);
+    const float2 ma = Ms[2 * wp][lane + g];       // (muR - c, 1/sigma_R or NaN)
+    const float2 mb = Ms[2 * wp + 1][lane + g];
+    float ra = SA[zz] * kLA * ma.y;
+    float rb = fmaf(dW, mb.x, P[zz]) * kLB * mb.y;
+    ra = fminf(fmaxf(ra, -1.f), 1.f);              // fmaxf(NaN, -1) = -1
+    rb = fminf(fmaxf(rb, -1.f), 1.f);
+    if (NZ < ZC && z > zend) ra = -3.f, rb = -3.f;  // masked tail slot
+    if (ra > best[0]) { best[0] = ra; bestz[0] = z; }
+    if (rb > best[1]) { best[1] = rb; bestz[1] = z; }
+    if (wchunk) {
+      if (z >= wlo[0] && z <= whi[0] && ra > best[2]) { best[2] = ra; bestz[2] = z; }
+      if (z >= wlo[1] && z <= whi[1] && rb > best[3]) { best[3] = rb; bestz[3] = z; }
+    }
+    const float oa = inA ? ra : 0.f;
+    const float ob = inB ? rb : 0.f;
+    const float ha = (__shfl_up_sync(kFull, oa, 1) + oa) + __shfl_down_sync(kFull, oa, 1);
+    const float hb = (__shfl_up_sync(kFull, ob, 1) + ob) + __shfl_down_sync(kFull, ob, 1);
+    Hx[zoff + zz][0][wp][lane] = ha;
+    Hx[zoff + zz][1][wp][lane] = hb;
+  }
+}
+
+template <int B, int DIR, int ZC, int NR, int MINB>
+__global__ void __launch_bounds__(NR * 32, MINB)
+sweep2_kernel(const SweepArgs a) {
+  using SM = Sweep2Smem<B, ZC, NR>;
+  constexpr int H2 = B / 2;
+  constexpr int NT = NR * 32;
+  constexpr int NROW = SM::NROW, RW = SM::RW, RR = SM::RR, SW = SM::SW, LC = SM::LC;
+  constexpr int KR = (RR * RW + NT - 1) / NT;
+  constexpr int KS = (NROW * SW + NT - 1) / NT;
+  extern __shared__ float4 smem4[];
+  typename SM::RsT* Rs = reinterpret_cast<typename SM::RsT*>(smem4);
+  typename SM::MsT* Ms = reinterpret_cast<typename SM::MsT*>(Rs + 2);
+  typename SM::HxT* Hx = reinterpret_cast<typename SM::HxT*>(Ms + 2);
+
+  const int lane = threadIdx.x & 31;
+  const int wp = threadIdx.x >> 5;
+  const int x0 = blockIdx.x * 30;
+  const int y0 = blockIdx.y * (NROW - 2);
+  const int iA = y0 - 1 + 2 * wp, iB = iA + 1;
+  const int j = x0 - 1 + lane;
+  const int H = a.H, W = a.W, d = a.d;
+  const bool colin = j >= 0 && j < W;
+  const bool inA = colin && iA >= 0 && iA < H;
+  const bool inB = colin && iB >= 0 && iB < H;
+  const bool lanein = lane >= 1 && lane <= 30;
+  const bool innerA = inA && lanein && wp >= 1;
+  const bool innerB = inB && lanein && wp <= NR - 2;
+  const float qnan = __int_as_float(0x7fc00000);
+
+  const double cR = a.R[(int64_t)clampi(y0 + NR - 1, 0, H - 1) * a.ld + clampi(x0 + 15, 0, W - 1)];
+  const float cRf = (float)cR;
+
+  double pr[KR];
+  float2 pm[KS];
+  auto fetch = [&](int z0) {
+    const int s0 = DIR > 0 ? (x0 - 1 - H2 - z0 - (ZC - 1)) : (x0 - 1 - H2 + z0);
+#pragma unroll
+    for (int k = 0; k < KR; ++k) {
+      const int t = threadIdx.x + k * NT;
+      if (t < RR * RW) {
+        const int rr = t / RW, e = t - rr * RW;
+        pr[k] = a.R[(int64_t)clampi(y0 - 1 - H2 + rr, 0, H - 1) * a.ld + clampi(s0 + e, 0, W - 1)];
+      }
+    }
+    const int q0 = DIR > 0 ? (x0 - 1 - z0 - (ZC - 1)) : (x0 - 1 + z0);
+#pragma unroll
+    for (int k = 0; k < KS; ++k) {
+      const int t = threadIdx.x + k * NT;
+      if (t < NROW * SW) {
+        const int rr = t / SW, e = t - rr * SW;
+        const int64_t o = (int64_t)clampi(y0 - 1 + rr, 0, H - 1) * a.lds + clampi(q0 + e, 0, W - 1);
+        pm[k] = make_float2(a.muR[o], a.isR[o]);   // raw; validity applied at store time
+      }
+    }
+  };
+  auto store = [&](int buf, int z0) {
+#pragma unroll
+    for (int k = 0; k < KR; ++k) {
+      const int t = threadIdx.x + k * NT;
+      if (t < RR * RW) {
+        const int rr = t / RW, e = t - rr * RW;
+        Rs[buf][rr][e] = (float)(pr[k] - cR);
+      }
+    }
+    const int q0 = DIR > 0 ? (x0 - 1 - z0 - (ZC - 1)) : (x0 - 1 + z0);
+#pragma unroll
+    for (int k = 0; k < KS; ++k) {
+      const int t = threadIdx.x + k * NT;
+      if (t < NROW * SW) {
+        const int rr = t / SW, e = t - rr * SW;
+        const int gq = q0 + e;
+        const bool valid = gq >= 0 && gq < W && pm[k].y > 0.f;
+        // (muR - c, 1/sigma_R); NaN marks a right centre outside the image or
+        // a degenerate right block: its cost becomes exactly -1 (fmaxf)
+        Ms[buf][rr][e] = make_float2(pm[k].x - cRf, valid ? pm[k].y : qnan);
+      }
+    }
+  };
+  fetch(0);
+
+  // ---- left tile (fp64) through shared memory (aliases Hx, written later)
+  using LsT = typename SM::LsT;
+  static_assert(sizeof(LsT) <= 2 * sizeof(typename SM::HxT), "left tile must fit");
+  LsT& Ls = *reinterpret_cast<LsT*>(Hx);
+  for (int t = threadIdx.x; t < RR * LC; t += NT) {
+    const int rr = t / LC, e = t - rr * LC;
+    Ls[rr][e] = a.L[(int64_t)clampi(y0 - 1 - H2 + rr, 0, H - 1) * a.ld +
+                    clampi(x0 - 1 - H2 + e, 0, W - 1)];
+  }
+  __syncthreads();
+
+  // ---- left windows: A centred by muA (rows 0..B-1), B's bottom row by muA
+  float Lt[B][B], Lb[B];
+  float kLA, kLB, dW;
+  {
+    const int r0 = 2 * wp;
+    double sA = 0.0, top = 0.0, bot = 0.0;
+#pragma unroll
+    for (int r = 0; r < B; ++r)
+#pragma unroll
+      for (int c = 0; c < B; ++c) sA += Ls[r0 + r][lane + c];
+#pragma unroll
+    for (int c = 0; c < B; ++c) top += Ls[r0][lane + c], bot += Ls[r0 + B][lane + c];
+    const double muA = sA / (double)(B * B);
+    const double muB = (sA - top + bot) / (double)(B * B);
+    double ssA = 0.0, ssB = 0.0;
+#pragma unroll
+    for (int r = 0; r < B; ++r)
+#pragma unroll
+      for (int c = 0; c < B; ++c) {
+        const double v = Ls[r0 + r][lane + c];
+        const double da = v - muA;
+        ssA = fma(da, da, ssA);
+        Lt[r][c] = (float)da;
+      }
+#pragma unroll
+    for (int r = 1; r <= B; ++r)
+#pragma unroll
+      for (int c = 0; c < B; ++c) {
+        const double db = Ls[r0 + r][lane + c] - muB;
+        ssB = fma(db, db, ssB);
+      }
+#pragma unroll
+    for (int c = 0; c < B; ++c) Lb[c] = (float)(Ls[r0 + B][lane + c] - muA);
+    const double sgA = sqrt(ssA / (double)(B * B)), sgB = sqrt(ssB / (double)(B * B));
+    kLA = (inA && sgA >= a.sigma_eps) ? (float)(1.0 / ((double)(B * B) * sgA)) : qnan;
+    kLB = (inB && sgB >= a.sigma_eps) ? (float)(1.0 / ((double)(B * B) * sgB)) : qnan;
+    dW = (float)((double)(B * B) * (muA - muB));
+  }
+
+  // ---- prior windows of A and B
+  bool trusted[2] = {false, false};
+  int wlo[2] = {1, 1}, whi[2] = {0, 0};
+  if (a.wc != nullptr) {
+    const bool inn[2] = {innerA, innerB};
+    const int ii[2] = {iA, iB};
+#pragma unroll
+    for (int p = 0; p < 2; ++p) {
+      if (inn[p]) {
+        const int c = a.wc[(int64_t)ii[p] * a.ldw + j];
+        if (c != kWcNone) {
+          trusted[p] = true;
+          wlo[p] = max(c - a.radius, 0);
+          whi[p] = min(c + a.radius, d);
+        }
+      }
+    }
+  }
+
+  const int zmax = min(d, DIR > 0 ? (x0 + 30) : (W - x0));
+  // best[0..1]: full range A/B, best[2..3]: window A/B; nbv/nbz: 3x3 sums
+  float best[4] = {-2.f, -2.f, -2.f, -2.f};
+  int bestz[4] = {0, 0, wlo[0], wlo[1]};
+  float nbv[2] = {-3.0e38f, -3.0e38f};
+  int nbz[2] = {0, 0};
+
+  store(0, 0);
+  __syncthreads();
+  int cur = 0;
+  for (int z0 = 0; z0 <= zmax; z0 += ZC, cur ^= 1) {
+    const bool more = z0 + ZC <= zmax;
+    if (more) fetch(z0 + ZC);
+    const bool wchunk = __any_sync(kFull, (trusted[0] && wlo[0] <= z0 + ZC - 1 && whi[0] >= z0) ||
+                                             (trusted[1] && wlo[1] <= z0 + ZC - 1 && whi[1] >= z0));
+    int nz;
+    if (z0 + ZC - 1 <= zmax) {
+      chunk2<B, DIR, ZC, NR, ZC>(Rs[cur], Ms[cur], Hx[cur], Lt, Lb, kLA, kLB, dW, z0, 0, zmax,
+                                 inA, inB, lane, wp, best, bestz, wchunk, wlo, whi);
+      nz = ZC;
+    } else {
+      nz = zmax - z0 + 1;
+      for (int zo = 0; zo < nz; zo += 4)
+        chunk2<B, DIR, ZC, NR, 4>(Rs[cur], Ms[cur], Hx[cur], Lt, Lb, kLA, kLB, dW, z0, zo, zmax,
+                                  inA, inB, lane, wp, best, bestz, wchunk, wlo, whi);
+    }
+    if (more) store(cur ^ 1, z0 + ZC);
+    __syncthreads();
+    const typename SM::HxT& hx = Hx[cur];
+    if (innerA) {
+#pragma unroll
+      for (int zz = 0; zz < ZC; ++zz) {
+        const float nb = (hx[zz][1][wp - 1][lane] + hx[zz][0][wp][lane]) + hx[zz][1][wp][lane];
+        if (zz < nz && nb > nbv[0]) { nbv[0] = nb; nbz[0] = z0 + zz; }
+      }
+    }
+    if (innerB) {
+#pragma unroll
+      for (int zz = 0; zz < ZC; ++zz) {
+        const float nb = (hx[zz][0][wp][lane] + hx[zz][1][wp][lane]) + hx[zz][0][wp + 1][lane];
+        if (zz < nz && nb > nbv[1]) { nbv[1] = nb; nbz[1] = z0 + zz; }
+      }
+    }
+  }
+
+  // ---- epilogue: the reference's gates, per pixel
+  const bool inner[2] = {innerA, innerB};
+  const int ii[2] = {iA, iB};
+  unsigned nlow = 0;
+#pragma unroll
+  for (int p = 0; p < 2; ++p) {
+    const int i = ii[p];
+    float bw = best[2 + p];
+    if (trusted[p] && bw == -2.f) bw = -1.f;   // window beyond zmax: all -1
+    const int members = ((i > 0) + 1 + (i < H - 1)) * ((j > 0) + 1 + (j < W - 1));
+    bool low = false;
+    if (a.mode == kSweepPipeline) {
+      if (inner[p]) {
+        const float cs = trusted[p] ? bw : best[p];
+        const int zs = trusted[p] ? bestz[2 + p] : bestz[p];
+        low = (double)cs <= a.alpha;
+        const int64_t o = (int64_t)i * a.ldo + j;
+        a.dout[o] = (int16_t)(low ? nbz[p] : zs);
+        a.cout[o] = low ? nbv[p] / (float)members : cs;
+        a.low[o] = (uint8_t)low;
+      }
+      nlow += low ? 1u : 0u;
+    } else if (inner[p]) {
+      const int64_t o = (int64_t)i * W + j;
+      a.fz[o] = (int16_t)bestz[p];
+      a.fc[o] = best[p];
+      if (a.wz) { a.wz[o] = (int16_t)bestz[2 + p]; a.wcst[o] = trusted[p] ? bw : -2.f; }
+      a.nz[o] = (int16_t)nbz[p];
+      a.nc[o] = nbv[p] / (float)members;
+    }
+  }
+  if (a.mode == kSweepPipeline) {
+    const int slot[1] = {kCntRefined};
+    const unsigned long long val[1] = {nlow};
+    const bool mx[1] = {false};
+    block_accumulate<1>(a.counters, slot, val, mx);
+  }
+}
+
+template <int B, int DIR, int ZC, int NR, int MINB>
+cudaError_t launch2(const SweepArgs& a, cudaStream_t s) {
+  constexpr size_t smem = Sweep2Smem<B, ZC, NR>::bytes();
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(sweep2_kernel<B, DIR, ZC, NR, MINB>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  constexpr int NROW = 2 * NR;
+  dim3 grid((a.W + 29) / 30, (a.H + NROW - 3) / (NROW - 2));
+  sweep2_kernel<B, DIR, ZC, NR, MINB><<<grid, NR * 32, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
+int g_v2 = -1;
+int v2() {
+  if (g_v2 < 0) {
+    const char* v = getenv("MSHBM_SWEEP2_VARIANT");
+    g_v2 = v ? atoi(v) : 0;
+  }
+  return g_v2;
+}
+
+template <int DIR>
+cudaError_t launch2_dir(const SweepArgs& a, cudaStream_t s) {
+  if (DIR > 0) {
+    switch (v2() * 100 + a.block) {
+      case 107: return launch2<7, DIR, 16, 8, 2>(a, s);
+      case 207: return launch2<7, DIR, 16, 8, 1>(a, s);
+      case 109: return launch2<9, DIR, 8, 8, 2>(a, s);
+      case 209: return launch2<9, DIR, 12, 8, 1>(a, s);
+      case 105: return launch2<5, DIR, 24, 8, 2>(a, s);
+      case 103: return launch2<3, DIR, 24, 8, 2>(a, s);
+      default: break;
+    }
+  }
+  switch (a.block) {
+    case 3: return launch2<3, DIR, 16, 8, 2>(a, s);
+    case 5: return launch2<5, DIR, 16, 8, 2>(a, s);
+    case 7: return launch2<7, DIR, 12, 8, 2>(a, s);
+    case 9: return launch2<9, DIR, 16, 8, 1>(a, s);
+    case 11: return launch2<11, DIR, 16, 8, 1>(a, s);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace
+
+bool sweep2_supported(int b) { return b == 3 || b == 5 || b == 7 || b == 9 || b == 11; }
+
+cudaError_t launch_sweep2(const SweepArgs& a, cudaStream_t s) {
+  return a.dir > 0 ? launch2_dir<1>(a, s) : launch2_dir<-1>(a, s);
+}
+
+}  // namespace mshbm
