@@ -172,6 +172,113 @@ def run_reference(args, cfg):
 
 
 # --------------------------------------------------------------------- ours
+class Workload:
+    """One bench step of a BASELINE config on this rank.
+
+    C1/C2/C3 (weak): every rank matches its own pair (seed + rank).
+    C4 (strong): the 64-pair batch is sharded round-robin over the ranks;
+        each rank runs its pairs through mshbm_run_batch.
+    C5 (strong): one pair split into 2^K-aligned row bands, one per rank
+        (mshbm_run_pipeline_band), bands gathered to rank 0 over NCCL.
+    """
+
+    def __init__(self, cfg, gpu, lib, dev, ws, rank):
+        import torch
+        self.cfg, self.gpu, self.lib, self.dev, self.ws, self.rank = cfg, gpu, lib, dev, ws, rank
+        self.mc = gpu.MatchConfig(d_max=cfg.d_max, levels=cfg.levels, block=cfg.block,
+                                  radius=cfg.radius)
+        self.ctx = lib.context(dev.index)
+        H, W = cfg.height, cfg.width
+        if cfg.name == "C4":
+            self.kind, self.scaling = "batch", "strong"
+            self.pairs = gpu.sharding.shard_pairs(cfg.batch, ws, rank)
+            imgs = [make_pair(cfg, seed=cfg.seed + i) for i in self.pairs]
+            self.host_l = torch.stack([torch.from_numpy(x[0]) for x in imgs]).pin_memory()
+            self.host_r = torch.stack([torch.from_numpy(x[1]) for x in imgs]).pin_memory()
+            self.L, self.R = self.host_l.to(dev), self.host_r.to(dev)
+            self.units = cfg.batch * cfg.full_search_pde
+            self.pairs_per_step = cfg.batch
+            n = len(self.pairs)
+            self.host_d = torch.empty((n, H, W), dtype=torch.int16).pin_memory()
+            self.host_c = torch.empty((n, H, W), dtype=torch.float32).pin_memory()
+            self.h2d = n * 2 * H * W * 4
+            self.d2h = n * H * W * 6
+            self.left, self.right = imgs[0][0], imgs[0][1]
+        elif cfg.name == "C5":
+            self.kind, self.scaling = "bands", "strong"
+            self.left, self.right, _ = make_pair(cfg)
+            self.bands = gpu.sharding.plan_bands(H, ws, cfg.levels)
+            self.b0, self.b1 = self.bands[rank]
+            self.host_l = torch.from_numpy(self.left).pin_memory()
+            self.host_r = torch.from_numpy(self.right).pin_memory()
+            self.L, self.R = self.host_l.to(dev), self.host_r.to(dev)
+            self.units = cfg.full_search_pde
+            self.pairs_per_step = 1
+            rows = self.b1 - self.b0
+            self.host_d = torch.empty((rows, W), dtype=torch.int16).pin_memory()
+            self.host_c = torch.empty((rows, W), dtype=torch.float32).pin_memory()
+            self.h2d = 2 * H * W * 4
+            self.d2h = rows * W * 6
+        else:
+            self.kind, self.scaling = "pair", "weak"
+            self.left, self.right, _ = make_pair(cfg, seed=cfg.seed + rank)
+            self.host_l = torch.from_numpy(self.left).pin_memory()
+            self.host_r = torch.from_numpy(self.right).pin_memory()
+            self.L, self.R = self.host_l.to(dev), self.host_r.to(dev)
+            self.units = ws * cfg.full_search_pde
+            self.pairs_per_step = ws
+            self.host_d = torch.empty((H, W), dtype=torch.int16).pin_memory()
+            self.host_c = torch.empty((H, W), dtype=torch.float32).pin_memory()
+            self.h2d = 2 * H * W * 4
+            self.d2h = H * W * 6
+
+    def parallelism(self):
+        return {"pair": f"independent pairs, one per rank x{self.ws}",
+                "batch": f"{self.cfg.batch} pairs sharded round-robin over {self.ws} rank(s)",
+                "bands": f"row bands x{self.ws} (2^K-aligned), NCCL gather"}[self.kind]
+
+    def step(self):
+        """Device-resident step (inputs already in HBM)."""
+        gpu = self.gpu
+        if self.kind == "pair":
+            gpu.run_pipeline_device(self.L, self.R, self.mc, trace=False)
+        elif self.kind == "batch":
+            gpu.run_batch(self.L, self.R, self.mc, n_streams=4, trace=False)
+        else:
+            if self.ws == 1:
+                gpu.run_pipeline_device(self.L, self.R, self.mc, trace=False)
+            else:
+                d, c, _ = gpu.run_pipeline_band(self.L, self.R, self.mc, self.b0, self.b1,
+                                                trace=False)
+                gpu.sharding.gather_bands(d, self.bands, self.rank, self.ws)
+                gpu.sharding.gather_bands(c, self.bands, self.rank, self.ws)
+
+    def step_e2e(self, stream):
+        """The same step through the C ABI from pinned host buffers."""
+        lib, cfg = self.lib, self.cfg
+        H, W = cfg.height, cfg.width
+        cc = self.mc.to_c()
+        sptr = C.c_void_p(stream.cuda_stream)
+        if self.kind == "pair" or (self.kind == "bands" and self.ws == 1):
+            st = lib.lib().mshbm_run_pipeline(self.ctx, self.host_l.data_ptr(),
+                                              self.host_r.data_ptr(), H, W, W, C.byref(cc),
+                                              self.host_d.data_ptr(), self.host_c.data_ptr(),
+                                              W, None, None, lib.IO_HOST, 0, sptr)
+        elif self.kind == "batch":
+            n = len(self.pairs)
+            ptrs = lambda t: (C.c_void_p * n)(*[t[i].data_ptr() for i in range(n)])  # noqa: E731
+            st = lib.lib().mshbm_run_batch(self.ctx, n, ptrs(self.host_l), ptrs(self.host_r), H,
+                                           W, W, C.byref(cc), ptrs(self.host_d),
+                                           ptrs(self.host_c), W, None, lib.IO_HOST, 4, sptr)
+        else:
+            st = lib.lib().mshbm_run_pipeline_band(self.ctx, self.host_l.data_ptr(),
+                                                   self.host_r.data_ptr(), H, W, W, C.byref(cc),
+                                                   self.b0, self.b1, self.host_d.data_ptr(),
+                                                   self.host_c.data_ptr(), W, None, None,
+                                                   lib.IO_HOST, 0, sptr)
+        lib.check(st, self.ctx)
+
+
 def run_ours(args, cfg):
     import torch
     import torch.distributed as dist
@@ -186,12 +293,7 @@ def run_ours(args, cfg):
     from paper_1901_09593_b200 import _lib
 
     gpu.matcher.STAGE_TIMING = False
-    seed = cfg.seed + rank
-    left, right, _ = make_pair(cfg, seed=seed)
-    lt = torch.from_numpy(left).to(dev)
-    rt = torch.from_numpy(right).to(dev)
-    mc = gpu.MatchConfig(d_max=cfg.d_max, levels=cfg.levels, block=cfg.block,
-                         radius=cfg.radius)
+    wl = Workload(cfg, gpu, _lib, dev, ws, rank)
     stream = torch.cuda.current_stream(dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
@@ -200,11 +302,20 @@ def run_ours(args, cfg):
             dist.barrier()
         torch.cuda.synchronize(dev)
 
-    # trace of this pair (exact counters): evaluated PDE count, level-0 work
-    _, _, trace = gpu.run_pipeline_device(lt, rt, mc, trace=True)
+    def max_over_ranks(v):
+        if ws == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # exact counters of one pair of the workload (evaluated PDEs, level-0 work)
+    lt = torch.from_numpy(wl.left).to(dev)
+    rt = torch.from_numpy(wl.right).to(dev)
+    _, _, trace = gpu.run_pipeline_device(lt, rt, wl.mc, trace=True)
     l0 = trace.levels[-1]
     for _ in range(args.warmup):
-        gpu.run_pipeline_device(lt, rt, mc, trace=False)
+        wl.step()
     barrier()
 
     # ---- device-resident timed region
@@ -217,59 +328,35 @@ def run_ours(args, cfg):
         for k in range(args.steps):
             flush.fill_(k & 0xFF)
             ev[k][0].record(stream)
-            gpu.run_pipeline_device(lt, rt, mc, trace=False)
+            wl.step()
             ev[k][1].record(stream)
         barrier()
     launches = int(_lib.lib().mshbm_launch_count(ctx) - n0)
-    ms_steps = [a.elapsed_time(b) for a, b in ev]
-    ms = sum(ms_steps) / len(ms_steps)
-    if ws > 1:
-        t = torch.tensor([ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
-    value = ws * cfg.full_search_pde / (ms * 1e-3) / 1e6
+    ms = max_over_ranks(sum(a.elapsed_time(b) for a, b in ev) / args.steps)
+    value = wl.units / (ms * 1e-3) / 1e6
 
     # ---- end to end through the C ABI with host buffers (pinned)
-    hl = torch.from_numpy(left).pin_memory()
-    hr = torch.from_numpy(right).pin_memory()
-    hd = torch.empty((cfg.height, cfg.width), dtype=torch.int16).pin_memory()
-    hc = torch.empty((cfg.height, cfg.width), dtype=torch.float32).pin_memory()
-    cc = mc.to_c()
-    sptr = C.c_void_p(stream.cuda_stream)
-
-    def e2e_call():
-        st = _lib.lib().mshbm_run_pipeline(ctx, hl.data_ptr(), hr.data_ptr(), cfg.height,
-                                           cfg.width, cfg.width, C.byref(cc), hd.data_ptr(),
-                                           hc.data_ptr(), cfg.width, None, None,
-                                           _lib.IO_HOST, 0, sptr)
-        _lib.check(st, ctx)
-
     for _ in range(max(1, args.warmup)):
-        e2e_call()
+        wl.step_e2e(stream)
     barrier()
+    e2e_steps = max(3, min(args.steps, 50))
     eev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-           for _ in range(args.steps)]
-    for k in range(args.steps):
+           for _ in range(e2e_steps)]
+    for k in range(e2e_steps):
         flush.fill_(k & 0xFF)
         eev[k][0].record(stream)
-        e2e_call()
+        wl.step_e2e(stream)
         eev[k][1].record(stream)
     barrier()
-    ems = sum(a.elapsed_time(b) for a, b in eev) / args.steps
-    if ws > 1:
-        t = torch.tensor([ems], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ems = float(t.item())
-    e2e_value = ws * cfg.full_search_pde / (ems * 1e-3) / 1e6
-    h2d = 2 * cfg.width * cfg.height * 4
-    d2h = cfg.width * cfg.height * (2 + 4)
+    ems = max_over_ranks(sum(a.elapsed_time(b) for a, b in eev) / e2e_steps)
+    e2e_value = wl.units / (ems * 1e-3) / 1e6
 
     # ---- roofline of the dominant kernel (level-0 sweep), live CUDA events
     gpu.matcher.STAGE_TIMING = True
     sweep_ms = []
-    for _ in range(5):
+    for _ in range(3 if cfg.name == "C5" else 5):
         flush.fill_(1)
-        _, _, tt = gpu.run_pipeline(left, right, mc)
+        _, _, tt = gpu.run_pipeline(wl.left, wl.right, wl.mc)
         sweep_ms.append(tt.levels[-1].seconds["select"] * 1e3)
     sweep_ms = statistics.median(sweep_ms)
     tf = C.c_double()
@@ -278,15 +365,17 @@ def run_ours(args, cfg):
     alg_flops = l0.evals * flops_per_pde(l0.block)
     achieved = alg_flops / (sweep_ms * 1e-3) / 1e12
     dense_flops = l0.pixels * (l0.d_max + 1) * flops_per_pde(l0.block)
-    roof = {"bound": "fp32", "kernel": "sweep_kernel<b=%d> (level 0)" % l0.block,
+    per_pair_ms = ms / max(1, wl.pairs_per_step / ws) if wl.kind != "bands" else ms
+    roof = {"bound": "fp32", "kernel": "sweep2_kernel<b=%d> (level 0)" % l0.block,
             "achieved": achieved, "peak": tf.value, "unit": "TFLOP/s",
-            "frac": achieved / tf.value, "traffic": None,
+            "frac": achieved / tf.value, "traffic": TRAFFIC.get(cfg.name),
             "peak_source": "measured live: mshbm_probe_fp32_peak FFMA probe on this GPU "
                            "(MEASURED_PEAKS.json has no FP32 figure)",
             "algorithmic_flops_per_launch": alg_flops,
             "algorithmic_basis": "level-0 trace evals (selection_evals + refine_evals) "
                                  "x F(b)=2b^2+8 (SURVEY 8d)",
-            "launch_ms": sweep_ms, "share_of_step": sweep_ms / ms,
+            "launch_ms": sweep_ms,
+            "share_of_step": sweep_ms / per_pair_ms if wl.kind != "bands" or ws == 1 else None,
             "dense_pde_flops_per_launch": dense_flops,
             "dense_achieved": dense_flops / (sweep_ms * 1e-3) / 1e12}
 
@@ -295,17 +384,19 @@ def run_ours(args, cfg):
         out = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "f32", "data": f"synthetic BASELINE generator ({cfg.name}), seed "
-                                    f"{cfg.seed}+rank; L2 flushed (256 MiB) between steps",
-            "config": dict(workload_desc(cfg), parallelism=f"pair-parallel x{ws}",
+            "higher_is_better": True, "scaling": wl.scaling, "vs_baseline": None,
+            "dtype": "f32", "data": f"synthetic BASELINE generator ({cfg.name}), seeds "
+                                    f"{cfg.seed}+; L2 flushed (256 MiB) between steps",
+            "config": dict(workload_desc(cfg), parallelism=wl.parallelism(),
                            l2="flushed between timed steps"),
-            "pairs_per_s": ws / (ms * 1e-3),
-            "evaluated_mpd_per_s": ws * trace.total_evals / (ms * 1e-3) / 1e6,
+            "pairs_per_s": wl.pairs_per_step / (ms * 1e-3),
+            "evaluated_mpd_per_s": (wl.units / cfg.full_search_pde) * trace.total_evals
+                                   / (ms * 1e-3) / 1e6,
             "total_evals_per_pair": trace.total_evals,
-            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
-                    "d2h_bytes_per_step": d2h, "ms_per_step": ems,
-                    "path": "mshbm_run_pipeline(MSHBM_IO_HOST) from pinned host buffers"},
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": wl.h2d,
+                    "d2h_bytes_per_step": wl.d2h, "ms_per_step": ems,
+                    "path": "C ABI (mshbm_run_pipeline / _batch / _band, MSHBM_IO_HOST) "
+                            "from pinned host buffers"},
             "roofline": roof,
             "gpu_launches": launches,
             "clocks": clocks.summary(),
@@ -325,10 +416,15 @@ def run_ours(args, cfg):
         print(json.dumps(out), flush=True)
 
 
+# dram__bytes_read.sum + dram__bytes_write.sum of the level-0 sweep launch from
+# the committed ncu --set full captures (profiles/), per config
+TRAFFIC = {"C2": 40962304 + 112896}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--steps", type=int, default=None)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--config", default="C2", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
@@ -336,6 +432,8 @@ def main():
     args = ap.parse_args()
     args.warmup = max(3, args.warmup) if args.impl == "ours" else args.warmup
     cfg = CONFIGS[args.config]
+    if args.steps is None:   # a timed region of roughly 0.3-2 s per config
+        args.steps = {"C1": 400, "C2": 200, "C3": 40, "C4": 20, "C5": 10}[cfg.name]
     if args.impl == "reference":
         run_reference(args, cfg)
     else:

@@ -120,6 +120,35 @@ int mshbm_run_pipeline(mshbm_ctx* ctx, const float* left, const float* right,
                        int32_t* out_levels, int32_t io, int32_t flags,
                        void* stream);
 
+/* Row band of run_pipeline for multi-GPU partitioning of one large pair
+ * (SURVEY 8e, config C5).  Produces level-0 rows [row_begin, row_end)
+ * bit-identical to the whole-image call: the cheap pyramid, statistics and
+ * levels >= 2 run on the whole image, levels 0/1 sweep only the band plus
+ * exact halos.  row_begin/row_end must be multiples of 2^K (row_end may be
+ * H).  disparity/cost receive (row_end - row_begin) rows; trace counters
+ * cover only the band's own rows at every level (row_begin>>k .. row_end>>k),
+ * so the traces of a partition of bands sum to the whole-image trace
+ * (trusted_window_max: take the max). */
+int mshbm_run_pipeline_band(mshbm_ctx* ctx, const float* left, const float* right,
+                            int32_t height, int32_t width, int64_t ld,
+                            const mshbm_config* cfg, int32_t row_begin,
+                            int32_t row_end, int16_t* disparity, float* cost,
+                            int64_t ld_out, mshbm_level_trace* trace,
+                            int32_t* out_levels, int32_t io, int32_t flags,
+                            void* stream);
+
+/* Batch of n independent same-shape pairs (config C4): pairs run
+ * round-robin on n_streams concurrent CUDA-graph plans (<= 0: 4).  Arrays of
+ * n pointers (host or device per `io`); traces: n * (K+1) entries or NULL.
+ * Ordered after prior work on `stream`; the call returns with all pairs
+ * complete on `stream` (synchronous for host I/O or traces). */
+int mshbm_run_batch(mshbm_ctx* ctx, int32_t n_pairs, const float* const* lefts,
+                    const float* const* rights, int32_t height, int32_t width,
+                    int64_t ld, const mshbm_config* cfg,
+                    int16_t* const* disparities, float* const* costs,
+                    int64_t ld_out, mshbm_level_trace* traces, int32_t io,
+                    int32_t n_streams, void* stream);
+
 /* run_pipeline(..., pyramid=...) with a caller-built pyramid (matcher.py:
  * 410-416): n_levels float64 device levels, level k has dims heights[k] x
  * widths[k] (dyadic), stride lds[k], search bound d_maxs[k], block blocks[k]. */

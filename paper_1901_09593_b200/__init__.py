@@ -15,7 +15,9 @@ from .matcher import (
     match_coarsest,
     match_level_with_prior,
     refine_level,
+    run_batch,
     run_pipeline,
+    run_pipeline_band,
     run_pipeline_device,
     select_with_prior,
     selective_median,
@@ -44,6 +46,8 @@ from .zncc import (
     zncc,
 )
 
+from . import sharding  # noqa: E402
+
 __version__ = "0.1.0"
 
 __all__ = [
@@ -52,7 +56,7 @@ __all__ = [
     "SIGN_MIDDLEBURY", "SIGN_PAPER_PLUS", "SelectionStats", "StereoPyramid",
     "auto_levels", "averaged_dsi", "build_pyramid", "dsi_entry",
     "gaussian_downsample", "level_block", "level_d_max", "match_coarsest",
-    "match_level_with_prior", "patch_stats", "refine_level", "run_pipeline",
-    "run_pipeline_device", "select_with_prior", "selective_median",
+    "match_level_with_prior", "patch_stats", "refine_level", "run_batch",
+    "run_pipeline", "run_pipeline_band", "run_pipeline_device", "select_with_prior", "selective_median",
     "upsample_prior", "zncc",
 ]

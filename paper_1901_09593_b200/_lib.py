@@ -59,6 +59,10 @@ SIGNATURES = {
     "mshbm_downsample": (C.c_int, [P, P, I32, I32, I64, P, I64, P]),
     "mshbm_run_pipeline": (C.c_int, [P, P, P, I32, I32, I64, C.POINTER(Config), P, P, I64,
                                      P, C.POINTER(I32), I32, I32, P]),
+    "mshbm_run_pipeline_band": (C.c_int, [P, P, P, I32, I32, I64, C.POINTER(Config), I32, I32, P,
+                                          P, I64, P, C.POINTER(I32), I32, I32, P]),
+    "mshbm_run_batch": (C.c_int, [P, I32, P, P, I32, I32, I64, C.POINTER(Config), P, P, I64, P,
+                                  I32, I32, P]),
     "mshbm_run_pyramid": (C.c_int, [P, I32, P, P, P, P, P, P, P, C.POINTER(Config), P, P,
                                     I64, P, P]),
     "mshbm_engine_create": (C.c_int, [P, P, P, I32, I32, I64, I32, I32, D, I32, C.POINTER(P)]),

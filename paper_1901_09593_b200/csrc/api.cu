@@ -37,17 +37,19 @@ struct LevelBuf {
   uint8_t* low = nullptr;
   double* coef = nullptr;   // spline coefficients of this level's cost map
   int64_t ldc = 0;
+  RowBand rows{0, 0, 0, 0};  // sweep/prior/median rows and counted rows
 };
 
 struct PlanKey {
-  int H, W, K, user;
+  int H, W, K, user, band_lo, band_hi, slot;
   int d_max, block, radius, sign;
   double alpha, beta, eps;
   std::vector<int> lvl;     // per-level (h, w, d, b) for user pyramids
   bool operator<(const PlanKey& o) const {
-    return std::tie(H, W, K, user, d_max, block, radius, sign, alpha, beta, eps, lvl) <
-           std::tie(o.H, o.W, o.K, o.user, o.d_max, o.block, o.radius, o.sign, o.alpha,
-                    o.beta, o.eps, o.lvl);
+    return std::tie(H, W, K, user, band_lo, band_hi, slot, d_max, block, radius, sign, alpha,
+                    beta, eps, lvl) <
+           std::tie(o.H, o.W, o.K, o.user, o.band_lo, o.band_hi, o.slot, o.d_max, o.block,
+                    o.radius, o.sign, o.alpha, o.beta, o.eps, o.lvl);
   }
 };
 
@@ -64,6 +66,8 @@ struct Plan {
   void* arena = nullptr;
   cudaGraphExec_t exec = nullptr;
   int launches = 0;
+  cudaStream_t stream = nullptr;   // batch slot stream (run_batch)
+  cudaEvent_t done = nullptr;
 };
 
 }  // namespace
@@ -182,10 +186,35 @@ int build_plan(mshbm_ctx* ctx, Plan& p) {
   Carver probe;
   carve(p, probe);
   CK(cudaMalloc(&p.arena, probe.off + 256));
+  // finite contents everywhere: band runs prefilter rows they never sweep
+  CK(cudaMemset(p.arena, 0, probe.off + 256));
   Carver real;
   real.base = (char*)p.arena;
   carve(p, real);
   return MSHBM_OK;
+}
+
+// Row ranges per level for a level-0 band [b0, b1) (whole image: b0=0,
+// b1=H).  Level k sweeps rows S_k; level k+1 must provide exact disparities
+// for rows S_k/2 and exact costs within the 66-row reach of the tiled
+// spline prefilter + support around them.
+void plan_rows(Plan& p, int b0, int b1) {
+  const int K = p.K;
+  for (int k = 0; k <= K; ++k) {
+    LevelBuf& l = p.lv[k];
+    const int own_lo = b0 >> k;
+    const int own_hi = (b1 >= p.H) ? l.h : std::min(l.h, b1 >> k);
+    if (k == 0) {
+      l.rows.lo = std::max(0, b0 - 2);
+      l.rows.hi = std::min(l.h, b1 + 2);
+    } else {
+      const RowBand& f = p.lv[k - 1].rows;
+      l.rows.lo = std::max(0, (f.lo >> 1) - 66);
+      l.rows.hi = std::min(l.h, (f.hi >> 1) + 67);
+    }
+    l.rows.cnt_lo = own_lo;
+    l.rows.cnt_hi = own_hi;
+  }
 }
 
 struct StageEvents {
@@ -223,7 +252,7 @@ int enqueue(mshbm_ctx* ctx, Plan& p, cudaStream_t s, std::vector<StageEvents>* t
       CK(launch_bspline_prefilter(c.c, nullptr, c.h, c.w, c.ld, c.coef, c.ldc, s));
       n += 1;
       CK(launch_prior_eval(c.dmed, c.ld, c.h, c.w, c.coef, c.ldc, l.h, l.w, l.d, cfg.radius,
-                           cfg.beta, l.wc, l.ld, cnt, s));
+                           cfg.beta, l.wc, l.ld, cnt, l.rows, s));
       ++n;
     }
     if (ev) CK(cudaEventRecord(ev->up1, s));
@@ -236,11 +265,13 @@ int enqueue(mshbm_ctx* ctx, Plan& p, cudaStream_t s, std::vector<StageEvents>* t
     a.alpha = cfg.alpha; a.mode = kSweepPipeline;
     a.dout = l.dsel; a.cout = l.c; a.low = l.low; a.ldo = l.ld;
     a.counters = cnt;
+    a.rows = l.rows;
     if (ev) CK(cudaEventRecord(ev->sel0, s));
     CK(launch_sweep(a, s, &n));
     if (ev) CK(cudaEventRecord(ev->sel1, s));
     if (ev) CK(cudaEventRecord(ev->med0, s));
-    CK(launch_median_pipeline(l.dsel, l.c, l.low, l.ld, l.h, l.w, cfg.alpha, l.dmed, cnt, s));
+    CK(launch_median_pipeline(l.dsel, l.c, l.low, l.ld, l.h, l.w, cfg.alpha, l.dmed, cnt, l.rows,
+                              s));
     ++n;
     if (ev) CK(cudaEventRecord(ev->med1, s));
   }
@@ -273,6 +304,7 @@ Plan* get_plan(mshbm_ctx* ctx, const PlanKey& key, const mshbm_config& cfg,
     delete p;
     return nullptr;
   }
+  plan_rows(*p, key.band_lo, key.band_hi);
   ctx->plans[key] = p;
   return p;
 }
@@ -312,13 +344,10 @@ int launch_plan(mshbm_ctx* ctx, Plan& p, cudaStream_t s, int flags,
   return MSHBM_OK;
 }
 
-// Copy the device counters back (synchronises `s`) and pack the trace
-// exactly as run_pipeline fills LevelTrace (matcher.py:377-463, A.10).
-int finish_trace(mshbm_ctx* ctx, Plan& p, cudaStream_t s, mshbm_level_trace* trace,
-                 std::vector<StageEvents>* tev) {
-  std::vector<unsigned long long> h((size_t)(p.K + 1) * kCntSlots);
-  CK(cudaMemcpyAsync(h.data(), p.counters, h.size() * sizeof(h[0]), cudaMemcpyDeviceToHost, s));
-  CK(cudaStreamSynchronize(s));
+// Pack host copies of the device counters into LevelTrace records exactly as
+// run_pipeline fills them (matcher.py:377-463).
+void pack_trace(const Plan& p, const unsigned long long* h, mshbm_level_trace* trace,
+                std::vector<StageEvents>* tev) {
   for (int t = 0; t <= p.K; ++t) {
     const int k = p.K - t;
     const LevelBuf& l = p.lv[k];
@@ -330,7 +359,7 @@ int finish_trace(mshbm_ctx* ctx, Plan& p, cudaStream_t s, mshbm_level_trace* tra
     o.width = l.w;
     o.d_max = l.d;
     o.block = l.b;
-    const int64_t N = (int64_t)l.h * l.w;
+    const int64_t N = (int64_t)(l.rows.cnt_hi - l.rows.cnt_lo) * l.w;
     if (k == p.K) {
       o.full_search_pixels = N;
       o.selection_evals = N * (l.d + 1);
@@ -358,6 +387,15 @@ int finish_trace(mshbm_ctx* ctx, Plan& p, cudaStream_t s, mshbm_level_trace* tra
       o.ms_median = ms;
     }
   }
+}
+
+// Copy the device counters back (synchronises `s`) and pack the trace.
+int finish_trace(mshbm_ctx* ctx, Plan& p, cudaStream_t s, mshbm_level_trace* trace,
+                 std::vector<StageEvents>* tev) {
+  std::vector<unsigned long long> h((size_t)(p.K + 1) * kCntSlots);
+  CK(cudaMemcpyAsync(h.data(), p.counters, h.size() * sizeof(h[0]), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  pack_trace(p, h.data(), trace, tev);
   return MSHBM_OK;
 }
 
@@ -372,7 +410,7 @@ void destroy_events(std::vector<StageEvents>& tev) {
 // inputs (optional) -> plan -> outputs (+ trace).  Host I/O synchronises.
 int run_plan_io(mshbm_ctx* ctx, Plan* p, const float* left, const float* right, int64_t ld,
                 int16_t* disparity, float* cost, int64_t ld_out, mshbm_level_trace* trace,
-                int32_t io, int32_t flags, cudaStream_t s) {
+                int32_t io, int32_t flags, cudaStream_t s, bool allow_sync = true) {
   const bool host = io == MSHBM_IO_HOST;
   const cudaMemcpyKind kin = host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
   const cudaMemcpyKind kout = host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
@@ -388,12 +426,15 @@ int run_plan_io(mshbm_ctx* ctx, Plan* p, const float* left, const float* right, 
     return st;
   }
   const LevelBuf& l0 = p->lv[0];
+  const int r0 = l0.rows.cnt_lo, nr = l0.rows.cnt_hi - l0.rows.cnt_lo;
   if (disparity)
-    CK(cudaMemcpy2DAsync(disparity, ld_out * 2, l0.dmed, l0.ld * 2, (size_t)l0.w * 2, l0.h, kout, s));
+    CK(cudaMemcpy2DAsync(disparity, ld_out * 2, l0.dmed + (int64_t)r0 * l0.ld, l0.ld * 2,
+                         (size_t)l0.w * 2, nr, kout, s));
   if (cost)
-    CK(cudaMemcpy2DAsync(cost, ld_out * 4, l0.c, l0.ld * 4, (size_t)l0.w * 4, l0.h, kout, s));
+    CK(cudaMemcpy2DAsync(cost, ld_out * 4, l0.c + (int64_t)r0 * l0.ld, l0.ld * 4,
+                         (size_t)l0.w * 4, nr, kout, s));
   if (trace) st = finish_trace(ctx, *p, s, trace, &tev);
-  else if (host) {
+  else if (host && allow_sync) {
     CK(cudaStreamSynchronize(s));
   }
   destroy_events(tev);
@@ -448,6 +489,8 @@ int mshbm_destroy(mshbm_ctx* ctx) {
   cudaStreamSynchronize(ctx->stream);
   for (auto& kv : ctx->plans) {
     if (kv.second->exec) cudaGraphExecDestroy(kv.second->exec);
+    if (kv.second->stream) cudaStreamDestroy(kv.second->stream);
+    if (kv.second->done) cudaEventDestroy(kv.second->done);
     cudaFree(kv.second->arena);
     delete kv.second;
   }
@@ -523,17 +566,19 @@ int mshbm_downsample(mshbm_ctx* ctx, const double* in, int32_t h, int32_t w, int
   return MSHBM_OK;
 }
 
-int mshbm_run_pipeline(mshbm_ctx* ctx, const float* left, const float* right, int32_t height,
-                       int32_t width, int64_t ld, const mshbm_config* cfg, int16_t* disparity,
-                       float* cost, int64_t ld_out, mshbm_level_trace* trace,
-                       int32_t* out_levels, int32_t io, int32_t flags, void* stream) {
-  if (!ctx) return fail(nullptr, MSHBM_ERR_VALUE, "null context");
-  if (!left || !right) return fail(ctx, MSHBM_ERR_VALUE, "null image pointer");
-  if (ld < width || ld_out < width) return fail(ctx, MSHBM_ERR_VALUE, "row stride < width");
+static int prepare_plan(mshbm_ctx* ctx, int32_t height, int32_t width, const mshbm_config* cfg,
+                        int32_t band_lo, int32_t band_hi, int32_t slot, int32_t* out_levels,
+                        Plan** out) {
   int K = 0;
   int st = mshbm_resolve_levels(cfg, height, width, &K);
   if (st) return fail(ctx, st, g_err);
   if (out_levels) *out_levels = K;
+  if (band_lo < 0 || band_hi > height || band_lo >= band_hi)
+    return fail(ctx, MSHBM_ERR_VALUE, "row band outside the image");
+  const int align = 1 << K;
+  if (band_lo % align != 0 || (band_hi != height && band_hi % align != 0))
+    return fail(ctx, MSHBM_ERR_VALUE,
+                "row band limits must be multiples of 2^levels (" + std::to_string(align) + ")");
   CK(cudaSetDevice(ctx->device));
   std::vector<std::tuple<int, int, int, int>> dims;
   int h = height, w = width;
@@ -544,12 +589,93 @@ int mshbm_run_pipeline(mshbm_ctx* ctx, const float* left, const float* right, in
     h = (h + 1) / 2;
     w = (w + 1) / 2;
   }
-  PlanKey key{height, width, K, 0, cfg->d_max, cfg->block, cfg->radius, cfg->sign,
-              cfg->alpha, cfg->beta, cfg->sigma_eps, {}};
+  PlanKey key{height, width, K, 0, band_lo, band_hi, slot, cfg->d_max, cfg->block, cfg->radius,
+              cfg->sign, cfg->alpha, cfg->beta, cfg->sigma_eps, {}};
   Plan* p = get_plan(ctx, key, *cfg, dims, &st);
   if (!p) return st;
+  *out = p;
+  return MSHBM_OK;
+}
+
+int mshbm_run_pipeline(mshbm_ctx* ctx, const float* left, const float* right, int32_t height,
+                       int32_t width, int64_t ld, const mshbm_config* cfg, int16_t* disparity,
+                       float* cost, int64_t ld_out, mshbm_level_trace* trace,
+                       int32_t* out_levels, int32_t io, int32_t flags, void* stream) {
+  if (!ctx) return fail(nullptr, MSHBM_ERR_VALUE, "null context");
+  if (!left || !right) return fail(ctx, MSHBM_ERR_VALUE, "null image pointer");
+  if (ld < width || ld_out < width) return fail(ctx, MSHBM_ERR_VALUE, "row stride < width");
+  Plan* p = nullptr;
+  int st = prepare_plan(ctx, height, width, cfg, 0, height, 0, out_levels, &p);
+  if (st) return st;
+  return run_plan_io(ctx, p, left, right, ld, disparity, cost, ld_out, trace, io, flags,
+                     pick(ctx, stream));
+}
+
+int mshbm_run_pipeline_band(mshbm_ctx* ctx, const float* left, const float* right,
+                            int32_t height, int32_t width, int64_t ld, const mshbm_config* cfg,
+                            int32_t row_begin, int32_t row_end, int16_t* disparity, float* cost,
+                            int64_t ld_out, mshbm_level_trace* trace, int32_t* out_levels,
+                            int32_t io, int32_t flags, void* stream) {
+  if (!ctx) return fail(nullptr, MSHBM_ERR_VALUE, "null context");
+  if (!left || !right) return fail(ctx, MSHBM_ERR_VALUE, "null image pointer");
+  if (ld < width || ld_out < width) return fail(ctx, MSHBM_ERR_VALUE, "row stride < width");
+  Plan* p = nullptr;
+  int st = prepare_plan(ctx, height, width, cfg, row_begin, row_end, 0, out_levels, &p);
+  if (st) return st;
+  return run_plan_io(ctx, p, left, right, ld, disparity, cost, ld_out, trace, io, flags,
+                     pick(ctx, stream));
+}
+
+int mshbm_run_batch(mshbm_ctx* ctx, int32_t n_pairs, const float* const* lefts,
+                    const float* const* rights, int32_t height, int32_t width, int64_t ld,
+                    const mshbm_config* cfg, int16_t* const* disparities, float* const* costs,
+                    int64_t ld_out, mshbm_level_trace* traces, int32_t io, int32_t n_streams,
+                    void* stream) {
+  if (!ctx) return fail(nullptr, MSHBM_ERR_VALUE, "null context");
+  if (n_pairs < 0 || (n_pairs > 0 && (!lefts || !rights)))
+    return fail(ctx, MSHBM_ERR_VALUE, "bad pair arrays");
+  if (ld < width || ld_out < width) return fail(ctx, MSHBM_ERR_VALUE, "row stride < width");
+  if (n_pairs == 0) return MSHBM_OK;
+  const int nslot = std::max(1, std::min(n_streams > 0 ? n_streams : 4, n_pairs));
   cudaStream_t s = pick(ctx, stream);
-  return run_plan_io(ctx, p, left, right, ld, disparity, cost, ld_out, trace, io, flags, s);
+  std::vector<Plan*> slot(nslot, nullptr);
+  int K = 0;
+  for (int k = 0; k < nslot; ++k) {
+    int st = prepare_plan(ctx, height, width, cfg, 0, height, 1 + k, &K, &slot[k]);
+    if (st) return st;
+    Plan* p = slot[k];
+    if (!p->stream) {
+      CK(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
+      CK(cudaEventCreateWithFlags(&p->done, cudaEventDisableTiming));
+    }
+  }
+  const size_t per = (size_t)(K + 1) * kCntSlots;
+  unsigned long long* hc = nullptr;
+  if (traces) CK(cudaMallocHost((void**)&hc, per * n_pairs * sizeof(unsigned long long)));
+  cudaEvent_t start;
+  CK(cudaEventCreateWithFlags(&start, cudaEventDisableTiming));
+  CK(cudaEventRecord(start, s));
+  for (int k = 0; k < nslot; ++k) CK(cudaStreamWaitEvent(slot[k]->stream, start, 0));
+  for (int i = 0; i < n_pairs; ++i) {
+    Plan* p = slot[i % nslot];
+    int st = run_plan_io(ctx, p, lefts[i], rights[i], ld, disparities ? disparities[i] : nullptr,
+                         costs ? costs[i] : nullptr, ld_out, nullptr, io, 0, p->stream, false);
+    if (st) return st;
+    if (hc)
+      CK(cudaMemcpyAsync(hc + per * i, p->counters, per * sizeof(unsigned long long),
+                         cudaMemcpyDeviceToHost, p->stream));
+  }
+  for (int k = 0; k < nslot; ++k) {
+    CK(cudaEventRecord(slot[k]->done, slot[k]->stream));
+    CK(cudaStreamWaitEvent(s, slot[k]->done, 0));
+  }
+  cudaEventDestroy(start);
+  if (hc || io == MSHBM_IO_HOST) CK(cudaStreamSynchronize(s));
+  if (hc) {
+    for (int i = 0; i < n_pairs; ++i) pack_trace(*slot[i % nslot], hc + per * i, traces + (size_t)(K + 1) * i, nullptr);
+    cudaFreeHost(hc);
+  }
+  return MSHBM_OK;
 }
 
 int mshbm_run_pyramid(mshbm_ctx* ctx, int32_t n_levels, const double* const* lefts,
@@ -574,8 +700,8 @@ int mshbm_run_pyramid(mshbm_ctx* ctx, int32_t n_levels, const double* const* lef
     dims.emplace_back(heights[k], widths[k], d_maxs[k], blocks[k]);
     flat.insert(flat.end(), {heights[k], widths[k], d_maxs[k], blocks[k]});
   }
-  PlanKey key{heights[0], widths[0], n_levels - 1, 1, cfg->d_max, cfg->block, cfg->radius,
-              cfg->sign, cfg->alpha, cfg->beta, cfg->sigma_eps, flat};
+  PlanKey key{heights[0], widths[0], n_levels - 1, 1, 0, heights[0], 0, cfg->d_max, cfg->block,
+              cfg->radius, cfg->sign, cfg->alpha, cfg->beta, cfg->sigma_eps, flat};
   Plan* p = get_plan(ctx, key, *cfg, dims, &st);
   if (!p) return st;
   cudaStream_t s = pick(ctx, stream);
@@ -729,6 +855,7 @@ static SweepArgs raw_args(mshbm_engine* e, const int* wc, int radius) {
   a.wc = wc; a.ldw = e->W; a.radius = radius;
   a.alpha = 0.5; a.mode = kSweepRaw;
   a.fz = e->fz; a.fc = e->fc; a.wz = e->wz; a.wcst = e->wcst; a.nz = e->nz; a.nc = e->nc;
+  a.rows = RowBand{0, e->H, 0, e->H};
   return a;
 }
 

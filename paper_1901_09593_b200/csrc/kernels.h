@@ -13,6 +13,12 @@ namespace mshbm {
 // reference's selection/refinement gates in the epilogue.
 enum SweepMode { kSweepPipeline = 0, kSweepRaw = 1 };
 
+// Row range a stage computes ([lo, hi)) and the rows whose pixels it counts
+// in the trace ([cnt_lo, cnt_hi)); whole-image runs use [0, H) for both.
+struct RowBand {
+  int lo, hi, cnt_lo, cnt_hi;
+};
+
 struct SweepArgs {
   const double* L;      // level images, float64, row stride ld
   const double* R;
@@ -33,6 +39,7 @@ struct SweepArgs {
   uint8_t* low;
   int64_t ldo;
   unsigned long long* counters;
+  RowBand rows;         // output rows computed / counted
   // raw outputs (dense H x W): full, window, 3x3-summed winners
   int16_t* fz; float* fc; int16_t* wz; float* wcst; int16_t* nz; float* nc;
 };
@@ -72,7 +79,7 @@ cudaError_t launch_prior_eval(const int16_t* dcoarse, int64_t ldd, int ch,
                               int cw, const double* coef, int64_t ldc, int h,
                               int w, int d, int radius, double beta, int* wc,
                               int64_t ldw, unsigned long long* counters,
-                              cudaStream_t s);
+                              RowBand rows, cudaStream_t s);
 // stage prior from explicit float64 (d_hat, c_hat) maps (dense h x w)
 cudaError_t launch_prior_maps(const double* d_hat, const double* c_hat, int h,
                               int w, int d, int radius, double beta, int* wc,
@@ -88,7 +95,7 @@ cudaError_t launch_upsample(const double* dcoarse, int ch, int cw,
 cudaError_t launch_median_pipeline(const int16_t* d, const float* c,
                                    const uint8_t* low, int64_t ld, int h,
                                    int w, double alpha, int16_t* out,
-                                   unsigned long long* counters,
+                                   unsigned long long* counters, RowBand rows,
                                    cudaStream_t s);
 // stage API: float64 dense maps, NaN-aware
 cudaError_t launch_median_f64(const double* d, const double* c, int h, int w,

@@ -386,30 +386,6 @@ __device__ __forceinline__ void count_trusted(bool trusted, int c, int r, int d,
   block_accumulate<3>(counters, slot, val, mx);
 }
 
-// upsample_prior + the trust gate of select_with_prior (matcher.py:236-260,
-// 276-281): d_hat = 2 d[i/2, j/2], c_hat = clamp(spline, -1, 1),
-// trusted = c_hat > beta and [c-r, c+r] intersects [0, d].
-__global__ void prior_eval_kernel(const int16_t* dco, int64_t ldd, int ch,
-                                  int cw, const double* coef, int64_t ldc,
-                                  int h, int w, int d, int r, double beta,
-                                  int* wc, int64_t ldw,
-                                  unsigned long long* counters) {
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  const int i = blockIdx.y * blockDim.y + threadIdx.y;
-  const bool in = i < h && j < w;
-  bool trusted = false;
-  int center = 0;
-  if (in) {
-    double chat = spline_at(coef, ldc, ch, cw, h, w, i, j);
-    chat = fmin(fmax(chat, -1.0), 1.0);
-    center = 2 * (int)dco[(int64_t)(i >> 1) * ldd + (j >> 1)];
-    const bool ok = (center + r >= 0) && (center - r <= d);
-    trusted = (chat > beta) && ok;
-    wc[(int64_t)i * ldw + j] = trusted ? center : kWcNone;
-  }
-  count_trusted(trusted, center, r, d, counters);
-}
-
 __global__ void prior_maps_kernel(const double* d_hat, const double* c_hat,
                                   int h, int w, int d, int r, double beta,
                                   int* wc, int64_t ldw,
@@ -459,49 +435,6 @@ __device__ __forceinline__ T lower_median(T* v, int n) {
     if (less <= m && m < leq) { best = v[k]; break; }
   }
   return best;
-}
-
-__global__ void median_pipeline_kernel(const int16_t* d, const float* c,
-                                       const uint8_t* low, int64_t ld, int h,
-                                       int w, double alpha, int16_t* out,
-                                       unsigned long long* counters) {
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  const int i = blockIdx.y * blockDim.y + threadIdx.y;
-  const bool in = i < h && j < w;
-  bool changed = false, needed = false;
-  if (in) {
-    const int64_t o = (int64_t)i * ld + j;
-    const int16_t d0 = d[o];
-    int16_t res = d0;
-    for (int di = -1; di <= 1; ++di)
-      for (int dj = -1; dj <= 1; ++dj) {
-        const int qi = i + di, qj = j + dj;
-        if (qi >= 0 && qi < h && qj >= 0 && qj < w && low[(int64_t)qi * ld + qj]) needed = true;
-      }
-    if ((double)c[o] <= alpha) {
-      int v[24];
-      int n = 0;
-      for (int di = -2; di <= 2; ++di) {
-        const int qi = i + di;
-        if (qi < 0 || qi >= h) continue;
-        for (int dj = -2; dj <= 2; ++dj) {
-          const int qj = j + dj;
-          if (qj < 0 || qj >= w) continue;
-          const int64_t q = (int64_t)qi * ld + qj;
-          if ((double)c[q] > alpha && n < 24) v[n++] = d[q];
-        }
-      }
-      if (n > 0) res = (int16_t)lower_median(v, n);
-    }
-    out[o] = res;
-    changed = res != d0;
-  }
-  const unsigned bc = __ballot_sync(kFull, changed);
-  const unsigned bn = __ballot_sync(kFull, needed);
-  if ((threadIdx.x & 31) == 0) {
-    if (bc) atomicAdd(&counters[kCntMedianReplaced], (unsigned long long)__popc(bc));
-    if (bn) atomicAdd(&counters[kCntNeeded], (unsigned long long)__popc(bn));
-  }
 }
 
 __global__ void median_f64_kernel(const double* d, const double* c, int h,
@@ -689,12 +622,13 @@ __global__ void __launch_bounds__(kTX * kTY) stats_tiled_kernel(const double* im
 // prior_eval with the 4x4 spline support of the block staged in smem
 __global__ void __launch_bounds__(kTX * kTY) prior_eval_tiled_kernel(
     const int16_t* dco, int64_t ldd, int ch, int cw, const double* coef, int64_t ldc, int h,
-    int w, int d, int r, double beta, int* wc, int64_t ldw, unsigned long long* counters) {
+    int w, int d, int r, double beta, int* wc, int64_t ldw, unsigned long long* counters,
+    RowBand band) {
   constexpr int CR = 12, CC = 24;
   __shared__ double Cs[CR][CC];
   const int nh = ch + 2 * kNpad, nw = cw + 2 * kNpad;
   const double ry = (double)ch / (double)h, rx = (double)cw / (double)w;
-  const int i0 = blockIdx.y * kTY, j0 = blockIdx.x * kTX;
+  const int i0 = band.lo + blockIdx.y * kTY, j0 = blockIdx.x * kTX;
   const int ylo = (int)floor(((double)i0 + 0.5) * ry - 0.5 + kNpad) - 1;
   const int xlo = (int)floor(((double)j0 + 0.5) * rx - 0.5 + kNpad) - 1;
   const int tid = threadIdx.y * kTX + threadIdx.x;
@@ -704,7 +638,7 @@ __global__ void __launch_bounds__(kTX * kTY) prior_eval_tiled_kernel(
   }
   __syncthreads();
   const int i = i0 + threadIdx.y, j = j0 + threadIdx.x;
-  const bool in = i < h && j < w;
+  const bool in = i < band.hi && i < h && j < w;
   bool trusted = false;
   int center = 0;
   if (in) {
@@ -729,18 +663,19 @@ __global__ void __launch_bounds__(kTX * kTY) prior_eval_tiled_kernel(
     trusted = (chat > beta) && ok;
     wc[(int64_t)i * ldw + j] = trusted ? center : kWcNone;
   }
-  count_trusted(trusted, center, r, d, counters);
+  const bool counted = i >= band.cnt_lo && i < band.cnt_hi;
+  count_trusted(trusted && counted, center, r, d, counters);
 }
 
 // selective median (pipeline) with the 5x5 neighbourhood staged in smem
 __global__ void __launch_bounds__(kTX * kTY) median_tiled_kernel(
     const int16_t* d, const float* c, const uint8_t* low, int64_t ld, int h, int w,
-    double alpha, int16_t* out, unsigned long long* counters) {
+    double alpha, int16_t* out, unsigned long long* counters, RowBand band) {
   constexpr int TR = kTY + 4, TC = kTX + 4;
   __shared__ float Cs[TR][TC];
   __shared__ int16_t Ds[TR][TC];
   __shared__ uint8_t Lw[TR][TC];
-  const int x0 = blockIdx.x * kTX, y0 = blockIdx.y * kTY;
+  const int x0 = blockIdx.x * kTX, y0 = band.lo + blockIdx.y * kTY;
   const int tid = threadIdx.y * kTX + threadIdx.x;
   for (int t = tid; t < TR * TC; t += kTX * kTY) {
     const int a = t / TC, b = t - a * TC;
@@ -758,7 +693,7 @@ __global__ void __launch_bounds__(kTX * kTY) median_tiled_kernel(
   }
   __syncthreads();
   const int i = y0 + threadIdx.y, j = x0 + threadIdx.x;
-  const bool in = i < h && j < w;
+  const bool in = i < band.hi && i < h && j < w;
   bool changed = false, needed = false;
   if (in) {
     const int ty = threadIdx.y + 2, tx = threadIdx.x + 2;
@@ -781,8 +716,10 @@ __global__ void __launch_bounds__(kTX * kTY) median_tiled_kernel(
     out[(int64_t)i * ld + j] = res;
     changed = res != d0;
   }
+  const bool counted = i >= band.cnt_lo && i < band.cnt_hi;
   const int slot[2] = {kCntMedianReplaced, kCntNeeded};
-  const unsigned long long val[2] = {changed ? 1ull : 0ull, needed ? 1ull : 0ull};
+  const unsigned long long val[2] = {(changed && counted) ? 1ull : 0ull,
+                                     (needed && counted) ? 1ull : 0ull};
   const bool mx[2] = {false, false};
   block_accumulate<2>(counters, slot, val, mx);
 }
@@ -855,16 +792,11 @@ cudaError_t launch_prior_eval(const int16_t* dcoarse, int64_t ldd, int ch,
                               int cw, const double* coef, int64_t ldc, int h,
                               int w, int d, int radius, double beta, int* wc,
                               int64_t ldw, unsigned long long* counters,
-                              cudaStream_t s) {
+                              RowBand rows, cudaStream_t s) {
   dim3 blk(32, 8);
-  if (2 * ch <= h + 2 && 2 * cw <= w + 2) {   // dyadic parent: the tile covers the support
-    prior_eval_tiled_kernel<<<grid2d(w, h, blk), blk, 0, s>>>(dcoarse, ldd, ch, cw, coef, ldc, h,
-                                                               w, d, radius, beta, wc, ldw,
-                                                               counters);
-    return cudaGetLastError();
-  }
-  prior_eval_kernel<<<grid2d(w, h, blk), blk, 0, s>>>(dcoarse, ldd, ch, cw, coef, ldc, h, w,
-                                                       d, radius, beta, wc, ldw, counters);
+  const dim3 g((w + 31) / 32, (rows.hi - rows.lo + 7) / 8);
+  prior_eval_tiled_kernel<<<g, blk, 0, s>>>(dcoarse, ldd, ch, cw, coef, ldc, h, w, d, radius,
+                                            beta, wc, ldw, counters, rows);
   return cudaGetLastError();
 }
 
@@ -890,13 +822,11 @@ cudaError_t launch_upsample(const double* dcoarse, int ch, int cw,
 cudaError_t launch_median_pipeline(const int16_t* d, const float* c,
                                    const uint8_t* low, int64_t ld, int h,
                                    int w, double alpha, int16_t* out,
-                                   unsigned long long* counters,
+                                   unsigned long long* counters, RowBand rows,
                                    cudaStream_t s) {
   dim3 blk(32, 8);
-  median_tiled_kernel<<<grid2d(w, h, blk), blk, 0, s>>>(d, c, low, ld, h, w, alpha, out, counters);
-  return cudaGetLastError();
-  median_pipeline_kernel<<<grid2d(w, h, blk), blk, 0, s>>>(d, c, low, ld, h, w, alpha, out,
-                                                            counters);
+  const dim3 g((w + 31) / 32, (rows.hi - rows.lo + 7) / 8);
+  median_tiled_kernel<<<g, blk, 0, s>>>(d, c, low, ld, h, w, alpha, out, counters, rows);
   return cudaGetLastError();
 }
 

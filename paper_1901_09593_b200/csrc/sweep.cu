@@ -102,7 +102,7 @@ sweep_kernel(const SweepArgs a) {
   const int lane = threadIdx.x & 31;
   const int wp = threadIdx.x >> 5;
   const int x0 = blockIdx.x * 30;
-  const int y0 = blockIdx.y * (NR - 2);
+  const int y0 = a.rows.lo + blockIdx.y * (NR - 2);
   const int i = y0 - 1 + wp;
   const int j = x0 - 1 + lane;
   const int H = a.H, W = a.W, d = a.d;
@@ -280,7 +280,7 @@ sweep_kernel(const SweepArgs a) {
       a.cout[o] = low ? bN / (float)members : cs;
       a.low[o] = (uint8_t)low;
     }
-    const unsigned bal = __ballot_sync(kFull, low);
+    const unsigned bal = __ballot_sync(kFull, low && i >= a.rows.cnt_lo && i < a.rows.cnt_hi);
     if (lane == 0 && bal) atomicAdd(&a.counters[kCntRefined], (unsigned long long)__popc(bal));
   } else if (inner) {
     const int64_t o = (int64_t)i * W + j;
@@ -302,7 +302,7 @@ sweep_generic(const SweepArgs a) {
   __shared__ float Hs[NR][32];
   const int B = a.block, H2 = B / 2;
   const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
-  const int x0 = blockIdx.x * 30, y0 = blockIdx.y * (NR - 2);
+  const int x0 = blockIdx.x * 30, y0 = a.rows.lo + blockIdx.y * (NR - 2);
   const int i = y0 - 1 + wp, j = x0 - 1 + lane;
   const int H = a.H, W = a.W, d = a.d;
   const bool inimg = (i >= 0) && (i < H) && (j >= 0) && (j < W);
@@ -379,7 +379,7 @@ sweep_generic(const SweepArgs a) {
       a.cout[o] = low ? bN / (float)members : cs;
       a.low[o] = (uint8_t)low;
     }
-    const unsigned bal = __ballot_sync(kFull, low);
+    const unsigned bal = __ballot_sync(kFull, low && i >= a.rows.cnt_lo && i < a.rows.cnt_hi);
     if (lane == 0 && bal) atomicAdd(&a.counters[kCntRefined], (unsigned long long)__popc(bal));
   } else if (inner) {
     const int64_t o = (int64_t)i * W + j;
@@ -417,8 +417,10 @@ cudaError_t launch_v(const SweepArgs& a, cudaStream_t s) {
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  dim3 grid((a.W + 29) / 30, (a.H + NR - 3) / (NR - 2));
-  sweep_kernel<B, DIR, ZC, NR, MINB><<<grid, NR * 32, smem, s>>>(a);
+  SweepArgs b = a;   // CTA rows on the whole-image grid (see sweep2.cu)
+  b.rows.lo = (a.rows.lo / (NR - 2)) * (NR - 2);
+  dim3 grid((a.W + 29) / 30, (b.rows.hi - b.rows.lo + NR - 3) / (NR - 2));
+  sweep_kernel<B, DIR, ZC, NR, MINB><<<grid, NR * 32, smem, s>>>(b);
   return cudaGetLastError();
 }
 
@@ -449,8 +451,10 @@ cudaError_t launch_dir(const SweepArgs& a, cudaStream_t s) {
     case 11: return launch_b<11, DIR>(a, s);
     default: {
       constexpr int NR = 8;
-      dim3 grid((a.W + 29) / 30, (a.H + NR - 3) / (NR - 2));
-      sweep_generic<DIR, NR><<<grid, NR * 32, 0, s>>>(a);
+      SweepArgs b = a;
+      b.rows.lo = (a.rows.lo / (NR - 2)) * (NR - 2);
+      dim3 grid((a.W + 29) / 30, (b.rows.hi - b.rows.lo + NR - 3) / (NR - 2));
+      sweep_generic<DIR, NR><<<grid, NR * 32, 0, s>>>(b);
       return cudaGetLastError();
     }
   }

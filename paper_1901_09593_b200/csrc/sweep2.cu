@@ -118,7 +118,7 @@ sweep2_kernel(const SweepArgs a) {
   const int lane = threadIdx.x & 31;
   const int wp = threadIdx.x >> 5;
   const int x0 = blockIdx.x * 30;
-  const int y0 = blockIdx.y * (NROW - 2);
+  const int y0 = a.rows.lo + blockIdx.y * (NROW - 2);
   const int iA = y0 - 1 + 2 * wp, iB = iA + 1;
   const int j = x0 - 1 + lane;
   const int H = a.H, W = a.W, d = a.d;
@@ -316,7 +316,7 @@ sweep2_kernel(const SweepArgs a) {
         a.cout[o] = low ? nbv[p] / (float)members : cs;
         a.low[o] = (uint8_t)low;
       }
-      nlow += low ? 1u : 0u;
+      nlow += (low && i >= a.rows.cnt_lo && i < a.rows.cnt_hi) ? 1u : 0u;
     } else if (inner[p]) {
       const int64_t o = (int64_t)i * W + j;
       a.fz[o] = (int16_t)bestz[p];
@@ -345,8 +345,12 @@ cudaError_t launch2(const SweepArgs& a, cudaStream_t s) {
     configured = true;
   }
   constexpr int NROW = 2 * NR;
-  dim3 grid((a.W + 29) / 30, (a.H + NROW - 3) / (NROW - 2));
-  sweep2_kernel<B, DIR, ZC, NR, MINB><<<grid, NR * 32, smem, s>>>(a);
+  // CTA rows stay on the whole-image grid (row bands are then bit-identical:
+  // the per-CTA offset c of the right strip depends on the CTA)
+  SweepArgs b = a;
+  b.rows.lo = (a.rows.lo / (NROW - 2)) * (NROW - 2);
+  dim3 grid((a.W + 29) / 30, (b.rows.hi - b.rows.lo + NROW - 3) / (NROW - 2));
+  sweep2_kernel<B, DIR, ZC, NR, MINB><<<grid, NR * 32, smem, s>>>(b);
   return cudaGetLastError();
 }
 

@@ -37,6 +37,8 @@ __all__ = [
     "selective_median",
     "run_pipeline",
     "run_pipeline_device",
+    "run_pipeline_band",
+    "run_batch",
 ]
 
 # Per-stage CUDA-event timings in the trace (direct launches instead of the
@@ -393,3 +395,73 @@ def _run_user_pyramid(pyramid: StereoPyramid, config: MatchConfig, t_start: floa
                                             tr, _lib.current_stream()), ctx)
     trace = _trace_from(tr, n - 1, False, 0.0, t_start)
     return (d16.cpu().numpy().astype(np.float64), c32.cpu().numpy().astype(np.float64), trace)
+
+
+# --------------------------------------------------------------------- C4 / C5
+def run_batch(lefts, rights, config: MatchConfig, n_streams: int = 4, trace: bool = True):
+    """Independent same-shape pairs (BASELINE C4) through ``mshbm_run_batch``.
+
+    ``lefts``/``rights``: a stacked torch CUDA tensor (N, H, W) or a sequence
+    of arrays.  Pairs run round-robin on ``n_streams`` concurrent CUDA-graph
+    plans.  Returns (disparities int16 (N, H, W), costs float32 (N, H, W),
+    traces | None) as CUDA tensors.
+    """
+    torch = _torch()
+    L = torch.stack([torch.as_tensor(x) for x in lefts]) if not isinstance(lefts, torch.Tensor) else lefts
+    R = torch.stack([torch.as_tensor(x) for x in rights]) if not isinstance(rights, torch.Tensor) else rights
+    L = L.to(device="cuda", dtype=torch.float32).contiguous()
+    R = R.to(device="cuda", dtype=torch.float32).contiguous()
+    if L.ndim != 3 or L.shape != R.shape:
+        raise ValueError(f"batch shapes differ: {tuple(L.shape)} vs {tuple(R.shape)}")
+    n, h, w = L.shape
+    cfg = config.to_c()
+    K = C.c_int32()
+    _lib.check(_lib.lib().mshbm_resolve_levels(C.byref(cfg), h, w, C.byref(K)))
+    D = torch.empty((n, h, w), dtype=torch.int16, device=L.device)
+    Cc = torch.empty((n, h, w), dtype=torch.float32, device=L.device)
+    ptrs = lambda t: (C.c_void_p * n)(*[t[i].data_ptr() for i in range(n)])  # noqa: E731
+    tr = (_lib.LevelTraceC * (n * (K.value + 1)))() if trace else None
+    ctx = _lib.context(L.device.index)
+    _lib.check(_lib.lib().mshbm_run_batch(ctx, n, ptrs(L), ptrs(R), h, w, w, C.byref(cfg),
+                                          ptrs(D), ptrs(Cc), w, tr, _lib.IO_DEVICE,
+                                          int(n_streams), _lib.current_stream()), ctx)
+    traces = None
+    if trace:
+        k1 = K.value + 1
+        traces = []
+        for i in range(n):
+            t = PipelineTrace()
+            t.levels = [LevelTrace.from_c(tr[i * k1 + l], False) for l in range(k1)]
+            traces.append(t)
+    return D, Cc, traces
+
+
+def run_pipeline_band(left, right, config: MatchConfig, row_begin: int, row_end: int,
+                      trace: bool = True):
+    """Level-0 rows [row_begin, row_end) of run_pipeline (BASELINE C5 bands).
+
+    Bit-identical to the same rows of the whole-image result; limits must be
+    multiples of 2^levels (or the image height).  Trace counters cover the
+    band's own rows at every level, so a partition's traces sum to the
+    whole-image trace (see ``sharding.merge_traces``).  CUDA tensors in/out.
+    """
+    torch = _torch()
+    lt = left.to(device="cuda", dtype=torch.float32).contiguous()
+    rt = right.to(device="cuda", dtype=torch.float32).contiguous()
+    if lt.ndim != 2 or lt.shape != rt.shape:
+        raise ValueError(f"left/right shapes differ: {tuple(lt.shape)} vs {tuple(rt.shape)}")
+    h, w = lt.shape
+    cfg = config.to_c()
+    K = C.c_int32()
+    ctx = _lib.context(lt.device.index)
+    n = int(row_end) - int(row_begin)
+    d16 = torch.empty((max(n, 0), w), dtype=torch.int16, device=lt.device)
+    c32 = torch.empty((max(n, 0), w), dtype=torch.float32, device=lt.device)
+    _lib.check(_lib.lib().mshbm_resolve_levels(C.byref(cfg), h, w, C.byref(K)))
+    tr = (_lib.LevelTraceC * (K.value + 1))() if trace else None
+    _lib.check(_lib.lib().mshbm_run_pipeline_band(
+        ctx, lt.data_ptr(), rt.data_ptr(), h, w, w, C.byref(cfg), int(row_begin), int(row_end),
+        d16.data_ptr(), c32.data_ptr(), w, tr, C.byref(K), _lib.IO_DEVICE, 0,
+        _lib.current_stream()), ctx)
+    t = _trace_from(tr, K.value, False, 0.0, time.perf_counter()) if trace else None
+    return d16, c32, t
