@@ -165,7 +165,7 @@ void carve(Plan& p, Carver& cv) {
   p.ld_in = ldi;
   p.in_l = cv.take<float>((size_t)ldi * p.H);
   p.in_r = cv.take<float>((size_t)ldi * p.H);
-  p.counters = cv.take<unsigned long long>((size_t)(p.K + 1) * kCntSlots);
+  p.counters = cv.take<unsigned long long>((size_t)(p.K + 1) * kCntSlots * kCntCopies);
   for (auto& l : p.lv) {
     const size_t n = (size_t)l.ld * l.h;
     l.L = cv.take<double>(n);
@@ -226,7 +226,8 @@ int enqueue(mshbm_ctx* ctx, Plan& p, cudaStream_t s, std::vector<StageEvents>* t
   int n = 0;
   const mshbm_config& cfg = p.cfg;
   const int dir = cfg.sign == MSHBM_SIGN_PAPER ? -1 : 1;
-  CK(cudaMemsetAsync(p.counters, 0, sizeof(unsigned long long) * (p.K + 1) * kCntSlots, s));
+  CK(cudaMemsetAsync(p.counters, 0,
+                     sizeof(unsigned long long) * (p.K + 1) * kCntSlots * kCntCopies, s));
   if (!p.user) {
     CK(launch_f32_to_f64(p.in_l, p.in_r, p.H, p.W, p.ld_in, p.lv[0].L, p.lv[0].R, p.lv[0].ld, s));
     ++n;
@@ -244,7 +245,7 @@ int enqueue(mshbm_ctx* ctx, Plan& p, cudaStream_t s, std::vector<StageEvents>* t
   }
   for (int k = p.K; k >= 0; --k) {
     LevelBuf& l = p.lv[k];
-    unsigned long long* cnt = p.counters + (size_t)(p.K - k) * kCntSlots;
+    unsigned long long* cnt = p.counters + (size_t)(p.K - k) * kCntSlots * kCntCopies;
     StageEvents* ev = tev ? &(*tev)[p.K - k] : nullptr;
     if (ev) CK(cudaEventRecord(ev->up0, s));
     if (k < p.K) {
@@ -346,12 +347,23 @@ int launch_plan(mshbm_ctx* ctx, Plan& p, cudaStream_t s, int flags,
 
 // Pack host copies of the device counters into LevelTrace records exactly as
 // run_pipeline fills them (matcher.py:377-463).
+// sum (window max: max) the kCntCopies copies of one level's counters
+void reduce_copies(const unsigned long long* h, unsigned long long* c) {
+  for (int s = 0; s < kCntSlots; ++s) c[s] = 0;
+  for (int cp = 0; cp < kCntCopies; ++cp)
+    for (int s = 0; s < kCntSlots; ++s) {
+      const unsigned long long v = h[(size_t)cp * kCntSlots + s];
+      c[s] = s == kCntWindowMax ? std::max(c[s], v) : c[s] + v;
+    }
+}
+
 void pack_trace(const Plan& p, const unsigned long long* h, mshbm_level_trace* trace,
                 std::vector<StageEvents>* tev) {
   for (int t = 0; t <= p.K; ++t) {
     const int k = p.K - t;
     const LevelBuf& l = p.lv[k];
-    const unsigned long long* c = &h[(size_t)t * kCntSlots];
+    unsigned long long c[kCntSlots];
+    reduce_copies(&h[(size_t)t * kCntSlots * kCntCopies], c);
     mshbm_level_trace& o = trace[t];
     memset(&o, 0, sizeof o);
     o.level = k;
@@ -392,7 +404,7 @@ void pack_trace(const Plan& p, const unsigned long long* h, mshbm_level_trace* t
 // Copy the device counters back (synchronises `s`) and pack the trace.
 int finish_trace(mshbm_ctx* ctx, Plan& p, cudaStream_t s, mshbm_level_trace* trace,
                  std::vector<StageEvents>* tev) {
-  std::vector<unsigned long long> h((size_t)(p.K + 1) * kCntSlots);
+  std::vector<unsigned long long> h((size_t)(p.K + 1) * kCntSlots * kCntCopies);
   CK(cudaMemcpyAsync(h.data(), p.counters, h.size() * sizeof(h[0]), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
   pack_trace(p, h.data(), trace, tev);
@@ -649,7 +661,7 @@ int mshbm_run_batch(mshbm_ctx* ctx, int32_t n_pairs, const float* const* lefts,
       CK(cudaEventCreateWithFlags(&p->done, cudaEventDisableTiming));
     }
   }
-  const size_t per = (size_t)(K + 1) * kCntSlots;
+  const size_t per = (size_t)(K + 1) * kCntSlots * kCntCopies;
   unsigned long long* hc = nullptr;
   if (traces) CK(cudaMallocHost((void**)&hc, per * n_pairs * sizeof(unsigned long long)));
   cudaEvent_t start;
@@ -746,7 +758,7 @@ int mshbm_engine_create(mshbm_ctx* ctx, const double* left, const double* right,
     e->wc = cv.take<int>(n);
     e->fz = cv.take<int16_t>(nd); e->wz = cv.take<int16_t>(nd); e->nz = cv.take<int16_t>(nd);
     e->fc = cv.take<float>(nd); e->wcst = cv.take<float>(nd); e->nc = cv.take<float>(nd);
-    e->counters = cv.take<unsigned long long>(kCntSlots);
+    e->counters = cv.take<unsigned long long>(kCntSlots * kCntCopies);
     e->bad = cv.take<int>(1);
     if (pass == 0) {
       if (cudaMalloc(&e->arena, cv.off + 256) != cudaSuccess) {
@@ -879,15 +891,17 @@ int mshbm_select_with_prior(mshbm_engine* e, const double* d_hat, const double* 
   if (radius < 0) return fail(ctx, MSHBM_ERR_VALUE, "radius must be >= 0");
   CK(cudaSetDevice(ctx->device));
   cudaStream_t s = pick(ctx, stream);
-  CK(cudaMemsetAsync(e->counters, 0, kCntSlots * 8, s));
+  CK(cudaMemsetAsync(e->counters, 0, kCntSlots * kCntCopies * 8, s));
   CK(launch_prior_maps(d_hat, c_hat, e->H, e->W, e->d, radius, beta, e->wc, e->W, e->counters, s));
   int n = 1;
   CK(launch_sweep(raw_args(e, e->wc, radius), s, &n));
   CK(launch_combine_select(e->wc, e->H, e->W, e->fz, e->fc, e->wz, e->wcst, disparity, cost, s));
   ctx->launches += n + 1;
-  unsigned long long h[kCntSlots];
-  CK(cudaMemcpyAsync(h, e->counters, sizeof h, cudaMemcpyDeviceToHost, s));
+  std::vector<unsigned long long> hc((size_t)kCntSlots * kCntCopies);
+  CK(cudaMemcpyAsync(hc.data(), e->counters, hc.size() * 8, cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
+  unsigned long long h[kCntSlots];
+  reduce_copies(hc.data(), h);
   const int64_t N = (int64_t)e->H * e->W;
   if (stats) {
     stats[0] = (int64_t)h[kCntTrusted];
@@ -905,15 +919,17 @@ int mshbm_refine_level(mshbm_engine* e, const double* disparity, const double* c
   if (!e) return fail(nullptr, MSHBM_ERR_VALUE, "null engine");
   CK(cudaSetDevice(ctx->device));
   cudaStream_t s = pick(ctx, stream);
-  CK(cudaMemsetAsync(e->counters, 0, kCntSlots * 8, s));
+  CK(cudaMemsetAsync(e->counters, 0, kCntSlots * kCntCopies * 8, s));
   int n = 0;
   CK(launch_sweep(raw_args(e, nullptr, 0), s, &n));
   CK(launch_combine_refine(disparity, cost, e->H, e->W, alpha, e->nz, e->nc, out_disparity,
                            out_cost, e->counters, s));
   ctx->launches += n + 1;
-  unsigned long long h[kCntSlots];
-  CK(cudaMemcpyAsync(h, e->counters, sizeof h, cudaMemcpyDeviceToHost, s));
+  std::vector<unsigned long long> hc((size_t)kCntSlots * kCntCopies);
+  CK(cudaMemcpyAsync(hc.data(), e->counters, hc.size() * 8, cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
+  unsigned long long h[kCntSlots];
+  reduce_copies(hc.data(), h);
   if (evals) *evals = h[kCntRefined] > 0 ? (int64_t)h[kCntNeeded] * (e->d + 1) : 0;
   return MSHBM_OK;
 }

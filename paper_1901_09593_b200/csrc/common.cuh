@@ -39,6 +39,20 @@ MSHBM_DEV void warp_atomic_max(long long* dst, long long v) {
   if ((threadIdx.x & 31) == 0 && v > 0) atomicMax((long long*)dst, v);
 }
 
+// Per-level device counters (int64), see mshbm_level_trace; each level owns
+// kCntCopies copies of kCntSlots counters.
+enum CounterSlot {
+  kCntTrusted = 0,
+  kCntTrustedEvals = 1,
+  kCntWindowMax = 2,
+  kCntRefined = 3,
+  kCntNeeded = 4,
+  kCntMedianReplaced = 5,
+  kCntSlots = 8
+};
+constexpr int kCntCopies = 64;
+MSHBM_DEV int kCntCopyStride(unsigned b) { return (int)(b % kCntCopies); }
+
 // Block-level counter accumulation: warp shuffles, one shared-memory atomic
 // per warp, one global atomic per block (same-address global atomics from
 // every warp serialise in L2).  Every thread of the block must call it.
@@ -63,21 +77,14 @@ MSHBM_DEV void block_accumulate(unsigned long long* __restrict__ gdst, const int
     }
   }
   __syncthreads();
+  // counters are spread over kCntCopies cache-line-separated copies (block
+  // index modulo): same-address atomics from every block would serialise in
+  // L2; the host sums (or maxes) the copies when it reads the trace
   if (tid < NSLOT && acc[tid]) {
-    if (is_max[tid]) atomicMax(&gdst[slot[tid]], acc[tid]);
-    else atomicAdd(&gdst[slot[tid]], acc[tid]);
+    unsigned long long* dst = gdst + (size_t)kCntSlots * kCntCopyStride(blockIdx.x + gridDim.x * blockIdx.y) + slot[tid];
+    if (is_max[tid]) atomicMax(dst, acc[tid]);
+    else atomicAdd(dst, acc[tid]);
   }
 }
-
-// Per-level device counters (int64), see mshbm_level_trace.
-enum CounterSlot {
-  kCntTrusted = 0,
-  kCntTrustedEvals = 1,
-  kCntWindowMax = 2,
-  kCntRefined = 3,
-  kCntNeeded = 4,
-  kCntMedianReplaced = 5,
-  kCntSlots = 8
-};
 
 }  // namespace mshbm

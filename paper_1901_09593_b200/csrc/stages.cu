@@ -256,20 +256,22 @@ __device__ __forceinline__ void iir_line_smem(double* x, int stride, int lo, int
                                               bool exact_hi, int n_full, double g) {
   // x[lo .. hi) is the part of the line inside the tile (tile-local indices);
   // exact_lo: x[lo] is element 0 of the line; exact_hi: x[hi-1] is element n-1.
+  // The gain is applied on load; recursions run on register chunks of 8 so
+  // the shared-memory loads of a chunk are independent of the recursion.
+  constexpr int U = 8;
   const double z = kPole;
   const int n = hi - lo;
   if (n <= 0) return;
-  for (int k = lo; k < hi; ++k) x[k * stride] *= g;
   double acc;
   if (exact_lo) {
     if (exact_hi && n_full == n) {
       // whole line present: scipy's full reflect init
       const double zn = pow(z, (double)n);
-      const double c0 = x[lo * stride];
-      double s = c0 + zn * x[(hi - 1) * stride];
+      const double c0 = g * x[lo * stride];
+      double s = c0 + zn * (g * x[(hi - 1) * stride]);
       double zi = z;
       for (int i = 1; i < n; ++i) {
-        s += zi * (x[(lo + i) * stride] + zn * x[(hi - 1 - i) * stride]);
+        s += zi * (g * x[(lo + i) * stride] + zn * (g * x[(hi - 1 - i) * stride]));
         zi *= z;
       }
       acc = s * (z / (1.0 - zn * zn)) + c0;
@@ -278,23 +280,45 @@ __device__ __forceinline__ void iir_line_smem(double* x, int stride, int lo, int
       double s = 0.0, zi = z;
       const int m = min(n, kWU);
       for (int i = 1; i < m; ++i) {
-        s += zi * x[(lo + i) * stride];
+        s += zi * (g * x[(lo + i) * stride]);
         zi *= z;
       }
-      const double c0 = x[lo * stride];
+      const double c0 = g * x[lo * stride];
       acc = (c0 + s) * z + c0;
     }
   } else {
-    acc = x[lo * stride];
+    acc = g * x[lo * stride];
   }
   x[lo * stride] = acc;
-  for (int k = lo + 1; k < hi; ++k) {
-    acc = x[k * stride] + z * acc;
+  int k = lo + 1;
+  for (; k + U <= hi; k += U) {
+    double v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) v[u] = g * x[(k + u) * stride];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      acc = v[u] + z * acc;
+      x[(k + u) * stride] = acc;
+    }
+  }
+  for (; k < hi; ++k) {
+    acc = g * x[k * stride] + z * acc;
     x[k * stride] = acc;
   }
   acc = exact_hi ? x[(hi - 1) * stride] * (z / (z - 1.0)) : -z * x[(hi - 1) * stride];
   x[(hi - 1) * stride] = acc;
-  for (int k = hi - 2; k >= lo; --k) {
+  k = hi - 2;
+  for (; k - U + 1 >= lo; k -= U) {
+    double v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) v[u] = x[(k - u) * stride];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      acc = z * (acc - v[u]);
+      x[(k - u) * stride] = acc;
+    }
+  }
+  for (; k >= lo; --k) {
     acc = z * (acc - x[k * stride]);
     x[k * stride] = acc;
   }
@@ -343,11 +367,12 @@ __global__ void __launch_bounds__(128) bspline_tile_kernel(const float* c32, con
 }
 
 __device__ __forceinline__ void bspline_w(double t, double* wgt) {
-  const double u = 1.0 - t;
-  wgt[0] = u * u * u / 6.0;
-  wgt[1] = (4.0 - 6.0 * t * t + 3.0 * t * t * t) / 6.0;
-  wgt[2] = (1.0 + 3.0 * t + 3.0 * t * t - 3.0 * t * t * t) / 6.0;
-  wgt[3] = t * t * t / 6.0;
+  constexpr double k6 = 1.0 / 6.0;   // multiply: fp64 division is a subroutine call
+  const double u = 1.0 - t, t2 = t * t, t3 = t2 * t;
+  wgt[0] = u * u * u * k6;
+  wgt[1] = (4.0 - 6.0 * t2 + 3.0 * t3) * k6;
+  wgt[2] = (1.0 + 3.0 * t + 3.0 * t2 - 3.0 * t3) * k6;
+  wgt[3] = t3 * k6;
 }
 
 // spline value at fine pixel (i, j) of an h x w target from a ch x cw map
@@ -582,40 +607,55 @@ __global__ void __launch_bounds__(kTX * kTY) stats_tiled_kernel(const double* im
                                                               int64_t ld, double sigma_eps,
                                                               float* mu32, float* is32,
                                                               int64_t lds) {
+  // Separable box sums of x' and x'^2 (x' = x - c, c the tile's first sample,
+  // fp64); windows whose shifted variance cancels to < 1e-9 of E[x'^2]
+  // (flat or near-flat) recompute it centred from the tile, so flat blocks
+  // keep sigma == 0 exactly (zncc.py:182-189 degeneracy rule).
   constexpr int H2 = B / 2, TR = kTY + B - 1, TC = kTX + B - 1;
   __shared__ double T[TR][TC];
-  __shared__ double Hs[TR][kTX];
+  __shared__ double H1[TR][kTX], H2s[TR][kTX];
   const int x0 = blockIdx.x * kTX, y0 = blockIdx.y * kTY;
   const int tid = threadIdx.y * kTX + threadIdx.x;
+  const double c = img[(int64_t)clampi(y0, 0, h - 1) * ld + clampi(x0, 0, w - 1)];
   for (int t = tid; t < TR * TC; t += kTX * kTY) {
-    const int r = t / TC, c = t - r * TC;
-    T[r][c] = img[(int64_t)clampi(y0 - H2 + r, 0, h - 1) * ld + clampi(x0 - H2 + c, 0, w - 1)];
+    const int r = t / TC, cc = t - r * TC;
+    T[r][cc] = img[(int64_t)clampi(y0 - H2 + r, 0, h - 1) * ld + clampi(x0 - H2 + cc, 0, w - 1)] - c;
   }
   __syncthreads();
   for (int t = tid; t < TR * kTX; t += kTX * kTY) {
-    const int r = t / kTX, c = t - r * kTX;
-    double s = 0.0;
+    const int r = t / kTX, cc = t - r * kTX;
+    double s1 = 0.0, s2 = 0.0;
 #pragma unroll
-    for (int k = 0; k < B; ++k) s += T[r][c + k];
-    Hs[r][c] = s;
+    for (int k = 0; k < B; ++k) {
+      const double v = T[r][cc + k];
+      s1 += v;
+      s2 = fma(v, v, s2);
+    }
+    H1[r][cc] = s1;
+    H2s[r][cc] = s2;
   }
   __syncthreads();
   const int x = x0 + threadIdx.x, y = y0 + threadIdx.y;
   if (x >= w || y >= h) return;
-  double s = 0.0;
+  double s1 = 0.0, s2 = 0.0;
 #pragma unroll
-  for (int k = 0; k < B; ++k) s += Hs[threadIdx.y + k][threadIdx.x];
-  const double mu = s / (double)(B * B);
-  double ss = 0.0;
+  for (int k = 0; k < B; ++k) s1 += H1[threadIdx.y + k][threadIdx.x], s2 += H2s[threadIdx.y + k][threadIdx.x];
+  constexpr double inv = 1.0 / (double)(B * B);
+  const double m1 = s1 * inv, m2 = s2 * inv;
+  double var = m2 - m1 * m1;
+  if (var <= 1e-9 * m2) {
+    double ss = 0.0;
 #pragma unroll
-  for (int r = 0; r < B; ++r)
+    for (int r = 0; r < B; ++r)
 #pragma unroll
-    for (int c = 0; c < B; ++c) {
-      const double dv = T[threadIdx.y + r][threadIdx.x + c] - mu;
-      ss = fma(dv, dv, ss);
-    }
-  const double sigma = sqrt(ss / (double)(B * B));
-  mu32[(int64_t)y * lds + x] = (float)mu;
+      for (int cc = 0; cc < B; ++cc) {
+        const double dv = T[threadIdx.y + r][threadIdx.x + cc] - m1;
+        ss = fma(dv, dv, ss);
+      }
+    var = ss * inv;
+  }
+  const double sigma = sqrt(fmax(var, 0.0));
+  mu32[(int64_t)y * lds + x] = (float)(m1 + c);
   is32[(int64_t)y * lds + x] = sigma >= sigma_eps ? (float)(1.0 / sigma) : 0.f;
 }
 
@@ -623,11 +663,10 @@ __global__ void __launch_bounds__(kTX * kTY) stats_tiled_kernel(const double* im
 __global__ void __launch_bounds__(kTX * kTY) prior_eval_tiled_kernel(
     const int16_t* dco, int64_t ldd, int ch, int cw, const double* coef, int64_t ldc, int h,
     int w, int d, int r, double beta, int* wc, int64_t ldw, unsigned long long* counters,
-    RowBand band) {
+    RowBand band, double ry, double rx) {
   constexpr int CR = 12, CC = 24;
   __shared__ double Cs[CR][CC];
   const int nh = ch + 2 * kNpad, nw = cw + 2 * kNpad;
-  const double ry = (double)ch / (double)h, rx = (double)cw / (double)w;
   const int i0 = band.lo + blockIdx.y * kTY, j0 = blockIdx.x * kTX;
   const int ylo = (int)floor(((double)i0 + 0.5) * ry - 0.5 + kNpad) - 1;
   const int xlo = (int)floor(((double)j0 + 0.5) * rx - 0.5 + kNpad) - 1;
@@ -704,14 +743,39 @@ __global__ void __launch_bounds__(kTX * kTY) median_tiled_kernel(
     const int16_t d0 = Ds[ty][tx];
     int16_t res = d0;
     if ((double)Cs[ty][tx] <= alpha) {
-      int v[24];
+      // qualifying neighbours in static slots (others = +inf sentinel), a
+      // 32-wide bitonic network, then the lower median (n-1)/2
+      int v[32];
       int n = 0;
 #pragma unroll
-      for (int di = -2; di <= 2; ++di)
+      for (int t = 0; t < 32; ++t) {
+        const int di = t / 5 - 2, dj = t % 5 - 2;
+        bool q = false;
+        if (t < 25 && t != 12) q = (double)Cs[ty + di][tx + dj] > alpha;
+        v[t] = q ? (int)Ds[ty + di][tx + dj] : 0x7fffffff;
+        n += q;
+      }
+      if (n > 0) {
 #pragma unroll
-        for (int dj = -2; dj <= 2; ++dj)
-          if ((di | dj) != 0 && (double)Cs[ty + di][tx + dj] > alpha) v[n++] = Ds[ty + di][tx + dj];
-      if (n > 0) res = (int16_t)lower_median(v, n);
+        for (int k = 2; k <= 32; k <<= 1)
+#pragma unroll
+          for (int jj = k >> 1; jj > 0; jj >>= 1)
+#pragma unroll
+            for (int t = 0; t < 32; ++t) {
+              const int l = t ^ jj;
+              if (l > t) {
+                const int a = v[t], b = v[l];
+                const bool up = (t & k) == 0;
+                v[t] = up ? min(a, b) : max(a, b);
+                v[l] = up ? max(a, b) : min(a, b);
+              }
+            }
+        const int m = (n - 1) >> 1;
+        int pick = v[0];
+#pragma unroll
+        for (int t = 1; t < 24; ++t) pick = (m == t) ? v[t] : pick;
+        res = (int16_t)pick;
+      }
     }
     out[(int64_t)i * ld + j] = res;
     changed = res != d0;
@@ -796,7 +860,8 @@ cudaError_t launch_prior_eval(const int16_t* dcoarse, int64_t ldd, int ch,
   dim3 blk(32, 8);
   const dim3 g((w + 31) / 32, (rows.hi - rows.lo + 7) / 8);
   prior_eval_tiled_kernel<<<g, blk, 0, s>>>(dcoarse, ldd, ch, cw, coef, ldc, h, w, d, radius,
-                                            beta, wc, ldw, counters, rows);
+                                            beta, wc, ldw, counters, rows, (double)ch / (double)h,
+                                            (double)cw / (double)w);
   return cudaGetLastError();
 }
 
