@@ -37,6 +37,10 @@ struct LevelBuf {
   uint8_t* low = nullptr;
   double* coef = nullptr;   // spline coefficients of this level's cost map
   int64_t ldc = 0;
+  float* Rp = nullptr;      // padded staging arrays of the sweep (prep_staging)
+  float2* Mp = nullptr;
+  int64_t ldp = 0;
+  int pc = 0;
   RowBand rows{0, 0, 0, 0};  // sweep/prior/median rows and counted rows
 };
 
@@ -90,6 +94,10 @@ struct mshbm_engine {
   double *L = nullptr, *R = nullptr;
   double *muL = nullptr, *sgL = nullptr, *muR = nullptr, *sgR = nullptr;
   float *muR32 = nullptr, *isR32 = nullptr;
+  float* Rp = nullptr;
+  float2* Mp = nullptr;
+  int64_t ldp = 0;
+  int pc = 0;
   int* wc = nullptr;
   int16_t *fz = nullptr, *wz = nullptr, *nz = nullptr;
   float *fc = nullptr, *wcst = nullptr, *nc = nullptr;
@@ -179,6 +187,10 @@ void carve(Plan& p, Carver& cv) {
     l.low = cv.take<uint8_t>(n);
     l.ldc = round_up(l.w + 24, 32);
     l.coef = cv.take<double>((size_t)l.ldc * (l.h + 24) * 2);   // + IIR scratch
+    l.pc = staging_margin(l.d, l.b);
+    l.ldp = round_up(l.w + 2 * l.pc, 32);
+    l.Rp = cv.take<float>((size_t)l.ldp * l.h);
+    l.Mp = cv.take<float2>((size_t)l.ldp * l.h);
   }
 }
 
@@ -241,7 +253,8 @@ int enqueue(mshbm_ctx* ctx, Plan& p, cudaStream_t s, std::vector<StageEvents>* t
   for (int k = 0; k <= p.K; ++k) {
     LevelBuf& l = p.lv[k];
     CK(launch_stats_f32(l.R, l.h, l.w, l.ld, l.b, cfg.sigma_eps, l.muR, l.isR, l.ld, s));
-    ++n;
+    CK(launch_prep_staging(l.R, l.ld, l.muR, l.isR, l.ld, l.h, l.w, l.pc, l.Rp, l.Mp, l.ldp, s));
+    n += 2;
   }
   for (int k = p.K; k >= 0; --k) {
     LevelBuf& l = p.lv[k];
@@ -267,6 +280,7 @@ int enqueue(mshbm_ctx* ctx, Plan& p, cudaStream_t s, std::vector<StageEvents>* t
     a.dout = l.dsel; a.cout = l.c; a.low = l.low; a.ldo = l.ld;
     a.counters = cnt;
     a.rows = l.rows;
+    a.Rp = l.Rp; a.Mp = l.Mp; a.ldp = l.ldp; a.pc = l.pc;
     if (ev) CK(cudaEventRecord(ev->sel0, s));
     CK(launch_sweep(a, s, &n));
     if (ev) CK(cudaEventRecord(ev->sel1, s));
@@ -755,6 +769,10 @@ int mshbm_engine_create(mshbm_ctx* ctx, const double* left, const double* right,
     e->muL = cv.take<double>(nd); e->sgL = cv.take<double>(nd);
     e->muR = cv.take<double>(nd); e->sgR = cv.take<double>(nd);
     e->muR32 = cv.take<float>(n); e->isR32 = cv.take<float>(n);
+    e->pc = staging_margin(d_max, block);
+    e->ldp = round_up(width + 2 * e->pc, 32);
+    e->Rp = cv.take<float>((size_t)e->ldp * height);
+    e->Mp = cv.take<float2>((size_t)e->ldp * height);
     e->wc = cv.take<int>(n);
     e->fz = cv.take<int16_t>(nd); e->wz = cv.take<int16_t>(nd); e->nz = cv.take<int16_t>(nd);
     e->fc = cv.take<float>(nd); e->wcst = cv.take<float>(nd); e->nc = cv.take<float>(nd);
@@ -774,7 +792,9 @@ int mshbm_engine_create(mshbm_ctx* ctx, const double* left, const double* right,
   CK(launch_stats_f64(e->L, height, width, e->ld, block, e->muL, e->sgL, s));
   CK(launch_stats_f64(e->R, height, width, e->ld, block, e->muR, e->sgR, s));
   CK(launch_stats_f32(e->R, height, width, e->ld, block, sigma_eps, e->muR32, e->isR32, e->ld, s));
-  ctx->launches += 3;
+  CK(launch_prep_staging(e->R, e->ld, e->muR32, e->isR32, e->ld, height, width, e->pc, e->Rp,
+                         e->Mp, e->ldp, s));
+  ctx->launches += 4;
   CK(cudaStreamSynchronize(s));
   *out = e;
   return MSHBM_OK;
@@ -868,6 +888,7 @@ static SweepArgs raw_args(mshbm_engine* e, const int* wc, int radius) {
   a.alpha = 0.5; a.mode = kSweepRaw;
   a.fz = e->fz; a.fc = e->fc; a.wz = e->wz; a.wcst = e->wcst; a.nz = e->nz; a.nc = e->nc;
   a.rows = RowBand{0, e->H, 0, e->H};
+  a.Rp = e->Rp; a.Mp = e->Mp; a.ldp = e->ldp; a.pc = e->pc;
   return a;
 }
 

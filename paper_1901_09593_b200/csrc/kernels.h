@@ -40,6 +40,12 @@ struct SweepArgs {
   int64_t ldo;
   unsigned long long* counters;
   RowBand rows;         // output rows computed / counted
+  // padded fp32 staging arrays (prep_staging): R' = R - c and (muR - c,
+  // 1/sigma_R | NaN), column margins of `pc` on both sides, row stride ldp
+  const float* Rp;
+  const float2* Mp;
+  int64_t ldp;
+  int pc;
   // raw outputs (dense H x W): full, window, 3x3-summed winners
   int16_t* fz; float* fc; int16_t* wz; float* wcst; int16_t* nz; float* nc;
 };
@@ -48,6 +54,14 @@ bool sweep_supported_block(int b);
 // two-pixels-per-thread variant (sweep2.cu) for b in {3,5,7,9,11}
 bool sweep2_supported(int b);
 cudaError_t launch_sweep2(const SweepArgs& a, cudaStream_t s);
+
+// Column margin of the padded staging arrays for search bound d, block b.
+inline int staging_margin(int d, int b) { return (d + 16 + b + 40 + 3) / 4 * 4; }
+// Rp = fl32(R - c) (replicate-padded columns), Mp = (muR - c, isR > 0 ? isR :
+// NaN) inside the image and (0, NaN) in the margins; c = muR at the centre.
+cudaError_t launch_prep_staging(const double* R, int64_t ld, const float* muR, const float* isR,
+                                int64_t lds, int h, int w, int pc, float* Rp, float2* Mp,
+                                int64_t ldp, cudaStream_t s);
 
 // ---------------------------------------------------------------- pyramid
 cudaError_t launch_f32_to_f64(const float* a, const float* b, int h, int w,

@@ -788,6 +788,26 @@ __global__ void __launch_bounds__(kTX * kTY) median_tiled_kernel(
   block_accumulate<2>(counters, slot, val, mx);
 }
 
+// ------------------------------------------------------------------ staging
+__global__ void prep_staging_kernel(const double* R, int64_t ld, const float* muR,
+                                    const float* isR, int64_t lds, int h, int w, int pc,
+                                    float* Rp, float2* Mp, int64_t ldp) {
+  const int xp = blockIdx.x * blockDim.x + threadIdx.x;   // padded column
+  const int y = blockIdx.y * blockDim.y + threadIdx.y;
+  if (y >= h || xp >= w + 2 * pc) return;
+  const float c = muR[(int64_t)(h / 2) * lds + w / 2];
+  const int x = xp - pc;
+  const int xc = clampi(x, 0, w - 1);
+  Rp[(int64_t)y * ldp + xp] = (float)(R[(int64_t)y * ld + xc] - (double)c);
+  const float qnan = __int_as_float(0x7fc00000);
+  float2 m = make_float2(0.f, qnan);
+  if (x >= 0 && x < w) {
+    const float is = isR[(int64_t)y * lds + x];
+    m = make_float2(muR[(int64_t)y * lds + x] - c, is > 0.f ? is : qnan);
+  }
+  Mp[(int64_t)y * ldp + xp] = m;
+}
+
 }  // namespace
 
 // ------------------------------------------------------------------ launchers
@@ -796,6 +816,15 @@ cudaError_t launch_f32_to_f64(const float* a, const float* b, int h, int w,
                               int64_t ld_out, cudaStream_t s) {
   dim3 blk(64, 4);
   f32_to_f64_kernel<<<grid2d(w, h, blk, b ? 2 : 1), blk, 0, s>>>(a, b, h, w, ld_in, oa, ob, ld_out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_prep_staging(const double* R, int64_t ld, const float* muR, const float* isR,
+                                int64_t lds, int h, int w, int pc, float* Rp, float2* Mp,
+                                int64_t ldp, cudaStream_t s) {
+  dim3 blk(64, 4);
+  prep_staging_kernel<<<grid2d(w + 2 * pc, h, blk), blk, 0, s>>>(R, ld, muR, isR, lds, h, w, pc,
+                                                                  Rp, Mp, ldp);
   return cudaGetLastError();
 }
 

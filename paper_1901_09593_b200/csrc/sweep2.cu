@@ -24,6 +24,17 @@ namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
 
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(d), "l"(src));
+}
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(src));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
+
 template <int B, int ZC, int NR>
 struct Sweep2Smem {
   static constexpr int NROW = 2 * NR;
@@ -108,8 +119,6 @@ sweep2_kernel(const SweepArgs a) {
   constexpr int H2 = B / 2;
   constexpr int NT = NR * 32;
   constexpr int NROW = SM::NROW, RW = SM::RW, RR = SM::RR, SW = SM::SW, LC = SM::LC;
-  constexpr int KR = (RR * RW + NT - 1) / NT;
-  constexpr int KS = (NROW * SW + NT - 1) / NT;
   extern __shared__ float4 smem4[];
   typename SM::RsT* Rs = reinterpret_cast<typename SM::RsT*>(smem4);
   typename SM::MsT* Ms = reinterpret_cast<typename SM::MsT*>(Rs + 2);
@@ -130,56 +139,25 @@ sweep2_kernel(const SweepArgs a) {
   const bool innerB = inB && lanein && wp <= NR - 2;
   const float qnan = __int_as_float(0x7fc00000);
 
-  const double cR = a.R[(int64_t)clampi(y0 + NR - 1, 0, H - 1) * a.ld + clampi(x0 + 15, 0, W - 1)];
-  const float cRf = (float)cR;
-
-  double pr[KR];
-  float2 pm[KS];
-  auto fetch = [&](int z0) {
+  // ---- staging: cp.async from the padded fp32 arrays (prep_staging) straight
+  // into the double-buffered strip; no clamps on columns, no conversion, no
+  // prefetch registers.  Warp w copies rows w, w+NR, ...
+  const float* __restrict__ Rp = a.Rp + a.pc;
+  const float2* __restrict__ Mp = a.Mp + a.pc;
+  auto issue = [&](int buf, int z0) {
     const int s0 = DIR > 0 ? (x0 - 1 - H2 - z0 - (ZC - 1)) : (x0 - 1 - H2 + z0);
-#pragma unroll
-    for (int k = 0; k < KR; ++k) {
-      const int t = threadIdx.x + k * NT;
-      if (t < RR * RW) {
-        const int rr = t / RW, e = t - rr * RW;
-        pr[k] = a.R[(int64_t)clampi(y0 - 1 - H2 + rr, 0, H - 1) * a.ld + clampi(s0 + e, 0, W - 1)];
-      }
+    for (int rr = wp; rr < RR; rr += NR) {
+      const float* src = Rp + (int64_t)clampi(y0 - 1 - H2 + rr, 0, H - 1) * a.ldp + s0;
+      for (int e = lane; e < RW; e += 32) cp_async4(&Rs[buf][rr][e], src + e);
     }
     const int q0 = DIR > 0 ? (x0 - 1 - z0 - (ZC - 1)) : (x0 - 1 + z0);
-#pragma unroll
-    for (int k = 0; k < KS; ++k) {
-      const int t = threadIdx.x + k * NT;
-      if (t < NROW * SW) {
-        const int rr = t / SW, e = t - rr * SW;
-        const int64_t o = (int64_t)clampi(y0 - 1 + rr, 0, H - 1) * a.lds + clampi(q0 + e, 0, W - 1);
-        pm[k] = make_float2(a.muR[o], a.isR[o]);   // raw; validity applied at store time
-      }
+    for (int rr = wp; rr < NROW; rr += NR) {
+      const float2* src = Mp + (int64_t)clampi(y0 - 1 + rr, 0, H - 1) * a.ldp + q0;
+      for (int e = lane; e < SW; e += 32) cp_async8(&Ms[buf][rr][e], src + e);
     }
+    cp_async_commit();
   };
-  auto store = [&](int buf, int z0) {
-#pragma unroll
-    for (int k = 0; k < KR; ++k) {
-      const int t = threadIdx.x + k * NT;
-      if (t < RR * RW) {
-        const int rr = t / RW, e = t - rr * RW;
-        Rs[buf][rr][e] = (float)(pr[k] - cR);
-      }
-    }
-    const int q0 = DIR > 0 ? (x0 - 1 - z0 - (ZC - 1)) : (x0 - 1 + z0);
-#pragma unroll
-    for (int k = 0; k < KS; ++k) {
-      const int t = threadIdx.x + k * NT;
-      if (t < NROW * SW) {
-        const int rr = t / SW, e = t - rr * SW;
-        const int gq = q0 + e;
-        const bool valid = gq >= 0 && gq < W && pm[k].y > 0.f;
-        // (muR - c, 1/sigma_R); NaN marks a right centre outside the image or
-        // a degenerate right block: its cost becomes exactly -1 (fmaxf)
-        Ms[buf][rr][e] = make_float2(pm[k].x - cRf, valid ? pm[k].y : qnan);
-      }
-    }
-  };
-  fetch(0);
+  issue(0, 0);
 
   // ---- left tile (fp64) through shared memory (aliases Hx, written later)
   using LsT = typename SM::LsT;
@@ -257,12 +235,12 @@ sweep2_kernel(const SweepArgs a) {
   float nbv[2] = {-3.0e38f, -3.0e38f};
   int nbz[2] = {0, 0};
 
-  store(0, 0);
+  cp_async_wait_all();
   __syncthreads();
   int cur = 0;
   for (int z0 = 0; z0 <= zmax; z0 += ZC, cur ^= 1) {
     const bool more = z0 + ZC <= zmax;
-    if (more) fetch(z0 + ZC);
+    if (more) issue(cur ^ 1, z0 + ZC);   // lands during this chunk's math
     const bool wchunk = __any_sync(kFull, (trusted[0] && wlo[0] <= z0 + ZC - 1 && whi[0] >= z0) ||
                                              (trusted[1] && wlo[1] <= z0 + ZC - 1 && whi[1] >= z0));
     int nz;
@@ -276,7 +254,7 @@ sweep2_kernel(const SweepArgs a) {
         chunk2<B, DIR, ZC, NR, 4>(Rs[cur], Ms[cur], Hx[cur], Lt, Lb, kLA, kLB, dW, z0, zo, zmax,
                                   inA, inB, lane, wp, best, bestz, wchunk, wlo, whi);
     }
-    if (more) store(cur ^ 1, z0 + ZC);
+    cp_async_wait_all();
     __syncthreads();
     const typename SM::HxT& hx = Hx[cur];
     if (innerA) {
@@ -367,7 +345,7 @@ template <int DIR>
 cudaError_t launch2_dir(const SweepArgs& a, cudaStream_t s) {
   if (DIR > 0) {
     switch (v2() * 100 + a.block) {
-      case 107: return launch2<7, DIR, 16, 8, 2>(a, s);
+      case 107: return launch2<7, DIR, 12, 16, 1>(a, s);
       case 207: return launch2<7, DIR, 16, 8, 1>(a, s);
       case 109: return launch2<9, DIR, 8, 8, 2>(a, s);
       case 209: return launch2<9, DIR, 12, 8, 1>(a, s);
@@ -384,7 +362,7 @@ cudaError_t launch2_dir(const SweepArgs& a, cudaStream_t s) {
   switch (a.block) {
     case 3: return launch2<3, DIR, 16, 8, 2>(a, s);
     case 5: return launch2<5, DIR, 16, 8, 2>(a, s);
-    case 7: return launch2<7, DIR, 12, 16, 1>(a, s);
+    case 7: return launch2<7, DIR, 16, 8, 2>(a, s);
     case 9: return launch2<9, DIR, 16, 8, 1>(a, s);
     case 11: return launch2<11, DIR, 16, 8, 1>(a, s);
     default: return cudaErrorInvalidValue;
