@@ -59,21 +59,20 @@ MSHBM_DEV int kCntCopyStride(unsigned b) { return (int)(b % kCntCopies); }
 template <int NSLOT>
 MSHBM_DEV void block_accumulate(unsigned long long* __restrict__ gdst, const int (&slot)[NSLOT],
                                 const unsigned long long (&val)[NSLOT], const bool (&is_max)[NSLOT]) {
-  __shared__ unsigned long long acc[NSLOT];
+  // per-thread values are small (< 2^32 per block): 32-bit warp reductions
+  // (REDUX, one instruction), 32-bit shared atomics, one 64-bit global
+  // atomic per block and slot
+  __shared__ unsigned acc[NSLOT];
   const int tid = threadIdx.x + blockDim.x * (threadIdx.y + blockDim.y * threadIdx.z);
-  if (tid < NSLOT) acc[tid] = 0ull;
+  if (tid < NSLOT) acc[tid] = 0u;
   __syncthreads();
 #pragma unroll
   for (int k = 0; k < NSLOT; ++k) {
-    unsigned long long x = val[k];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const unsigned long long y = __shfl_xor_sync(0xffffffffu, x, o);
-      x = is_max[k] ? (y > x ? y : x) : x + y;
-    }
-    if ((tid & 31) == 0 && x) {
-      if (is_max[k]) atomicMax(&acc[k], x);
-      else atomicAdd(&acc[k], x);
+    const unsigned x = (unsigned)val[k];
+    const unsigned r = is_max[k] ? __reduce_max_sync(0xffffffffu, x) : __reduce_add_sync(0xffffffffu, x);
+    if ((tid & 31) == 0 && r) {
+      if (is_max[k]) atomicMax(&acc[k], r);
+      else atomicAdd(&acc[k], r);
     }
   }
   __syncthreads();
@@ -82,8 +81,8 @@ MSHBM_DEV void block_accumulate(unsigned long long* __restrict__ gdst, const int
   // L2; the host sums (or maxes) the copies when it reads the trace
   if (tid < NSLOT && acc[tid]) {
     unsigned long long* dst = gdst + (size_t)kCntSlots * kCntCopyStride(blockIdx.x + gridDim.x * blockIdx.y) + slot[tid];
-    if (is_max[tid]) atomicMax(dst, acc[tid]);
-    else atomicAdd(dst, acc[tid]);
+    if (is_max[tid]) atomicMax(dst, (unsigned long long)acc[tid]);
+    else atomicAdd(dst, (unsigned long long)acc[tid]);
   }
 }
 
