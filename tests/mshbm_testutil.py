@@ -56,3 +56,38 @@ def counts_close(a, b, rel=2e-3):
     if np.array_equal(a, b):
         return True
     return bool(np.all(np.abs(a - b) <= rel * np.maximum(np.abs(b), 1.0) + 2))
+
+
+def classify_mismatches(d_gpu, d_ref, left, right, block, d_max, sign="middlebury",
+                        tol=1e-4):
+    """Explain level-0 disparity mismatches.
+
+    A mismatch is a *near tie* when the reference's own cost or its clipped
+    3x3-averaged cost differs by < ``tol`` between the two disparities, and
+    a *median descendant* when it lies within the 5x5 median window of a
+    near tie.  Returns (n_mismatch, n_near_tie, n_descendant, n_unexplained).
+    """
+    from oracle import mshbm_oracle as O
+    d_gpu = np.asarray(d_gpu).astype(np.int64)
+    d_ref = np.asarray(d_ref).astype(np.int64)
+    bad = np.argwhere(d_gpu != d_ref)
+    if bad.size == 0:
+        return 0, 0, 0, 0
+    e = O.Engine(left, right, block, d_max, sign=sign)
+    h, w = d_ref.shape
+    ties = []
+    for i, j in bad:
+        a, b = int(d_gpu[i, j]), int(d_ref[i, j])
+        own = e.dsi_rows(np.array([i]), np.array([j]))[0]
+        nb = [(i + p, j + q) for p in (-1, 0, 1) for q in (-1, 0, 1)
+              if 0 <= i + p < h and 0 <= j + q < w]
+        s = e.dsi_rows(np.array([r for r, _ in nb]), np.array([c for _, c in nb])).sum(0)
+        ties.append(min(abs(own[a] - own[b]), abs(s[a] - s[b]) / len(nb)) < tol)
+    ties = np.array(ties)
+    tie_px = bad[ties]
+    desc = 0
+    for k, (i, j) in enumerate(bad):
+        if not ties[k] and tie_px.size and np.any(np.max(np.abs(tie_px - [i, j]), axis=1) <= 2):
+            desc += 1
+    n = len(bad)
+    return n, int(ties.sum()), desc, n - int(ties.sum()) - desc

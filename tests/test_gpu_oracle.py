@@ -99,3 +99,48 @@ def test_baseline_configs_at_parity_size(gpu, name, shape):
     assert frac <= 5e-4 or (frac * d.size) <= 2, f"{name}: {frac:.4%} flipped"
     assert cerr <= 1e-4 and med <= 1e-6
     assert counts_close(counts_of(tr), counts_of(otr))
+
+
+def test_gate_variants_match_oracle(gpu):
+    """Non-default alpha/beta move many pixels across the gates."""
+    from oracle import mshbm_oracle as O
+    left, right = _pair(96, 128, 21)
+    for alpha, beta in ((0.5, 0.99), (0.97, 0.6)):
+        cfg = gpu.MatchConfig(d_max=24, levels=2, block=5, radius=2, alpha=alpha, beta=beta)
+        d, c, tr = gpu.run_pipeline(left, right, cfg)
+        od, oc, otr = O.run_pipeline(left, right, 24, 2, 5, alpha=alpha, beta=beta, radius=2)
+        frac, cerr, med = parity_report(d, c, od, oc)
+        assert frac <= 5e-4 or frac * d.size <= 2
+        assert cerr <= 1e-4 and med <= 1e-6
+        assert counts_close(counts_of(tr), counts_of(otr))
+
+
+def test_unit_range_images_match_oracle(gpu):
+    """[0, 1] float64 images (the reference test-suite convention)."""
+    from oracle import mshbm_oracle as O
+    rng = np.random.default_rng(33)
+    left = rng.random((40, 56))
+    right = np.roll(left, -3, axis=1) + 0.01 * rng.random((40, 56))
+    cfg = gpu.MatchConfig(d_max=8, levels=1, block=5)
+    d, c, _ = gpu.run_pipeline(left, right, cfg)
+    od, oc, _ = O.run_pipeline(left, right, 8, 1, 5)
+    frac, cerr, med = parity_report(d, c, od, oc)
+    assert frac <= 1e-3 and cerr <= 1e-4
+
+
+def test_tiny_and_degenerate_shapes(gpu):
+    from oracle import mshbm_oracle as O
+    rng = np.random.default_rng(34)
+    for h, w in ((3, 3), (4, 7), (9, 2)):
+        left, right = rng.random((h, w)) * 255, rng.random((h, w)) * 255
+        cfg = gpu.MatchConfig(d_max=3, levels=0, block=3)
+        d, c, _ = gpu.run_pipeline(left, right, cfg)
+        od, oc, _ = O.run_pipeline(left, right, 3, 0, 3)
+        np.testing.assert_array_equal(d, od)
+        np.testing.assert_allclose(c, oc, atol=1e-5)
+    with pytest.raises(ValueError):
+        gpu.run_pipeline(np.zeros((0, 5)), np.zeros((0, 5)), gpu.MatchConfig(d_max=2, levels=0))
+    with pytest.raises(ValueError):
+        gpu.run_pipeline(np.zeros((8, 8)), np.zeros((8, 9)), gpu.MatchConfig(d_max=4, levels=0))
+    with pytest.raises(ValueError):   # too deep (pyramid.py:139-151)
+        gpu.run_pipeline(np.zeros((16, 16)), np.zeros((16, 16)), gpu.MatchConfig(d_max=64, levels=3))

@@ -13,7 +13,8 @@ import os
 import numpy as np
 import pytest
 
-from mshbm_testutil import GOLDEN, counts_close, counts_of, load_golden, parity_report
+from mshbm_testutil import (GOLDEN, classify_mismatches, counts_close, counts_of, load_golden,
+                            parity_report)
 
 pytestmark = pytest.mark.gpu
 
@@ -46,6 +47,11 @@ def test_pipeline_matches_reference_golden(gpu, name):
     assert frac <= TIE_BUDGET, f"{name}: {frac:.4%} pixels flipped"
     assert cerr <= COST_TOL, f"{name}: cost error {cerr:.3e}"
     assert med <= 1e-6, f"{name}: median cost error {med:.3e}"
+    # every disparity mismatch must be explained by an fp32-vs-fp64 near tie
+    n, ties, desc, unexplained = classify_mismatches(
+        d, g["disparity"], g["left"], g["right"], block, d_max,
+        "paper" if paper else "middlebury")
+    assert unexplained <= 1, f"{name}: {n} mismatches, {ties} near ties, {desc} descendants"
     assert d.dtype == np.float64 and c.dtype == np.float64
     assert counts_close(counts_of(trace), g["counts"]), (counts_of(trace), g["counts"])
 
