@@ -353,15 +353,21 @@ cudaError_t launch2_dir(const SweepArgs& a, cudaStream_t s) {
       case 103: return launch2<3, DIR, 24, 8, 2>(a, s);
       case 307: return launch2<7, DIR, 12, 8, 2>(a, s);
       case 407: return launch2<7, DIR, 16, 16, 1>(a, s);
-      case 305: return launch2<5, DIR, 16, 16, 1>(a, s);
+      case 305: return launch2<5, DIR, 16, 8, 2>(a, s);
       case 303: return launch2<3, DIR, 16, 16, 1>(a, s);
       case 507: return launch2<7, DIR, 8, 16, 1>(a, s);
+      case 405: return launch2<5, DIR, 12, 8, 2>(a, s);
+      case 505: return launch2<5, DIR, 16, 8, 1>(a, s);
+      case 403: return launch2<3, DIR, 12, 8, 2>(a, s);
+      case 503: return launch2<3, DIR, 16, 8, 1>(a, s);
+      case 409: return launch2<9, DIR, 12, 8, 1>(a, s);
+      case 509: return launch2<9, DIR, 16, 4, 1>(a, s);
       default: break;
     }
   }
   switch (a.block) {
     case 3: return launch2<3, DIR, 16, 8, 2>(a, s);
-    case 5: return launch2<5, DIR, 16, 8, 2>(a, s);
+    case 5: return launch2<5, DIR, 16, 16, 1>(a, s);
     case 7: return launch2<7, DIR, 16, 8, 2>(a, s);
     case 9: return launch2<9, DIR, 16, 8, 1>(a, s);
     case 11: return launch2<11, DIR, 16, 8, 1>(a, s);
