@@ -332,15 +332,24 @@ __global__ void __launch_bounds__(128) bspline_tile_kernel(const float* c32, con
   const int nh = ch + 2 * kNpad, nw = cw + 2 * kNpad;
   const int y0 = blockIdx.y * kTile, x0 = blockIdx.x * kTile;
   const int gy0 = y0 - kWU, gx0 = x0 - kWU;
-  for (int t = threadIdx.x; t < kExt * kExt; t += blockDim.x) {
-    const int r = t / kExt, c = t - r * kExt;
-    const int gy = gy0 + r, gx = gx0 + c;
-    double v = 0.0;
-    if (gy >= 0 && gy < nh && gx >= 0 && gx < nw) {
-      const int64_t o = (int64_t)clampi(gy - kNpad, 0, ch - 1) * ldcin + clampi(gx - kNpad, 0, cw - 1);
-      v = c32 ? (double)c32[o] : c64[o];
+  // rows of the tile are loaded by warps, 3 coalesced columns per lane
+  // (kExt = 96), all loads of a row in flight together
+  {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+    for (int r = warp; r < kExt; r += nwarp) {
+      const int gy = gy0 + r;
+      const bool rowin = gy >= 0 && gy < nh;
+      const int64_t ro = (int64_t)clampi(gy - kNpad, 0, ch - 1) * ldcin;
+      double v[3];
+#pragma unroll
+      for (int u = 0; u < 3; ++u) {
+        const int gx = gx0 + lane + 32 * u;
+        const int64_t o = ro + clampi(gx - kNpad, 0, cw - 1);
+        v[u] = (rowin && gx >= 0 && gx < nw) ? (c32 ? (double)c32[o] : c64[o]) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 3; ++u) S[r * SP + lane + 32 * u] = v[u];
     }
-    S[r * SP + c] = v;
   }
   __syncthreads();
   const double gain = (1.0 - kPole) * (1.0 - 1.0 / kPole);
@@ -617,6 +626,7 @@ __global__ void __launch_bounds__(kTX * kTY) stats_tiled_kernel(const double* im
   const int x0 = blockIdx.x * kTX, y0 = blockIdx.y * kTY;
   const int tid = threadIdx.y * kTX + threadIdx.x;
   const double c = img[(int64_t)clampi(y0, 0, h - 1) * ld + clampi(x0, 0, w - 1)];
+#pragma unroll 4
   for (int t = tid; t < TR * TC; t += kTX * kTY) {
     const int r = t / TC, cc = t - r * TC;
     T[r][cc] = img[(int64_t)clampi(y0 - H2 + r, 0, h - 1) * ld + clampi(x0 - H2 + cc, 0, w - 1)] - c;
