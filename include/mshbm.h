@@ -210,6 +210,17 @@ int mshbm_upsample_prior(mshbm_ctx* ctx, const double* d_coarse,
                          int32_t h, int32_t w, double* d_hat, double* c_hat,
                          void* stream);
 
+/* ---- scoring (SURVEY 8f "next": device-side evaluate) ------------------ */
+/* evaluate (evaluation.py:77-109) on device arrays of n pixels: disparity
+ * (f64, NaN = invalid), gt_values (f64), gt_invalid (u8), scale > 0,
+ * taus[3] = bad thresholds (1, 2, 4).  Host outputs: counts[6] = {evaluated,
+ * bad_tau0, bad_tau1, bad_tau2, gt_invalid, output_invalid}, abs_err_sum =
+ * sum over evaluated pixels of |disparity*scale - gt|.  Synchronises. */
+int mshbm_evaluate(mshbm_ctx* ctx, const double* disparity, const double* gt_values,
+                   const uint8_t* gt_invalid, int64_t n, double scale,
+                   const double* taus, int64_t* counts, double* abs_err_sum,
+                   void* stream);
+
 /* ---- diagnostics ------------------------------------------------------- */
 /* FP32 FFMA throughput of `device` (8 CTAs/SM x 256 threads, 8 independent
  * FMA chains per thread, `iters` x 128 FMAs): the roofline denominator of

@@ -564,3 +564,66 @@ def run_pipeline(left, right, d_max, levels=None, block=11, alpha=0.9,
 
 def total_evals(trace):
     return sum(t["selection_evals"] + t["refine_evals"] for t in trace)
+
+
+# ---------------------------------------------------------------------------
+# SURVEY §8(f) "next" rows: the naive baseline and scoring
+# ---------------------------------------------------------------------------
+
+def baseline_bm(left, right, d_max, block, sigma_eps=1e-6, sign="middlebury"):
+    """Direct-form full search (baseline.py:18-81): per-block statistics
+    from scratch, no box-filter machinery, ties keep the smallest z.
+    Vectorised over pixels per disparity (the reference loops per pixel;
+    the arithmetic per pixel is the same)."""
+    left = np.asarray(left, dtype=np.float64)
+    right = np.asarray(right, dtype=np.float64)
+    if left.ndim != 2 or left.shape != right.shape:
+        raise ValueError("left/right shapes differ")
+    if block < 3 or block % 2 == 0:
+        raise ValueError("block must be odd and >= 3")
+    if d_max < 0:
+        raise ValueError("d_max must be >= 0")
+    if sign not in ("middlebury", "paper"):
+        raise ValueError("unknown sign convention")
+    h, w = left.shape
+    half = block // 2
+    area = block * block
+    step = -1 if sign == "middlebury" else 1
+    win = np.lib.stride_tricks.sliding_window_view
+    lb = win(np.pad(left, half, mode="edge"), (block, block))      # h, w, b, b
+    rb = win(np.pad(right, half, mode="edge"), (block, block))
+    ldev = lb - lb.mean(axis=(2, 3), keepdims=True)
+    lss = (ldev * ldev).sum(axis=(2, 3))
+    left_ok = np.sqrt(lss / area) >= sigma_eps
+    rdev = rb - rb.mean(axis=(2, 3), keepdims=True)
+    rss = (rdev * rdev).sum(axis=(2, 3))
+    right_ok = np.sqrt(rss / area) >= sigma_eps
+    best_c = np.full((h, w), -2.0)
+    best_z = np.zeros((h, w))
+    jj = np.arange(w)
+    for z in range(d_max + 1):
+        col = jj + step * z
+        inside = (col >= 0) & (col <= w - 1)
+        colc = np.clip(col, 0, w - 1)
+        num = (ldev * rdev[:, colc]).sum(axis=(2, 3))
+        ok = left_ok & right_ok[:, colc] & inside[None, :]
+        with np.errstate(invalid="ignore", divide="ignore"):
+            c = np.where(ok, num / np.sqrt(lss * rss[:, colc]), -1.0)
+        c = np.minimum(1.0, np.maximum(-1.0, c))
+        better = c > best_c
+        best_c = np.where(better, c, best_c)
+        best_z = np.where(better, float(z), best_z)
+    return best_z, best_c, h * w * (d_max + 1)
+
+
+def evaluate_counts(disparity, gt_values, gt_invalid, scale=1.0,
+                    thresholds=(1.0, 2.0, 4.0)):
+    """evaluation.py:77-109 as raw counts: (evaluated, [bad counts],
+    abs error sum, gt_invalid, output_invalid)."""
+    d = np.asarray(disparity, dtype=np.float64)
+    out_bad = ~np.isfinite(d)
+    gt_bad = np.asarray(gt_invalid, dtype=bool)
+    mask = ~out_bad & ~gt_bad
+    err = np.abs(d[mask] * scale - np.asarray(gt_values)[mask])
+    return (int(mask.sum()), [int((err > t).sum()) for t in thresholds],
+            float(err.sum()), int(gt_bad.sum()), int(out_bad.sum()))

@@ -2,8 +2,9 @@
 hot path (``/root/reference/pkg/src/pyrstereo``: pyramid, cost engine,
 matcher).  ``import paper_1901_09593_b200 as pyrstereo`` exposes the same
 names for the disparity path; the work runs in libmshbm.so (sm_100a CUDA)
-through the C ABI in include/mshbm.h.  Codecs, evaluation, the naive
-baseline and the CLI are out of scope.
+through the C ABI in include/mshbm.h.  The naive full-search baseline and
+scoring (``baseline_bm``, ``evaluate``) also run on the GPU; codecs and the
+CLI are out of scope.
 """
 
 from .matcher import (
@@ -47,6 +48,16 @@ from .zncc import (
 )
 
 from . import sharding  # noqa: E402
+from .synthetic import interior_mask, shifted_pair  # noqa: E402
+from .scoring import (  # noqa: E402
+    BAD_THRESHOLDS,
+    ComparisonSummary,
+    EvalReport,
+    GroundTruthDisparity,
+    baseline_bm,
+    compare,
+    evaluate,
+)
 
 __version__ = "0.1.0"
 
@@ -58,5 +69,7 @@ __all__ = [
     "gaussian_downsample", "level_block", "level_d_max", "match_coarsest",
     "match_level_with_prior", "patch_stats", "refine_level", "run_batch",
     "run_pipeline", "run_pipeline_band", "run_pipeline_device", "select_with_prior", "selective_median",
-    "upsample_prior", "zncc",
+    "upsample_prior", "zncc", "BAD_THRESHOLDS", "ComparisonSummary", "EvalReport",
+    "GroundTruthDisparity", "baseline_bm", "compare", "evaluate", "interior_mask",
+    "shifted_pair",
 ]

@@ -76,6 +76,8 @@ SIGNATURES = {
     "mshbm_refine_level": (C.c_int, [P, P, P, D, P, P, P, P]),
     "mshbm_selective_median": (C.c_int, [P, P, P, I32, I32, D, P, P, P]),
     "mshbm_upsample_prior": (C.c_int, [P, P, P, I32, I32, I32, I32, P, P, P]),
+    "mshbm_evaluate": (C.c_int, [P, P, P, P, I64, D, C.POINTER(D), C.POINTER(I64), C.POINTER(D),
+                                 P]),
     "mshbm_probe_fp32_peak": (C.c_int, [C.c_int, C.c_int, C.POINTER(D), C.POINTER(D)]),
     "mshbm_probe_fp64_peak": (C.c_int, [C.c_int, C.c_int, C.POINTER(D), C.POINTER(D)]),
 }

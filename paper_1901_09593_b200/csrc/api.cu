@@ -997,4 +997,25 @@ int mshbm_upsample_prior(mshbm_ctx* ctx, const double* d_coarse, const double* c
   return MSHBM_OK;
 }
 
+int mshbm_evaluate(mshbm_ctx* ctx, const double* disparity, const double* gt_values,
+                   const uint8_t* gt_invalid, int64_t n, double scale, const double* taus,
+                   int64_t* counts, double* abs_err_sum, void* stream) {
+  if (!ctx) return fail(nullptr, MSHBM_ERR_VALUE, "null context");
+  if (!(scale > 0.0)) return fail(ctx, MSHBM_ERR_VALUE, "scale must be positive");
+  CK(cudaSetDevice(ctx->device));
+  cudaStream_t s = pick(ctx, stream);
+  unsigned long long* dc = nullptr;
+  CK(cudaMallocAsync((void**)&dc, 7 * 8, s));
+  CK(cudaMemsetAsync(dc, 0, 7 * 8, s));
+  CK(launch_evaluate(disparity, gt_values, gt_invalid, n, scale, taus, dc, (double*)(dc + 6), s));
+  ctx->launches += 1;
+  unsigned long long h[7];
+  CK(cudaMemcpyAsync(h, dc, sizeof h, cudaMemcpyDeviceToHost, s));
+  CK(cudaFreeAsync(dc, s));
+  CK(cudaStreamSynchronize(s));
+  for (int q = 0; q < 6; ++q) counts[q] = (int64_t)h[q];
+  memcpy(abs_err_sum, &h[6], sizeof(double));
+  return MSHBM_OK;
+}
+
 }  // extern "C"

@@ -116,6 +116,11 @@ cudaError_t launch_median_f64(const double* d, const double* c, int h, int w,
                               double alpha, double* out,
                               unsigned long long* replaced, cudaStream_t s);
 
+// ---------------------------------------------------------------- evaluate
+cudaError_t launch_evaluate(const double* d, const double* gt, const uint8_t* gt_invalid,
+                            int64_t n, double scale, const double* taus,
+                            unsigned long long* counts, double* abs_sum, cudaStream_t s);
+
 // ---------------------------------------------------------------- engine
 struct EngineView {
   const double* L; const double* R; int64_t ld;

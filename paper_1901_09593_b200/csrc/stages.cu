@@ -3,6 +3,8 @@
 // helpers (direct fp64 evaluation, gate combines).
 #include <math.h>
 
+#include <algorithm>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -818,6 +820,45 @@ __global__ void prep_staging_kernel(const double* R, int64_t ld, const float* mu
   Mp[(int64_t)y * ldp + xp] = m;
 }
 
+// ------------------------------------------------------------------ evaluate
+// evaluation.py:77-109: on pixels valid in both maps, |d*scale - gt| vs the
+// bad thresholds, mean absolute error; invalid counts.  counts[] = {evaluated,
+// bad_t0, bad_t1, bad_t2, gt_invalid, output_invalid}.
+__global__ void evaluate_kernel(const double* d, const double* gt, const uint8_t* gt_invalid,
+                                int64_t n, double scale, double t0, double t1, double t2,
+                                unsigned long long* counts, double* abs_sum) {
+  unsigned long long c[6] = {0, 0, 0, 0, 0, 0};
+  double acc = 0.0;
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const double v = d[k];
+    const bool out_bad = !isfinite(v);
+    const bool gt_bad = gt_invalid[k] != 0;
+    c[4] += gt_bad;
+    c[5] += out_bad;
+    if (!out_bad && !gt_bad) {
+      const double e = fabs(v * scale - gt[k]);
+      c[0] += 1;
+      c[1] += e > t0;
+      c[2] += e > t1;
+      c[3] += e > t2;
+      acc += e;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+    for (int q = 0; q < 6; ++q) c[q] += __shfl_xor_sync(kFull, c[q], o);
+    acc += __shfl_xor_sync(kFull, acc, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+#pragma unroll
+    for (int q = 0; q < 6; ++q)
+      if (c[q]) atomicAdd(&counts[q], c[q]);
+    atomicAdd(abs_sum, acc);
+  }
+}
+
 }  // namespace
 
 // ------------------------------------------------------------------ launchers
@@ -826,6 +867,16 @@ cudaError_t launch_f32_to_f64(const float* a, const float* b, int h, int w,
                               int64_t ld_out, cudaStream_t s) {
   dim3 blk(64, 4);
   f32_to_f64_kernel<<<grid2d(w, h, blk, b ? 2 : 1), blk, 0, s>>>(a, b, h, w, ld_in, oa, ob, ld_out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_evaluate(const double* d, const double* gt, const uint8_t* gt_invalid,
+                            int64_t n, double scale, const double* taus,
+                            unsigned long long* counts, double* abs_sum, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  const int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 8);
+  evaluate_kernel<<<blocks, 256, 0, s>>>(d, gt, gt_invalid, n, scale, taus[0], taus[1], taus[2],
+                                         counts, abs_sum);
   return cudaGetLastError();
 }
 

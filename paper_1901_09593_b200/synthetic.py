@@ -26,7 +26,8 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-__all__ = ["StereoConfig", "CONFIGS", "make_pair", "gaussian_blur"]
+__all__ = ["StereoConfig", "CONFIGS", "make_pair", "gaussian_blur", "shifted_pair",
+           "interior_mask"]
 
 
 @dataclass(frozen=True)
@@ -170,3 +171,42 @@ def make_pair(cfg: StereoConfig, seed: int | None = None,
     right = right + rng.normal(0.0, cfg.noise, (h, w))
     return (left.astype(np.float32), right.astype(np.float32),
             gt.astype(np.float32))
+
+
+# ---------------------------------------------------------------------------
+# Constant-shift fixtures (reference synthetic.py:33-69): band-limited noise
+# carved so that right[i, j] == left[i, j + shift] exactly.  Same RNG draws
+# as the reference, so seeded pairs are identical.
+# ---------------------------------------------------------------------------
+
+def shifted_pair(height: int, width: int, shift: int,
+                 rng: np.random.Generator | None = None,
+                 cutoff: float = 0.03) -> tuple[np.ndarray, np.ndarray]:
+    """Pair whose true disparity is ``shift`` everywhere outside the occluded
+    left margin.  ``cutoff`` = maximum spatial frequency (cycles/pixel)."""
+    if shift < 0:
+        raise ValueError(f"shift must be >= 0, got {shift}")
+    if not 0.0 < cutoff <= 0.5:
+        raise ValueError(f"cutoff must lie in (0, 0.5], got {cutoff}")
+    rng = np.random.default_rng() if rng is None else rng
+    cw = width + shift
+    noise = rng.standard_normal((height, cw))
+    spec = np.fft.rfft2(noise)
+    r2 = np.fft.fftfreq(height)[:, None] ** 2 + np.fft.rfftfreq(cw)[None, :] ** 2
+    spec[r2 > cutoff * cutoff] = 0.0
+    tex = np.fft.irfft2(spec, s=(height, cw))
+    lo = tex.min()
+    tex = (tex - lo) / max(np.ptp(tex), 1e-12)
+    return np.ascontiguousarray(tex[:, :width]), np.ascontiguousarray(tex[:, shift:])
+
+
+def interior_mask(shape: tuple[int, int], shift: int, block: int,
+                  extra: int = 0) -> np.ndarray:
+    """Pixels whose block and true match lie inside both images."""
+    h, w = shape
+    m = block // 2 + extra
+    out = np.zeros((h, w), dtype=bool)
+    first = max(m + shift, m)
+    if h - m > m and w - m > first:
+        out[m:h - m, first:w - m] = True
+    return out

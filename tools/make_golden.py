@@ -235,8 +235,50 @@ def stage_cases():
     save("stages.npz", **out)
 
 
+def scoring_cases():
+    """baseline.py / evaluation.py / synthetic.py vectors."""
+    out = {}
+    rng = np.random.default_rng(31)
+    left, right = ref.shifted_pair(24, 40, 4, rng, cutoff=0.15)
+    out.update(sp_left=left, sp_right=right,
+               sp_mask=ref.interior_mask(left.shape, 4, 5),
+               sp_mask_x=ref.interior_mask((30, 41), 3, 11, extra=2))
+    d, c, n = ref.baseline_bm(left, right, 8, 5)
+    out.update(bm_d=d, bm_c=c, bm_evals=np.array(n))
+    rng = np.random.default_rng(32)
+    l2 = rng.random((18, 26))
+    r2 = np.roll(l2, -3, axis=1) + 0.01 * rng.random((18, 26))
+    l2[4:10, 6:14] = 0.5                       # flat blocks -> degenerate ZNCC
+    d, c, n = ref.baseline_bm(l2, r2, 6, 3, sign="middlebury")
+    out.update(bm2_left=l2, bm2_right=r2, bm2_d=d, bm2_c=c, bm2_evals=np.array(n))
+    d, c, n = ref.baseline_bm(r2, l2, 6, 7, sign="paper")
+    out.update(bm3_d=d, bm3_c=c, bm3_evals=np.array(n))
+    d, c, n = ref.baseline_bm(l2, r2, 0, 3)
+    out.update(bm4_d=d, bm4_c=c, bm4_evals=np.array(n))
+    # evaluate: random maps with NaN outputs and invalid reference pixels
+    rng = np.random.default_rng(33)
+    ev_d = rng.uniform(0, 40, (37, 53))
+    ev_d[rng.random(ev_d.shape) < 0.07] = np.nan
+    ev_d[0, :5] = np.inf
+    ev_g = ev_d + rng.normal(0, 3, ev_d.shape)
+    ev_inv = rng.random(ev_d.shape) < 0.1
+    ev_g[ev_inv] = np.nan
+    gt = ref.GroundTruthDisparity(values=ev_g, invalid=ev_inv)
+    rows = []
+    for scale in (1.0, 0.5, 2.0):
+        r = ref.evaluate(ev_d, gt, scale=scale)
+        rows.append([scale, r.bad_1, r.bad_2, r.bad_4, r.avg_abs_err, r.evaluated,
+                     r.gt_invalid, r.output_invalid])
+    out.update(ev_d=ev_d, ev_g=ev_g, ev_inv=ev_inv, ev_reports=np.array(rows))
+    save("scoring.npz", **out)
+
+
 def main():
     os.makedirs(OUT, exist_ok=True)
+    if sys.argv[1:] == ["scoring"]:
+        scoring_cases()
+        return
+    scoring_cases()
     stage_cases()
     rng = np.random.default_rng(16)
     left, right = ref.shifted_pair(64, 64, 6, rng, cutoff=0.05)
