@@ -815,7 +815,8 @@ __global__ void prep_staging_kernel(const double* R, int64_t ld, const float* mu
   float2 m = make_float2(0.f, qnan);
   if (x >= 0 && x < w) {
     const float is = isR[(int64_t)y * lds + x];
-    m = make_float2(muR[(int64_t)y * lds + x] - c, is > 0.f ? is : qnan);
+    // 0.5/sigma_R: the sweep computes the half-range cost c/2 + 1/2
+    m = make_float2(muR[(int64_t)y * lds + x] - c, is > 0.f ? 0.5f * is : qnan);
   }
   Mp[(int64_t)y * ldp + xp] = m;
 }

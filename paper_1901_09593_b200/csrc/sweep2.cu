@@ -35,67 +35,166 @@ __device__ __forceinline__ void cp_async8(void* dst, const void* src) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
 
-template <int B, int ZC, int NR>
+// Packed FP32 (FFMA2) helpers: one instruction, two lanes of fp32 FMA.
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+  unsigned long long r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;"
+      : "=l"(r)
+      : "l"(*reinterpret_cast<unsigned long long*>(&a)),
+        "l"(*reinterpret_cast<unsigned long long*>(&b)),
+        "l"(*reinterpret_cast<unsigned long long*>(&c)));
+  return *reinterpret_cast<float2*>(&r);
+}
+__device__ __forceinline__ float fma_sat(float a, float b, float c) {
+  float r;
+  asm("fma.rn.sat.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+__device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
+  unsigned long long r;
+  asm("add.rn.f32x2 %0, %1, %2;"
+      : "=l"(r)
+      : "l"(*reinterpret_cast<unsigned long long*>(&a)),
+        "l"(*reinterpret_cast<unsigned long long*>(&b)));
+  return *reinterpret_cast<float2*>(&r);
+}
+
+// PK: the right strip is staged twice (as-is and shifted by one element) so
+// every pair (v[e], v[e+1]) is one aligned 8-byte shared load, and the cross
+// sums run as FFMA2 over pairs of disparities with the left weight broadcast.
+// Row length of the staged strip.  With PK the two copies must sit 16 banks
+// apart (copy 1 = copy 0 + RR*RW words), so the even lanes (copy 0) and odd
+// lanes (copy 1) of an 8-byte load hit disjoint banks.
+constexpr int strip_row_words(int base, int rr, bool pk) {
+  int rw = (base + 1) & ~1;
+  if (pk)
+    for (int k = 0; k < 32 && (rr * rw) % 32 != 16; ++k) rw += 2;
+  return rw;
+}
+
+template <int B, int ZC, int NR, bool PK = false>
 struct Sweep2Smem {
   static constexpr int NROW = 2 * NR;
-  static constexpr int RW = 30 + B + ZC;
+  static constexpr int RW = strip_row_words(30 + B + ZC, NROW + B - 1, PK);
   static constexpr int RR = NROW + B - 1;
+  static_assert(!PK || (RR * RW) % 32 == 16, "copy offset must be 16 banks");
   static constexpr int SW = 31 + ZC;
   static constexpr int LC = 31 + B;
   using RsT = float[RR][RW];
   using MsT = float2[NROW][SW];
   using HxT = float[ZC][2][NR][32];   // [0] hsA, [1] hsB (horizontal 3-sums)
   using LsT = double[RR][LC];
+  static constexpr int NRS = PK ? 4 : 2;   // strip buffers (x2 copies when PK)
   static constexpr size_t bytes() {
-    return 2 * sizeof(RsT) + 2 * sizeof(MsT) + 2 * sizeof(HxT);
+    return NRS * sizeof(RsT) + 2 * sizeof(MsT) + 2 * sizeof(HxT);
   }
 };
 
 // One chunk of NZ disparities (NZ == ZC, or 4 for the tail) for pixels A, B.
-template <int B, int DIR, int ZC, int NR, int NZ>
+template <int B, int DIR, int ZC, int NR, int NZ, bool PK>
 __device__ __forceinline__ void chunk2(
-    const typename Sweep2Smem<B, ZC, NR>::RsT& Rs, const typename Sweep2Smem<B, ZC, NR>::MsT& Ms,
-    typename Sweep2Smem<B, ZC, NR>::HxT& Hx, const float (&Lt)[B][B], const float (&Lb)[B],
+    const typename Sweep2Smem<B, ZC, NR, PK>::RsT& Rs,
+    const typename Sweep2Smem<B, ZC, NR, PK>::RsT& Rs1,
+    const typename Sweep2Smem<B, ZC, NR, PK>::MsT& Ms,
+    typename Sweep2Smem<B, ZC, NR, PK>::HxT& Hx, const float (&Lt)[B][B], const float (&Lb)[B],
     float kLA, float kLB, float dW, int z0, int zoff, int zend, bool inA, bool inB, int lane,
     int wp, float (&best)[4], int (&bestz)[4], bool wchunk, const int (&wlo)[2],
     const int (&whi)[2]) {
   float SA[NZ], P[NZ];
+  if constexpr (PK) {
+    // g-space accumulators: pair h holds g = 2h (x) and 2h+1 (y); zz is
+    // g (DIR < 0) or NZ-1-g (DIR > 0); v[e] = strip[row][lane + eo0 + e]
+    constexpr int NH = NZ / 2;
+    float2 SA2[NH], P2[NH];
 #pragma unroll
-  for (int zz = 0; zz < NZ; ++zz) SA[zz] = 0.f, P[zz] = 0.f;
-  // window rows r = 0 (A only), 1..B-1 (shared), B (B's bottom)
+    for (int h = 0; h < NH; ++h) SA2[h] = make_float2(0.f, 0.f), P2[h] = SA2[h];
+    const int base = lane + (DIR > 0 ? (ZC - NZ - zoff) : zoff);
+    const bool odd = base & 1;
 #pragma unroll
-  for (int r = 0; r <= B; ++r) {
-    const float* rp = &Rs[2 * wp + r][lane];
+    for (int r = 0; r <= B; ++r) {
+      const float* r0 = &Rs[2 * wp + r][0];
+      const float* r1 = &Rs1[2 * wp + r][0];
+      // pe[k] = (v[2k], v[2k+1]), po[k] = (v[2k+1], v[2k+2]); Rs1[e] = Rs[e+1]
+      const float2* pe = reinterpret_cast<const float2*>(odd ? r1 + base - 1 : r0 + base);
+      const float2* po = reinterpret_cast<const float2*>(odd ? r0 + base + 1 : r1 + base);
 #pragma unroll
-    for (int e = 0; e < NZ + B - 1; ++e) {
-      const int eo = DIR > 0 ? (ZC - NZ - zoff) + e : zoff + e;
-      const float v = rp[eo];
+      for (int k = 0; k < NH + (B - 1) / 2; ++k) {
+        const float2 v = pe[k];
 #pragma unroll
-      for (int c = 0; c < B; ++c) {
-        const int g = e - c;
-        if (g >= 0 && g < NZ) {
-          const int zz = DIR > 0 ? (NZ - 1 - g) : g;
-          if (r == 0) SA[zz] = fmaf(Lt[0][c], v, SA[zz]);
-          else if (r < B) P[zz] = fmaf(Lt[r][c], v, P[zz]);
-          else P[zz] = fmaf(Lb[c], v, P[zz]);
+        for (int c = 0; c < B; c += 2) {
+          const int h = k - c / 2;
+          if (h >= 0 && h < NH) {
+            if (r == 0) SA2[h] = ffma2(make_float2(Lt[0][c], Lt[0][c]), v, SA2[h]);
+            else if (r < B) P2[h] = ffma2(make_float2(Lt[r][c], Lt[r][c]), v, P2[h]);
+            else P2[h] = ffma2(make_float2(Lb[c], Lb[c]), v, P2[h]);
+          }
         }
       }
-    }
-    if (r == B - 1) {
 #pragma unroll
-      for (int zz = 0; zz < NZ; ++zz) SA[zz] += P[zz];   // S_A complete
+      for (int k = 0; k < NH + (B - 3) / 2; ++k) {
+        const float2 v = po[k];
+#pragma unroll
+        for (int c = 1; c < B; c += 2) {
+          const int h = k - (c - 1) / 2;
+          if (h >= 0 && h < NH) {
+            if (r == 0) SA2[h] = ffma2(make_float2(Lt[0][c], Lt[0][c]), v, SA2[h]);
+            else if (r < B) P2[h] = ffma2(make_float2(Lt[r][c], Lt[r][c]), v, P2[h]);
+            else P2[h] = ffma2(make_float2(Lb[c], Lb[c]), v, P2[h]);
+          }
+        }
+      }
+      if (r == B - 1) {
+#pragma unroll
+        for (int h = 0; h < NH; ++h) SA2[h] = fadd2(SA2[h], P2[h]);   // S_A complete
+      }
+    }
+#pragma unroll
+    for (int zz = 0; zz < NZ; ++zz) {
+      const int g = DIR > 0 ? (NZ - 1 - zz) : zz;
+      SA[zz] = (g & 1) ? SA2[g >> 1].y : SA2[g >> 1].x;
+      P[zz] = (g & 1) ? P2[g >> 1].y : P2[g >> 1].x;
+    }
+  } else {
+#pragma unroll
+    for (int zz = 0; zz < NZ; ++zz) SA[zz] = 0.f, P[zz] = 0.f;
+    // window rows r = 0 (A only), 1..B-1 (shared), B (B's bottom)
+#pragma unroll
+    for (int r = 0; r <= B; ++r) {
+      const float* rp = &Rs[2 * wp + r][lane];
+#pragma unroll
+      for (int e = 0; e < NZ + B - 1; ++e) {
+        const int eo = DIR > 0 ? (ZC - NZ - zoff) + e : zoff + e;
+        const float v = rp[eo];
+#pragma unroll
+        for (int c = 0; c < B; ++c) {
+          const int g = e - c;
+          if (g >= 0 && g < NZ) {
+            const int zz = DIR > 0 ? (NZ - 1 - g) : g;
+            if (r == 0) SA[zz] = fmaf(Lt[0][c], v, SA[zz]);
+            else if (r < B) P[zz] = fmaf(Lt[r][c], v, P[zz]);
+            else P[zz] = fmaf(Lb[c], v, P[zz]);
+          }
+        }
+      }
+      if (r == B - 1) {
+#pragma unroll
+        for (int zz = 0; zz < NZ; ++zz) SA[zz] += P[zz];   // S_A complete
+      }
     }
   }
 #pragma unroll
   for (int zz = 0; zz < NZ; ++zz) {
     const int z = z0 + zoff + zz;
     const int g = DIR > 0 ? (ZC - 1 - (zoff + zz)) : (zoff + zz);
-    const float2 ma = Ms[2 * wp][lane + g];       // (muR - c, 1/sigma_R or NaN)
+    const float2 ma = Ms[2 * wp][lane + g];       // (muR - c, 0.5/sigma_R or NaN)
     const float2 mb = Ms[2 * wp + 1][lane + g];
-    float ra = SA[zz] * kLA * ma.y;
-    float rb = fmaf(dW, mb.x, P[zz]) * kLB * mb.y;
-    ra = fminf(fmaxf(ra, -1.f), 1.f);              // fmaxf(NaN, -1) = -1
-    rb = fminf(fmaxf(rb, -1.f), 1.f);
+    // half-range cost c' = sat(c/2 + 1/2) in [0, 1]: the clamp of c to
+    // [-1, 1] is the .sat modifier, and NaN (degenerate or out-of-image
+    // blocks, right centre outside the image) saturates to 0, i.e. c = -1.
+    // Pixels outside the image also come out as 0, the neutral element of
+    // the 3x3 sums.
+    float ra = fma_sat(SA[zz] * kLA, ma.y, 0.5f);
+    float rb = fma_sat(fmaf(dW, mb.x, P[zz]) * kLB, mb.y, 0.5f);
     if (NZ < ZC && z > zend) ra = -3.f, rb = -3.f;  // masked tail slot
     if (ra > best[0]) { best[0] = ra; bestz[0] = z; }
     if (rb > best[1]) { best[1] = rb; bestz[1] = z; }
@@ -103,25 +202,24 @@ __device__ __forceinline__ void chunk2(
       if (z >= wlo[0] && z <= whi[0] && ra > best[2]) { best[2] = ra; bestz[2] = z; }
       if (z >= wlo[1] && z <= whi[1] && rb > best[3]) { best[3] = rb; bestz[3] = z; }
     }
-    const float oa = inA ? ra : 0.f;
-    const float ob = inB ? rb : 0.f;
-    const float ha = (__shfl_up_sync(kFull, oa, 1) + oa) + __shfl_down_sync(kFull, oa, 1);
-    const float hb = (__shfl_up_sync(kFull, ob, 1) + ob) + __shfl_down_sync(kFull, ob, 1);
+    // (masked tail slots carry -3 into sums the nb pass never reads)
+    const float ha = (__shfl_up_sync(kFull, ra, 1) + ra) + __shfl_down_sync(kFull, ra, 1);
+    const float hb = (__shfl_up_sync(kFull, rb, 1) + rb) + __shfl_down_sync(kFull, rb, 1);
     Hx[zoff + zz][0][wp][lane] = ha;
     Hx[zoff + zz][1][wp][lane] = hb;
   }
 }
 
-template <int B, int DIR, int ZC, int NR, int MINB>
+template <int B, int DIR, int ZC, int NR, int MINB, bool PK>
 __global__ void __launch_bounds__(NR * 32, MINB)
 sweep2_kernel(const SweepArgs a) {
-  using SM = Sweep2Smem<B, ZC, NR>;
+  using SM = Sweep2Smem<B, ZC, NR, PK>;
   constexpr int H2 = B / 2;
   constexpr int NT = NR * 32;
   constexpr int NROW = SM::NROW, RW = SM::RW, RR = SM::RR, SW = SM::SW, LC = SM::LC;
   extern __shared__ float4 smem4[];
   typename SM::RsT* Rs = reinterpret_cast<typename SM::RsT*>(smem4);
-  typename SM::MsT* Ms = reinterpret_cast<typename SM::MsT*>(Rs + 2);
+  typename SM::MsT* Ms = reinterpret_cast<typename SM::MsT*>(Rs + SM::NRS);
   typename SM::HxT* Hx = reinterpret_cast<typename SM::HxT*>(Ms + 2);
 
   const int lane = threadIdx.x & 31;
@@ -148,7 +246,14 @@ sweep2_kernel(const SweepArgs a) {
     const int s0 = DIR > 0 ? (x0 - 1 - H2 - z0 - (ZC - 1)) : (x0 - 1 - H2 + z0);
     for (int rr = wp; rr < RR; rr += NR) {
       const float* src = Rp + (int64_t)clampi(y0 - 1 - H2 + rr, 0, H - 1) * a.ldp + s0;
-      for (int e = lane; e < RW; e += 32) cp_async4(&Rs[buf][rr][e], src + e);
+      if constexpr (PK) {
+        for (int e = lane; e < RW; e += 32) {
+          cp_async4(&Rs[2 * buf][rr][e], src + e);
+          cp_async4(&Rs[2 * buf + 1][rr][e], src + e + 1);
+        }
+      } else {
+        for (int e = lane; e < RW; e += 32) cp_async4(&Rs[buf][rr][e], src + e);
+      }
     }
     const int q0 = DIR > 0 ? (x0 - 1 - z0 - (ZC - 1)) : (x0 - 1 + z0);
     for (int rr = wp; rr < NROW; rr += NR) {
@@ -245,13 +350,13 @@ sweep2_kernel(const SweepArgs a) {
                                              (trusted[1] && wlo[1] <= z0 + ZC - 1 && whi[1] >= z0));
     int nz;
     if (z0 + ZC - 1 <= zmax) {
-      chunk2<B, DIR, ZC, NR, ZC>(Rs[cur], Ms[cur], Hx[cur], Lt, Lb, kLA, kLB, dW, z0, 0, zmax,
+      chunk2<B, DIR, ZC, NR, ZC, PK>(Rs[PK ? 2 * cur : cur], Rs[PK ? 2 * cur + 1 : cur], Ms[cur], Hx[cur], Lt, Lb, kLA, kLB, dW, z0, 0, zmax,
                                  inA, inB, lane, wp, best, bestz, wchunk, wlo, whi);
       nz = ZC;
     } else {
       nz = zmax - z0 + 1;
       for (int zo = 0; zo < nz; zo += 4)
-        chunk2<B, DIR, ZC, NR, 4>(Rs[cur], Ms[cur], Hx[cur], Lt, Lb, kLA, kLB, dW, z0, zo, zmax,
+        chunk2<B, DIR, ZC, NR, 4, PK>(Rs[PK ? 2 * cur : cur], Rs[PK ? 2 * cur + 1 : cur], Ms[cur], Hx[cur], Lt, Lb, kLA, kLB, dW, z0, zo, zmax,
                                   inA, inB, lane, wp, best, bestz, wchunk, wlo, whi);
     }
     cp_async_wait_all();
@@ -280,28 +385,31 @@ sweep2_kernel(const SweepArgs a) {
 #pragma unroll
   for (int p = 0; p < 2; ++p) {
     const int i = ii[p];
-    float bw = best[2 + p];
-    if (trusted[p] && bw == -2.f) bw = -1.f;   // window beyond zmax: all -1
     const int members = ((i > 0) + 1 + (i < H - 1)) * ((j > 0) + 1 + (j < W - 1));
+    // back from half-range c' to c = 2c' - 1 (exact for c' >= 1/4)
+    float bw = best[2 + p];
+    bw = (trusted[p] && bw == -2.f) ? -1.f : 2.f * bw - 1.f;   // window beyond zmax: all -1
+    const float bf = 2.f * best[p] - 1.f;
+    const float nbc = 2.f * nbv[p] / (float)members - 1.f;
     bool low = false;
     if (a.mode == kSweepPipeline) {
       if (inner[p]) {
-        const float cs = trusted[p] ? bw : best[p];
+        const float cs = trusted[p] ? bw : bf;
         const int zs = trusted[p] ? bestz[2 + p] : bestz[p];
         low = (double)cs <= a.alpha;
         const int64_t o = (int64_t)i * a.ldo + j;
         a.dout[o] = (int16_t)(low ? nbz[p] : zs);
-        a.cout[o] = low ? nbv[p] / (float)members : cs;
+        a.cout[o] = low ? nbc : cs;
         a.low[o] = (uint8_t)low;
       }
       nlow += (low && i >= a.rows.cnt_lo && i < a.rows.cnt_hi) ? 1u : 0u;
     } else if (inner[p]) {
       const int64_t o = (int64_t)i * W + j;
       a.fz[o] = (int16_t)bestz[p];
-      a.fc[o] = best[p];
+      a.fc[o] = bf;
       if (a.wz) { a.wz[o] = (int16_t)bestz[2 + p]; a.wcst[o] = trusted[p] ? bw : -2.f; }
       a.nz[o] = (int16_t)nbz[p];
-      a.nc[o] = nbv[p] / (float)members;
+      a.nc[o] = nbc;
     }
   }
   if (a.mode == kSweepPipeline) {
@@ -312,12 +420,12 @@ sweep2_kernel(const SweepArgs a) {
   }
 }
 
-template <int B, int DIR, int ZC, int NR, int MINB>
+template <int B, int DIR, int ZC, int NR, int MINB, bool PK = false>
 cudaError_t launch2(const SweepArgs& a, cudaStream_t s) {
-  constexpr size_t smem = Sweep2Smem<B, ZC, NR>::bytes();
+  constexpr size_t smem = Sweep2Smem<B, ZC, NR, PK>::bytes();
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(sweep2_kernel<B, DIR, ZC, NR, MINB>,
+    cudaError_t e = cudaFuncSetAttribute(sweep2_kernel<B, DIR, ZC, NR, MINB, PK>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     configured = true;
@@ -328,7 +436,7 @@ cudaError_t launch2(const SweepArgs& a, cudaStream_t s) {
   SweepArgs b = a;
   b.rows.lo = (a.rows.lo / (NROW - 2)) * (NROW - 2);
   dim3 grid((a.W + 29) / 30, (b.rows.hi - b.rows.lo + NROW - 3) / (NROW - 2));
-  sweep2_kernel<B, DIR, ZC, NR, MINB><<<grid, NR * 32, smem, s>>>(b);
+  sweep2_kernel<B, DIR, ZC, NR, MINB, PK><<<grid, NR * 32, smem, s>>>(b);
   return cudaGetLastError();
 }
 
@@ -345,23 +453,13 @@ template <int DIR>
 cudaError_t launch2_dir(const SweepArgs& a, cudaStream_t s) {
   if (DIR > 0) {
     switch (v2() * 100 + a.block) {
-      case 107: return launch2<7, DIR, 12, 16, 1>(a, s);
-      case 207: return launch2<7, DIR, 16, 8, 1>(a, s);
-      case 109: return launch2<9, DIR, 8, 8, 2>(a, s);
-      case 209: return launch2<9, DIR, 12, 8, 1>(a, s);
-      case 105: return launch2<5, DIR, 24, 8, 2>(a, s);
-      case 103: return launch2<3, DIR, 24, 8, 2>(a, s);
-      case 307: return launch2<7, DIR, 12, 8, 2>(a, s);
-      case 407: return launch2<7, DIR, 16, 16, 1>(a, s);
-      case 305: return launch2<5, DIR, 16, 8, 2>(a, s);
-      case 303: return launch2<3, DIR, 16, 16, 1>(a, s);
-      case 507: return launch2<7, DIR, 8, 16, 1>(a, s);
-      case 405: return launch2<5, DIR, 12, 8, 2>(a, s);
-      case 505: return launch2<5, DIR, 16, 8, 1>(a, s);
-      case 403: return launch2<3, DIR, 12, 8, 2>(a, s);
-      case 503: return launch2<3, DIR, 16, 8, 1>(a, s);
-      case 409: return launch2<9, DIR, 12, 8, 1>(a, s);
-      case 509: return launch2<9, DIR, 16, 4, 1>(a, s);
+      case 103: return launch2<3, DIR, 16, 8, 2, true>(a, s);
+      case 105: return launch2<5, DIR, 16, 16, 1, true>(a, s);
+      case 107: return launch2<7, DIR, 16, 8, 2, true>(a, s);
+      case 109: return launch2<9, DIR, 16, 8, 1, true>(a, s);
+      case 111: return launch2<11, DIR, 16, 8, 1, true>(a, s);
+      case 207: return launch2<7, DIR, 12, 8, 2, true>(a, s);
+      case 307: return launch2<7, DIR, 16, 16, 1, true>(a, s);
       default: break;
     }
   }
