@@ -72,26 +72,26 @@ constexpr int strip_row_words(int base, int rr, bool pk) {
   return rw;
 }
 
-template <int B, int ZC, int NR, bool PK = false>
+template <int B, int ZC, int NR, int PK = 0>
 struct Sweep2Smem {
   static constexpr int NROW = 2 * NR;
-  static constexpr int RW = strip_row_words(30 + B + ZC, NROW + B - 1, PK);
+  static constexpr int RW = strip_row_words(30 + B + ZC, NROW + B - 1, PK == 1);
   static constexpr int RR = NROW + B - 1;
-  static_assert(!PK || (RR * RW) % 32 == 16, "copy offset must be 16 banks");
+  static_assert(PK != 1 || (RR * RW) % 32 == 16, "copy offset must be 16 banks");
   static constexpr int SW = 31 + ZC;
   static constexpr int LC = 31 + B;
   using RsT = float[RR][RW];
   using MsT = float2[NROW][SW];
   using HxT = float[ZC][2][NR][32];   // [0] hsA, [1] hsB (horizontal 3-sums)
   using LsT = double[RR][LC];
-  static constexpr int NRS = PK ? 4 : 2;   // strip buffers (x2 copies when PK)
+  static constexpr int NRS = PK == 1 ? 4 : 2;   // strip buffers (x2 copies when PK == 1)
   static constexpr size_t bytes() {
     return NRS * sizeof(RsT) + 2 * sizeof(MsT) + 2 * sizeof(HxT);
   }
 };
 
 // One chunk of NZ disparities (NZ == ZC, or 4 for the tail) for pixels A, B.
-template <int B, int DIR, int ZC, int NR, int NZ, bool PK>
+template <int B, int DIR, int ZC, int NR, int NZ, int PK>
 __device__ __forceinline__ void chunk2(
     const typename Sweep2Smem<B, ZC, NR, PK>::RsT& Rs,
     const typename Sweep2Smem<B, ZC, NR, PK>::RsT& Rs1,
@@ -101,7 +101,7 @@ __device__ __forceinline__ void chunk2(
     int wp, float (&best)[4], int (&bestz)[4], bool wchunk, const int (&wlo)[2],
     const int (&whi)[2]) {
   float SA[NZ], P[NZ];
-  if constexpr (PK) {
+  if constexpr (PK == 1) {
     // g-space accumulators: pair h holds g = 2h (x) and 2h+1 (y); zz is
     // g (DIR < 0) or NZ-1-g (DIR > 0); v[e] = strip[row][lane + eo0 + e]
     constexpr int NH = NZ / 2;
@@ -146,6 +146,43 @@ __device__ __forceinline__ void chunk2(
       if (r == B - 1) {
 #pragma unroll
         for (int h = 0; h < NH; ++h) SA2[h] = fadd2(SA2[h], P2[h]);   // S_A complete
+      }
+    }
+#pragma unroll
+    for (int zz = 0; zz < NZ; ++zz) {
+      const int g = DIR > 0 ? (NZ - 1 - zz) : zz;
+      SA[zz] = (g & 1) ? SA2[g >> 1].y : SA2[g >> 1].x;
+      P[zz] = (g & 1) ? P2[g >> 1].y : P2[g >> 1].x;
+    }
+  } else if constexpr (PK == 2) {
+    // FFMA2 over disparity pairs from one staged copy: scalar loads, the
+    // odd-offset pairs are assembled in registers
+    constexpr int NH = NZ / 2;
+    constexpr int NE = NZ + B - 1;
+    float2 SA2[NH], P2[NH];
+#pragma unroll
+    for (int h = 0; h < NH; ++h) SA2[h] = make_float2(0.f, 0.f), P2[h] = SA2[h];
+    const int eo0 = DIR > 0 ? (ZC - NZ - zoff) : zoff;
+#pragma unroll
+    for (int r = 0; r <= B; ++r) {
+      const float* rp = &Rs[2 * wp + r][lane + eo0];
+      float v[NE + 1];
+#pragma unroll
+      for (int e = 0; e < NE; ++e) v[e] = rp[e];
+      v[NE] = 0.f;
+#pragma unroll
+      for (int c = 0; c < B; ++c) {
+        const float w = r == 0 ? Lt[0][c] : (r < B ? Lt[r][c] : Lb[c]);
+#pragma unroll
+        for (int h = 0; h < NH; ++h) {
+          const float2 vv = make_float2(v[2 * h + c], v[2 * h + c + 1]);
+          if (r == 0) SA2[h] = ffma2(make_float2(w, w), vv, SA2[h]);
+          else P2[h] = ffma2(make_float2(w, w), vv, P2[h]);
+        }
+      }
+      if (r == B - 1) {
+#pragma unroll
+        for (int h = 0; h < NH; ++h) SA2[h] = fadd2(SA2[h], P2[h]);
       }
     }
 #pragma unroll
@@ -210,7 +247,7 @@ __device__ __forceinline__ void chunk2(
   }
 }
 
-template <int B, int DIR, int ZC, int NR, int MINB, bool PK>
+template <int B, int DIR, int ZC, int NR, int MINB, int PK>
 __global__ void __launch_bounds__(NR * 32, MINB)
 sweep2_kernel(const SweepArgs a) {
   using SM = Sweep2Smem<B, ZC, NR, PK>;
@@ -246,7 +283,7 @@ sweep2_kernel(const SweepArgs a) {
     const int s0 = DIR > 0 ? (x0 - 1 - H2 - z0 - (ZC - 1)) : (x0 - 1 - H2 + z0);
     for (int rr = wp; rr < RR; rr += NR) {
       const float* src = Rp + (int64_t)clampi(y0 - 1 - H2 + rr, 0, H - 1) * a.ldp + s0;
-      if constexpr (PK) {
+      if constexpr (PK == 1) {
         for (int e = lane; e < RW; e += 32) {
           cp_async4(&Rs[2 * buf][rr][e], src + e);
           cp_async4(&Rs[2 * buf + 1][rr][e], src + e + 1);
@@ -350,31 +387,28 @@ sweep2_kernel(const SweepArgs a) {
                                              (trusted[1] && wlo[1] <= z0 + ZC - 1 && whi[1] >= z0));
     int nz;
     if (z0 + ZC - 1 <= zmax) {
-      chunk2<B, DIR, ZC, NR, ZC, PK>(Rs[PK ? 2 * cur : cur], Rs[PK ? 2 * cur + 1 : cur], Ms[cur], Hx[cur], Lt, Lb, kLA, kLB, dW, z0, 0, zmax,
+      chunk2<B, DIR, ZC, NR, ZC, PK>(Rs[PK == 1 ? 2 * cur : cur], Rs[PK == 1 ? 2 * cur + 1 : cur], Ms[cur], Hx[cur], Lt, Lb, kLA, kLB, dW, z0, 0, zmax,
                                  inA, inB, lane, wp, best, bestz, wchunk, wlo, whi);
       nz = ZC;
     } else {
       nz = zmax - z0 + 1;
       for (int zo = 0; zo < nz; zo += 4)
-        chunk2<B, DIR, ZC, NR, 4, PK>(Rs[PK ? 2 * cur : cur], Rs[PK ? 2 * cur + 1 : cur], Ms[cur], Hx[cur], Lt, Lb, kLA, kLB, dW, z0, zo, zmax,
+        chunk2<B, DIR, ZC, NR, 4, PK>(Rs[PK == 1 ? 2 * cur : cur], Rs[PK == 1 ? 2 * cur + 1 : cur], Ms[cur], Hx[cur], Lt, Lb, kLA, kLB, dW, z0, zo, zmax,
                                   inA, inB, lane, wp, best, bestz, wchunk, wlo, whi);
     }
     cp_async_wait_all();
     __syncthreads();
+    // vertical 3-sums: A = B(above) + (A + B), B = (A + B) + A(below); the
+    // edge warps' out-of-tile reads are clamped and never used (innerA/B)
     const typename SM::HxT& hx = Hx[cur];
-    if (innerA) {
+    const int wu = wp > 0 ? wp - 1 : 0, wd = wp < NR - 1 ? wp + 1 : NR - 1;
 #pragma unroll
-      for (int zz = 0; zz < ZC; ++zz) {
-        const float nb = (hx[zz][1][wp - 1][lane] + hx[zz][0][wp][lane]) + hx[zz][1][wp][lane];
-        if (zz < nz && nb > nbv[0]) { nbv[0] = nb; nbz[0] = z0 + zz; }
-      }
-    }
-    if (innerB) {
-#pragma unroll
-      for (int zz = 0; zz < ZC; ++zz) {
-        const float nb = (hx[zz][0][wp][lane] + hx[zz][1][wp][lane]) + hx[zz][0][wp + 1][lane];
-        if (zz < nz && nb > nbv[1]) { nbv[1] = nb; nbz[1] = z0 + zz; }
-      }
+    for (int zz = 0; zz < ZC; ++zz) {
+      const float t = hx[zz][0][wp][lane] + hx[zz][1][wp][lane];
+      const float nba = hx[zz][1][wu][lane] + t;
+      const float nbb = t + hx[zz][0][wd][lane];
+      if (innerA && zz < nz && nba > nbv[0]) { nbv[0] = nba; nbz[0] = z0 + zz; }
+      if (innerB && zz < nz && nbb > nbv[1]) { nbv[1] = nbb; nbz[1] = z0 + zz; }
     }
   }
 
@@ -420,7 +454,7 @@ sweep2_kernel(const SweepArgs a) {
   }
 }
 
-template <int B, int DIR, int ZC, int NR, int MINB, bool PK = false>
+template <int B, int DIR, int ZC, int NR, int MINB, int PK = 0>
 cudaError_t launch2(const SweepArgs& a, cudaStream_t s) {
   constexpr size_t smem = Sweep2Smem<B, ZC, NR, PK>::bytes();
   static bool configured = false;
@@ -453,13 +487,28 @@ template <int DIR>
 cudaError_t launch2_dir(const SweepArgs& a, cudaStream_t s) {
   if (DIR > 0) {
     switch (v2() * 100 + a.block) {
-      case 103: return launch2<3, DIR, 16, 8, 2, true>(a, s);
-      case 105: return launch2<5, DIR, 16, 16, 1, true>(a, s);
-      case 107: return launch2<7, DIR, 16, 8, 2, true>(a, s);
-      case 109: return launch2<9, DIR, 16, 8, 1, true>(a, s);
-      case 111: return launch2<11, DIR, 16, 8, 1, true>(a, s);
-      case 207: return launch2<7, DIR, 12, 8, 2, true>(a, s);
-      case 307: return launch2<7, DIR, 16, 16, 1, true>(a, s);
+      case 103: return launch2<3, DIR, 16, 8, 2, 1>(a, s);
+      case 105: return launch2<5, DIR, 16, 16, 1, 1>(a, s);
+      case 107: return launch2<7, DIR, 16, 8, 2, 1>(a, s);
+      case 109: return launch2<9, DIR, 16, 8, 1, 1>(a, s);
+      case 111: return launch2<11, DIR, 16, 8, 1, 1>(a, s);
+      case 207: return launch2<7, DIR, 12, 8, 2, 1>(a, s);
+      case 307: return launch2<7, DIR, 16, 16, 1, 1>(a, s);
+      case 807: return launch2<7, DIR, 16, 8, 2, 2>(a, s);
+      case 907: return launch2<7, DIR, 16, 16, 1, 2>(a, s);
+      case 805: return launch2<5, DIR, 16, 16, 1, 2>(a, s);
+      case 809: return launch2<9, DIR, 16, 8, 1, 2>(a, s);
+      case 803: return launch2<3, DIR, 16, 8, 2, 2>(a, s);
+      case 407: return launch2<7, DIR, 12, 8, 2>(a, s);
+      case 507: return launch2<7, DIR, 16, 16, 1>(a, s);
+      case 607: return launch2<7, DIR, 8, 16, 2>(a, s);
+      case 707: return launch2<7, DIR, 12, 16, 1>(a, s);
+      case 409: return launch2<9, DIR, 12, 8, 1>(a, s);
+      case 509: return launch2<9, DIR, 8, 8, 2>(a, s);
+      case 405: return launch2<5, DIR, 16, 8, 2>(a, s);
+      case 505: return launch2<5, DIR, 12, 16, 1>(a, s);
+      case 403: return launch2<3, DIR, 16, 16, 1>(a, s);
+      case 503: return launch2<3, DIR, 24, 8, 2>(a, s);
       default: break;
     }
   }
