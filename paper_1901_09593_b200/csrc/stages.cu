@@ -101,279 +101,101 @@ __global__ void stats_kernel(const double* img, int h, int w, int64_t ld,
 // z = sqrt(3) - 2, gain (1-z)(1-1/z), 'reflect' causal/anticausal init.
 constexpr int kNpad = 12;
 
-__global__ void bspline_pad_kernel(const float* c32, const double* c64, int ch,
-                                   int cw, int64_t ldcin, double* coef,
-                                   int64_t ldc) {
-  const int x = blockIdx.x * blockDim.x + threadIdx.x;
-  const int y = blockIdx.y * blockDim.y + threadIdx.y;
-  const int nh = ch + 2 * kNpad, nw = cw + 2 * kNpad;
-  if (x >= nw || y >= nh) return;
-  const int64_t o = (int64_t)clampi(y - kNpad, 0, ch - 1) * ldcin + clampi(x - kNpad, 0, cw - 1);
-  coef[(int64_t)y * ldc + x] = c32 ? (double)c32[o] : c64[o];
-}
-
-// The IIR prefilter runs as parallel segments: each thread filters kSeg
-// samples of one line from a register window that also holds kWarm samples
-// of warm-up (|z|^32 ~ 5e-19, below fp64 resolution), so the result equals
-// scipy's sequential recursion to rounding.  All loads of the window are
-// independent and issued up front.  Segments touching a line end use
-// scipy's exact 'reflect' initialisation; lines of <= kWin samples run the
-// exact sequential recursion.
 constexpr double kPole = -0.26794919243112270;   // sqrt(3) - 2
-constexpr int kWarm = 32;
-constexpr int kSeg = 32;
-constexpr int kWin = kWarm + kSeg;
 
-__device__ __forceinline__ double line_at(const double* p, int64_t stride, int i) {
-  return p[(int64_t)i * stride];
+// The prefilter as a parallel FIR.  scipy's recursion (gain (1-z)(1-1/z),
+// causal + anticausal pass, exact 'reflect' initialisation at both line
+// ends) equals, on each axis, the symmetric filter h[m] = sqrt(3) z^|m|
+// applied to the half-sample-symmetric periodic extension of the padded
+// line (checked against the recursion to 1e-15 in tests).  |z|^29 < 3e-17,
+// so taps |m| <= 28 reproduce it to fp64 rounding.  Every output is an
+// independent 57-tap dot product: no sequential recursion, and a row band's
+// coefficients depend only on the +-28 padded rows around them.
+constexpr int kFirR = 28;
+constexpr int kFT = 32;                    // output tile (padded coords)
+constexpr int kFE = kFT + 2 * kFirR;       // 88: staged region per axis
+
+__device__ __forceinline__ double fir_tap(int m) {
+  // sqrt(3) * z^m, m in [0, 28], by repeated multiplication at compile time
+  double t = 1.7320508075688772;
+#pragma unroll
+  for (int k = 0; k < 28; ++k)
+    if (k < m) t *= kPole;
+  return t;
 }
 
-// exact scipy recursion (gain, reflect init, causal, anticausal) of a line
-__device__ void spline_line_exact(const double* x, double* y, int n, int64_t stride, double g,
-                                  bool causal) {
-  const double z = kPole;
-  if (causal) {
-    const double zn = pow(z, (double)n);
-    const double c0 = g * x[0];
-    double acc = c0 + zn * g * line_at(x, stride, n - 1);
-    double zi = z;
-    for (int i = 1; i < n; ++i) {
-      acc += zi * (g * line_at(x, stride, i) + zn * g * line_at(x, stride, n - 1 - i));
-      zi *= z;
-    }
-    double prev = acc * (z / (1.0 - zn * zn)) + c0;
-    y[0] = prev;
-    for (int i = 1; i < n; ++i) {
-      prev = g * line_at(x, stride, i) + z * prev;
-      y[(int64_t)i * stride] = prev;
-    }
-  } else {
-    double prev = line_at(x, stride, n - 1) * (z / (z - 1.0));
-    y[(int64_t)(n - 1) * stride] = prev;
-    for (int i = n - 2; i >= 0; --i) {
-      prev = z * (prev - line_at(x, stride, i));
-      y[(int64_t)i * stride] = prev;
-    }
-  }
+// half-sample-symmetric periodic extension of an index into [0, n)
+__device__ __forceinline__ int reflect_index(int p, int n) {
+  if (p >= 0 && p < n) return p;                 // interior: no division
+  if (p < 0 && p >= -n) return -1 - p;
+  if (p >= n && p < 2 * n) return 2 * n - 1 - p;
+  const int per = 2 * n;
+  int q = p % per;
+  if (q < 0) q += per;
+  return q < n ? q : per - 1 - q;
 }
 
-// causal pass: out[i] = g*in[i] + z*out[i-1]
-__global__ void __launch_bounds__(128) iir_causal_kernel(const double* __restrict__ in,
-                                                         double* __restrict__ out, int64_t ldc,
-                                                         int nh, int nw, int axis, double g) {
-  const int line = blockIdx.x * blockDim.x + threadIdx.x;
-  const int n = axis == 0 ? nh : nw;
-  const int nl = axis == 0 ? nw : nh;
-  if (line >= nl) return;
-  const int64_t stride = axis == 0 ? ldc : 1;
-  const int64_t base = axis == 0 ? line : (int64_t)line * ldc;
-  const double* x = in + base;
-  double* y = out + base;
-  if (n <= kWin) {
-    if (blockIdx.y == 0) spline_line_exact(x, y, n, stride, g, true);
-    return;
-  }
-  const int s = blockIdx.y * kSeg;
-  if (s >= n) return;
-  const int e = min(n, s + kSeg);
-  const int w0 = s - kWarm;              // window [w0, w0 + kWin), left-aligned
-  double v[kWin];
-#pragma unroll
-  for (int k = 0; k < kWin; ++k) {
-    const int idx = w0 + k;
-    v[k] = (idx >= 0 && idx < n) ? g * line_at(x, stride, idx) : 0.0;
-  }
-  const double z = kPole;
-  double acc;
-  if (w0 < 0) {
-    // s == 0: exact reflect init; n > kWin so z^n terms vanish (< 1e-36)
-    double sum = 0.0, zi = z;
-#pragma unroll
-    for (int k = kWarm + 1; k < kWin; ++k) {
-      sum += zi * v[k];
-      zi *= z;
-    }
-    acc = (v[kWarm] + sum) * z + v[kWarm];
-    y[0] = acc;
-  } else {
-    acc = v[0];
-  }
-#pragma unroll
-  for (int k = 1; k < kWin; ++k) {
-    const int idx = w0 + k;
-    if (w0 < 0 && k <= kWarm) continue;   // before the line start / the init sample
-    acc = v[k] + z * acc;
-    if (idx >= s && idx < e) y[(int64_t)idx * stride] = acc;
-  }
-}
-
-// anticausal pass: out[n-1] = in[n-1]*z/(z-1); out[i] = z*(out[i+1] - in[i])
-__global__ void __launch_bounds__(128) iir_anticausal_kernel(const double* __restrict__ in,
-                                                             double* __restrict__ out,
-                                                             int64_t ldc, int nh, int nw,
-                                                             int axis) {
-  const int line = blockIdx.x * blockDim.x + threadIdx.x;
-  const int n = axis == 0 ? nh : nw;
-  const int nl = axis == 0 ? nw : nh;
-  if (line >= nl) return;
-  const int64_t stride = axis == 0 ? ldc : 1;
-  const int64_t base = axis == 0 ? line : (int64_t)line * ldc;
-  const double* x = in + base;
-  double* y = out + base;
-  if (n <= kWin) {
-    if (blockIdx.y == 0) spline_line_exact(x, y, n, stride, 1.0, false);
-    return;
-  }
-  const int s = blockIdx.y * kSeg;
-  if (s >= n) return;
-  const int e = min(n, s + kSeg);
-  const int we = min(n, e + kWarm);      // window [we - kWin, we), right-aligned
-  const int w0 = we - kWin;
-  double v[kWin];
-#pragma unroll
-  for (int k = 0; k < kWin; ++k) {
-    const int idx = w0 + k;
-    v[k] = idx >= 0 ? line_at(x, stride, idx) : 0.0;
-  }
-  const double z = kPole;
-  double acc = we == n ? v[kWin - 1] * (z / (z - 1.0)) : -z * v[kWin - 1];
-  if (we - 1 < e) y[(int64_t)(we - 1) * stride] = acc;
-#pragma unroll
-  for (int k = kWin - 2; k >= 0; --k) {
-    const int idx = w0 + k;
-    acc = z * (acc - v[k]);
-    if (idx >= s && idx < e) y[(int64_t)idx * stride] = acc;
-  }
-}
-
-// Fused prefilter: one block per 32x32 tile of the padded coefficient array.
-// The block stages the (32+64)^2 padded input region (edge-replicated coarse
-// costs, i.e. scipy's 12-sample prepad) in shared memory, filters axis 0
-// (causal then anticausal per column) and axis 1 (per row) in place, and
-// writes the inner 32x32.  Lines are exact where the tile reaches a line end
-// (scipy init) and warmed up over 32 samples elsewhere (|z|^32 ~ 5e-19).
-constexpr int kTile = 32, kWU = 32, kExt = kTile + 2 * kWU;   // 96
-
-__device__ __forceinline__ void iir_line_smem(double* x, int stride, int lo, int hi, bool exact_lo,
-                                              bool exact_hi, int n_full, double g) {
-  // x[lo .. hi) is the part of the line inside the tile (tile-local indices);
-  // exact_lo: x[lo] is element 0 of the line; exact_hi: x[hi-1] is element n-1.
-  // The gain is applied on load; recursions run on register chunks of 8 so
-  // the shared-memory loads of a chunk are independent of the recursion.
-  constexpr int U = 8;
-  const double z = kPole;
-  const int n = hi - lo;
-  if (n <= 0) return;
-  double acc;
-  if (exact_lo) {
-    if (exact_hi && n_full == n) {
-      // whole line present: scipy's full reflect init
-      const double zn = pow(z, (double)n);
-      const double c0 = g * x[lo * stride];
-      double s = c0 + zn * (g * x[(hi - 1) * stride]);
-      double zi = z;
-      for (int i = 1; i < n; ++i) {
-        s += zi * (g * x[(lo + i) * stride] + zn * (g * x[(hi - 1 - i) * stride]));
-        zi *= z;
-      }
-      acc = s * (z / (1.0 - zn * zn)) + c0;
-    } else {
-      // line longer than the warm-up: z^n terms vanish (n > 64)
-      double s = 0.0, zi = z;
-      const int m = min(n, kWU);
-      for (int i = 1; i < m; ++i) {
-        s += zi * (g * x[(lo + i) * stride]);
-        zi *= z;
-      }
-      const double c0 = g * x[lo * stride];
-      acc = (c0 + s) * z + c0;
-    }
-  } else {
-    acc = g * x[lo * stride];
-  }
-  x[lo * stride] = acc;
-  int k = lo + 1;
-  for (; k + U <= hi; k += U) {
-    double v[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) v[u] = g * x[(k + u) * stride];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      acc = v[u] + z * acc;
-      x[(k + u) * stride] = acc;
-    }
-  }
-  for (; k < hi; ++k) {
-    acc = g * x[k * stride] + z * acc;
-    x[k * stride] = acc;
-  }
-  acc = exact_hi ? x[(hi - 1) * stride] * (z / (z - 1.0)) : -z * x[(hi - 1) * stride];
-  x[(hi - 1) * stride] = acc;
-  k = hi - 2;
-  for (; k - U + 1 >= lo; k -= U) {
-    double v[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) v[u] = x[(k - u) * stride];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      acc = z * (acc - v[u]);
-      x[(k - u) * stride] = acc;
-    }
-  }
-  for (; k >= lo; --k) {
-    acc = z * (acc - x[k * stride]);
-    x[k * stride] = acc;
-  }
-}
-
-__global__ void __launch_bounds__(128) bspline_tile_kernel(const float* c32, const double* c64,
-                                                           int ch, int cw, int64_t ldcin,
-                                                           double* coef, int64_t ldc) {
-  extern __shared__ double S[];   // [kExt][kExt + 1]
-  constexpr int SP = kExt + 1;
+template <typename T>
+__global__ void __launch_bounds__(256) bspline_fir_kernel(const T* cin, int ch, int cw,
+                                                          int64_t ldcin, double* coef,
+                                                          int64_t ldc) {
+  extern __shared__ double smem_d[];
+  T (*S)[kFE + 1] = reinterpret_cast<T (*)[kFE + 1]>(smem_d);        // [kFE][kFE+1] input
+  double (*Tm)[kFE + 1] = reinterpret_cast<double (*)[kFE + 1]>(
+      smem_d + (sizeof(T) * kFE * (kFE + 1) + 7) / 8);                 // [kFT][kFE+1] axis-0 pass
   const int nh = ch + 2 * kNpad, nw = cw + 2 * kNpad;
-  const int y0 = blockIdx.y * kTile, x0 = blockIdx.x * kTile;
-  const int gy0 = y0 - kWU, gx0 = x0 - kWU;
-  // rows of the tile are loaded by warps, 3 coalesced columns per lane
-  // (kExt = 96), all loads of a row in flight together
+  const int y0 = blockIdx.y * kFT, x0 = blockIdx.x * kFT;
+  const int lane = threadIdx.x & 31, ty = threadIdx.x >> 5;   // 8 warps
+  // stage the doubly extended padded input: P[y][x] = cost[clamp(y-12)][clamp(x-12)].
+  // All of a thread's loads are issued before any store, so their latency
+  // overlaps (a load->store loop would serialise ~31 memory round trips).
   {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
-    for (int r = warp; r < kExt; r += nwarp) {
-      const int gy = gy0 + r;
-      const bool rowin = gy >= 0 && gy < nh;
-      const int64_t ro = (int64_t)clampi(gy - kNpad, 0, ch - 1) * ldcin;
-      double v[3];
+    constexpr int kPer = (kFE * kFE + 255) / 256;   // 31
+    T v[kPer];
 #pragma unroll
-      for (int u = 0; u < 3; ++u) {
-        const int gx = gx0 + lane + 32 * u;
-        const int64_t o = ro + clampi(gx - kNpad, 0, cw - 1);
-        v[u] = (rowin && gx >= 0 && gx < nw) ? (c32 ? (double)c32[o] : c64[o]) : 0.0;
-      }
+    for (int k = 0; k < kPer; ++k) {
+      const int t = threadIdx.x + 256 * k;
+      const int r = t / kFE, c = t - r * kFE;
+      const int py = reflect_index(y0 - kFirR + r, nh);
+      const int px = reflect_index(x0 - kFirR + c, nw);
+      v[k] = t < kFE * kFE ? cin[(int64_t)clampi(py - kNpad, 0, ch - 1) * ldcin +
+                                  clampi(px - kNpad, 0, cw - 1)]
+                           : T(0);
+    }
 #pragma unroll
-      for (int u = 0; u < 3; ++u) S[r * SP + lane + 32 * u] = v[u];
+    for (int k = 0; k < kPer; ++k) {
+      const int t = threadIdx.x + 256 * k;
+      const int r = t / kFE, c = t - r * kFE;
+      if (t < kFE * kFE) S[r][c] = v[k];
     }
   }
   __syncthreads();
-  const double gain = (1.0 - kPole) * (1.0 - 1.0 / kPole);
-  // rows of the tile that lie in the array
-  const int rlo = max(0, -gy0), rhi = min(kExt, nh - gy0);
-  const int clo = max(0, -gx0), chi = min(kExt, nw - gx0);
-  // axis 0: one thread per column
-  for (int c = threadIdx.x; c < kExt; c += blockDim.x) {
-    if (c < clo || c >= chi) continue;
-    iir_line_smem(S + c, SP, rlo, rhi, gy0 + rlo == 0, gy0 + rhi == nh, nh, gain);
+  // axis 0: rows ty, ty+8, ty+16, ty+24 of the tile share the staged rows
+  for (int c = lane; c < kFE; c += 32) {
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+    for (int k = 0; k < 2 * kFirR + 1 + 24; ++k) {
+      const double v = (double)S[ty + k][c];
+#pragma unroll
+      for (int o = 0; o < 4; ++o) {
+        const int m = k - 8 * o - kFirR;
+        if (m >= -kFirR && m <= kFirR) acc[o] = fma(fir_tap(m < 0 ? -m : m), v, acc[o]);
+      }
+    }
+#pragma unroll
+    for (int o = 0; o < 4; ++o) Tm[ty + 8 * o][c] = acc[o];
   }
   __syncthreads();
-  // axis 1: one thread per output row of the tile
-  for (int r = kWU + threadIdx.x; r < kWU + kTile; r += blockDim.x) {
-    if (r < rlo || r >= rhi) continue;
-    iir_line_smem(S + r * SP, 1, clo, chi, gx0 + clo == 0, gx0 + chi == nw, nw, gain);
-  }
-  __syncthreads();
-  for (int t = threadIdx.x; t < kTile * kTile; t += blockDim.x) {
-    const int r = t / kTile, c = t - r * kTile;
-    const int gy = y0 + r, gx = x0 + c;
-    if (gy < nh && gx < nw) coef[(int64_t)gy * ldc + gx] = S[(kWU + r) * SP + kWU + c];
+  // axis 1
+#pragma unroll
+  for (int o = 0; o < 4; ++o) {
+    const int r = ty + 8 * o;
+    double acc = 0.0;
+#pragma unroll
+    for (int m = -kFirR; m <= kFirR; ++m)
+      acc = fma(fir_tap(m < 0 ? -m : m), Tm[r][lane + kFirR + m], acc);
+    const int gy = y0 + r, gx = x0 + lane;
+    if (gy < nh && gx < nw) coef[(int64_t)gy * ldc + gx] = acc;
   }
 }
 
@@ -742,60 +564,74 @@ __global__ void __launch_bounds__(kTX * kTY) median_tiled_kernel(
       Lw[a][b] = 0;
     }
   }
+  __shared__ int list[kTX * kTY];
+  __shared__ int nlist;
+  if (tid == 0) nlist = 0;
   __syncthreads();
   const int i = y0 + threadIdx.y, j = x0 + threadIdx.x;
   const bool in = i < band.hi && i < h && j < w;
-  bool changed = false, needed = false;
+  const bool counted_here = i >= band.cnt_lo && i < band.cnt_hi;
+  bool needed = false;
   if (in) {
     const int ty = threadIdx.y + 2, tx = threadIdx.x + 2;
 #pragma unroll
     for (int di = -1; di <= 1; ++di)
 #pragma unroll
       for (int dj = -1; dj <= 1; ++dj) needed |= Lw[ty + di][tx + dj] != 0;
+    // low-confidence pixels go to a block-local work list; the others keep
+    // their disparity.  The sorting network then runs only for listed
+    // pixels, packed densely into warps.
+    if ((double)Cs[ty][tx] <= alpha) list[atomicAdd(&nlist, 1)] = tid;
+    else out[(int64_t)i * ld + j] = Ds[ty][tx];
+  }
+  __syncthreads();
+  unsigned nchanged = 0;
+  const int n_items = nlist;
+  for (int k = tid; k < n_items; k += kTX * kTY) {
+    const int p = list[k];
+    const int py = p / kTX, px = p - py * kTX;
+    const int ty = py + 2, tx = px + 2;
     const int16_t d0 = Ds[ty][tx];
     int16_t res = d0;
-    if ((double)Cs[ty][tx] <= alpha) {
-      // qualifying neighbours in static slots (others = +inf sentinel), a
-      // 32-wide bitonic network, then the lower median (n-1)/2
-      int v[32];
-      int n = 0;
+    // qualifying neighbours in static slots (others = +inf sentinel), a
+    // 32-wide bitonic network, then the lower median (n-1)/2
+    int v[32];
+    int n = 0;
 #pragma unroll
-      for (int t = 0; t < 32; ++t) {
-        const int di = t / 5 - 2, dj = t % 5 - 2;
-        bool q = false;
-        if (t < 25 && t != 12) q = (double)Cs[ty + di][tx + dj] > alpha;
-        v[t] = q ? (int)Ds[ty + di][tx + dj] : 0x7fffffff;
-        n += q;
-      }
-      if (n > 0) {
-#pragma unroll
-        for (int k = 2; k <= 32; k <<= 1)
-#pragma unroll
-          for (int jj = k >> 1; jj > 0; jj >>= 1)
-#pragma unroll
-            for (int t = 0; t < 32; ++t) {
-              const int l = t ^ jj;
-              if (l > t) {
-                const int a = v[t], b = v[l];
-                const bool up = (t & k) == 0;
-                v[t] = up ? min(a, b) : max(a, b);
-                v[l] = up ? max(a, b) : min(a, b);
-              }
-            }
-        const int m = (n - 1) >> 1;
-        int pick = v[0];
-#pragma unroll
-        for (int t = 1; t < 24; ++t) pick = (m == t) ? v[t] : pick;
-        res = (int16_t)pick;
-      }
+    for (int t = 0; t < 32; ++t) {
+      const int di = t / 5 - 2, dj = t % 5 - 2;
+      bool q = false;
+      if (t < 25 && t != 12) q = (double)Cs[ty + di][tx + dj] > alpha;
+      v[t] = q ? (int)Ds[ty + di][tx + dj] : 0x7fffffff;
+      n += q;
     }
-    out[(int64_t)i * ld + j] = res;
-    changed = res != d0;
+    if (n > 0) {
+#pragma unroll
+      for (int kk = 2; kk <= 32; kk <<= 1)
+#pragma unroll
+        for (int jj = kk >> 1; jj > 0; jj >>= 1)
+#pragma unroll
+          for (int t = 0; t < 32; ++t) {
+            const int l = t ^ jj;
+            if (l > t) {
+              const int a = v[t], b = v[l];
+              const bool up = (t & kk) == 0;
+              v[t] = up ? min(a, b) : max(a, b);
+              v[l] = up ? max(a, b) : min(a, b);
+            }
+          }
+      const int m = (n - 1) >> 1;
+      int pick = v[0];
+#pragma unroll
+      for (int t = 1; t < 24; ++t) pick = (m == t) ? v[t] : pick;
+      res = (int16_t)pick;
+    }
+    const int gi = y0 + py, gj = x0 + px;
+    out[(int64_t)gi * ld + gj] = res;
+    nchanged += (res != d0 && gi >= band.cnt_lo && gi < band.cnt_hi) ? 1u : 0u;
   }
-  const bool counted = i >= band.cnt_lo && i < band.cnt_hi;
   const int slot[2] = {kCntMedianReplaced, kCntNeeded};
-  const unsigned long long val[2] = {(changed && counted) ? 1ull : 0ull,
-                                     (needed && counted) ? 1ull : 0ull};
+  const unsigned long long val[2] = {nchanged, (needed && counted_here) ? 1ull : 0ull};
   const bool mx[2] = {false, false};
   block_accumulate<2>(counters, slot, val, mx);
 }
@@ -926,21 +762,29 @@ cudaError_t launch_stats_f64(const double* img, int h, int w, int64_t ld,
   return cudaGetLastError();
 }
 
-cudaError_t launch_bspline_prefilter(const float* c32, const double* c64,
-                                     int ch, int cw, int64_t ldcin,
-                                     double* coef, int64_t ldc, cudaStream_t s) {
+template <typename T>
+cudaError_t launch_fir(const T* cin, int ch, int cw, int64_t ldcin, double* coef, int64_t ldc,
+                       cudaStream_t s) {
   const int nh = ch + 2 * kNpad, nw = cw + 2 * kNpad;
-  constexpr size_t smem = sizeof(double) * kExt * (kExt + 1);
+  constexpr size_t smem = (sizeof(T) * kFE * (kFE + 1) + 7) / 8 * 8 +
+                          sizeof(double) * kFT * (kFE + 1);
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(bspline_tile_kernel,
+    cudaError_t e = cudaFuncSetAttribute(bspline_fir_kernel<T>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  const dim3 grid((nw + kTile - 1) / kTile, (nh + kTile - 1) / kTile);
-  bspline_tile_kernel<<<grid, 128, smem, s>>>(c32, c64, ch, cw, ldcin, coef, ldc);
+  const dim3 grid((nw + kFT - 1) / kFT, (nh + kFT - 1) / kFT);
+  bspline_fir_kernel<T><<<grid, 256, smem, s>>>(cin, ch, cw, ldcin, coef, ldc);
   return cudaGetLastError();
+}
+
+cudaError_t launch_bspline_prefilter(const float* c32, const double* c64,
+                                     int ch, int cw, int64_t ldcin,
+                                     double* coef, int64_t ldc, cudaStream_t s) {
+  return c32 ? launch_fir(c32, ch, cw, ldcin, coef, ldc, s)
+             : launch_fir(c64, ch, cw, ldcin, coef, ldc, s);
 }
 
 cudaError_t launch_prior_eval(const int16_t* dcoarse, int64_t ldd, int ch,

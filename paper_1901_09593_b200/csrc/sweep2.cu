@@ -305,10 +305,24 @@ sweep2_kernel(const SweepArgs a) {
   using LsT = typename SM::LsT;
   static_assert(sizeof(LsT) <= 2 * sizeof(typename SM::HxT), "left tile must fit");
   LsT& Ls = *reinterpret_cast<LsT*>(Hx);
-  for (int t = threadIdx.x; t < RR * LC; t += NT) {
-    const int rr = t / LC, e = t - rr * LC;
-    Ls[rr][e] = a.L[(int64_t)clampi(y0 - 1 - H2 + rr, 0, H - 1) * a.ld +
-                    clampi(x0 - 1 - H2 + e, 0, W - 1)];
+  {
+    // all loads in flight before the stores (one memory latency, not NL)
+    constexpr int NL = (RR * LC + NT - 1) / NT;
+    double v[NL];
+#pragma unroll
+    for (int k = 0; k < NL; ++k) {
+      const int t = threadIdx.x + NT * k;
+      const int rr = t / LC, e = t - rr * LC;
+      v[k] = t < RR * LC ? a.L[(int64_t)clampi(y0 - 1 - H2 + rr, 0, H - 1) * a.ld +
+                              clampi(x0 - 1 - H2 + e, 0, W - 1)]
+                         : 0.0;
+    }
+#pragma unroll
+    for (int k = 0; k < NL; ++k) {
+      const int t = threadIdx.x + NT * k;
+      const int rr = t / LC, e = t - rr * LC;
+      if (t < RR * LC) Ls[rr][e] = v[k];
+    }
   }
   __syncthreads();
 
