@@ -234,7 +234,12 @@ struct StageEvents {
 };
 
 // Enqueue the whole pair on `s` (also used under stream capture).
-int enqueue(mshbm_ctx* ctx, Plan& p, cudaStream_t s, std::vector<StageEvents>* tev) {
+// side/evs (graph capture only): the window statistics and staging arrays
+// of levels K-1..0 run on a forked branch, so they overlap the coarse
+// levels' matching (which leaves most SMs idle); level k's sweep joins on
+// evs[k].  evs[K+1] is the fork point.
+int enqueue(mshbm_ctx* ctx, Plan& p, cudaStream_t s, std::vector<StageEvents>* tev,
+            cudaStream_t side = nullptr, cudaEvent_t* evs = nullptr) {
   int n = 0;
   const mshbm_config& cfg = p.cfg;
   const int dir = cfg.sign == MSHBM_SIGN_PAPER ? -1 : 1;
@@ -250,10 +255,17 @@ int enqueue(mshbm_ctx* ctx, Plan& p, cudaStream_t s, std::vector<StageEvents>* t
       ++n;
     }
   }
-  for (int k = 0; k <= p.K; ++k) {
+  const bool fork = side != nullptr && evs != nullptr && p.K > 0;
+  if (fork) {
+    CK(cudaEventRecord(evs[p.K + 1], s));
+    CK(cudaStreamWaitEvent(side, evs[p.K + 1], 0));
+  }
+  for (int k = p.K; k >= 0; --k) {
     LevelBuf& l = p.lv[k];
-    CK(launch_stats_f32(l.R, l.h, l.w, l.ld, l.b, cfg.sigma_eps, l.muR, l.isR, l.ld, s));
-    CK(launch_prep_staging(l.R, l.ld, l.muR, l.isR, l.ld, l.h, l.w, l.pc, l.Rp, l.Mp, l.ldp, s));
+    cudaStream_t t = (fork && k < p.K) ? side : s;
+    CK(launch_stats_f32(l.R, l.h, l.w, l.ld, l.b, cfg.sigma_eps, l.muR, l.isR, l.ld, t));
+    CK(launch_prep_staging(l.R, l.ld, l.muR, l.isR, l.ld, l.h, l.w, l.pc, l.Rp, l.Mp, l.ldp, t));
+    if (fork && k < p.K) CK(cudaEventRecord(evs[k], side));
     n += 2;
   }
   for (int k = p.K; k >= 0; --k) {
@@ -281,6 +293,7 @@ int enqueue(mshbm_ctx* ctx, Plan& p, cudaStream_t s, std::vector<StageEvents>* t
     a.counters = cnt;
     a.rows = l.rows;
     a.Rp = l.Rp; a.Mp = l.Mp; a.ldp = l.ldp; a.pc = l.pc;
+    if (fork && k < p.K) CK(cudaStreamWaitEvent(s, evs[k], 0));
     if (ev) CK(cudaEventRecord(ev->sel0, s));
     CK(launch_sweep(a, s, &n));
     if (ev) CK(cudaEventRecord(ev->sel1, s));
@@ -343,10 +356,16 @@ int launch_plan(mshbm_ctx* ctx, Plan& p, cudaStream_t s, int flags,
     if (!p.exec) {
       cudaStream_t cs;
       CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+      cudaStream_t side;
+      CK(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+      std::vector<cudaEvent_t> evs(p.K + 2);
+      for (auto& e : evs) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
       cudaGraph_t g;
       CK(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
-      int st = enqueue(ctx, p, cs, nullptr);
+      int st = enqueue(ctx, p, cs, nullptr, side, evs.data());
       cudaError_t ce = cudaStreamEndCapture(cs, &g);
+      for (auto& e : evs) cudaEventDestroy(e);
+      cudaStreamDestroy(side);
       cudaStreamDestroy(cs);
       if (st) return st;
       CK(ce);
