@@ -237,7 +237,9 @@ struct StageEvents {
 // side/evs (graph capture only): the window statistics and staging arrays
 // of levels K-1..0 run on a forked branch, so they overlap the coarse
 // levels' matching (which leaves most SMs idle); level k's sweep joins on
-// evs[k].  evs[K+1] is the fork point.
+// evs[k].  evs[K+1] is the fork point.  The spline prefilter of level k's
+// costs also runs on the branch, beside level k's median (evs[K+2+k] =
+// sweep k done, evs[2K+3+(k-1)] = prefilter done, joined by prior k-1).
 int enqueue(mshbm_ctx* ctx, Plan& p, cudaStream_t s, std::vector<StageEvents>* tev,
             cudaStream_t side = nullptr, cudaEvent_t* evs = nullptr) {
   int n = 0;
@@ -275,8 +277,12 @@ int enqueue(mshbm_ctx* ctx, Plan& p, cudaStream_t s, std::vector<StageEvents>* t
     if (ev) CK(cudaEventRecord(ev->up0, s));
     if (k < p.K) {
       LevelBuf& c = p.lv[k + 1];
-      CK(launch_bspline_prefilter(c.c, nullptr, c.h, c.w, c.ld, c.coef, c.ldc, s));
-      n += 1;
+      if (fork) {
+        CK(cudaStreamWaitEvent(s, evs[2 * p.K + 3 + k], 0));   // prefilter of level k+1
+      } else {
+        CK(launch_bspline_prefilter(c.c, nullptr, c.h, c.w, c.ld, c.coef, c.ldc, s));
+        n += 1;
+      }
       CK(launch_prior_eval(c.dmed, c.ld, c.h, c.w, c.coef, c.ldc, l.h, l.w, l.d, cfg.radius,
                            cfg.beta, l.wc, l.ld, cnt, l.rows, s));
       ++n;
@@ -297,6 +303,15 @@ int enqueue(mshbm_ctx* ctx, Plan& p, cudaStream_t s, std::vector<StageEvents>* t
     if (ev) CK(cudaEventRecord(ev->sel0, s));
     CK(launch_sweep(a, s, &n));
     if (ev) CK(cudaEventRecord(ev->sel1, s));
+    if (fork && k > 0) {
+      // the prefilter of this level's costs (next level's prior) overlaps
+      // this level's selective median
+      CK(cudaEventRecord(evs[p.K + 2 + k], s));
+      CK(cudaStreamWaitEvent(side, evs[p.K + 2 + k], 0));
+      CK(launch_bspline_prefilter(l.c, nullptr, l.h, l.w, l.ld, l.coef, l.ldc, side));
+      CK(cudaEventRecord(evs[2 * p.K + 3 + (k - 1)], side));
+      n += 1;
+    }
     if (ev) CK(cudaEventRecord(ev->med0, s));
     CK(launch_median_pipeline(l.dsel, l.c, l.low, l.ld, l.h, l.w, cfg.alpha, l.dmed, cnt, l.rows,
                               s));
@@ -358,7 +373,7 @@ int launch_plan(mshbm_ctx* ctx, Plan& p, cudaStream_t s, int flags,
       CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
       cudaStream_t side;
       CK(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
-      std::vector<cudaEvent_t> evs(p.K + 2);
+      std::vector<cudaEvent_t> evs(3 * p.K + 4);
       for (auto& e : evs) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
       cudaGraph_t g;
       CK(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
