@@ -53,6 +53,8 @@ cudaError_t launch_sweep(const SweepArgs& a, cudaStream_t s, int* n_launch);
 bool sweep_supported_block(int b);
 // two-pixels-per-thread variant (sweep2.cu) for b in {3,5,7,9,11}
 bool sweep2_supported(int b);
+bool sweep3_supported(int b);
+cudaError_t launch_sweep3(const SweepArgs& a, cudaStream_t s);
 cudaError_t launch_sweep2(const SweepArgs& a, cudaStream_t s);
 
 // Column margin of the padded staging arrays for search bound d, block b.

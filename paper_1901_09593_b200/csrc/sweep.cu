@@ -471,7 +471,8 @@ cudaError_t launch_sweep(const SweepArgs& a, cudaStream_t s, int* n_launch) {
     const char* v = getenv("MSHBM_SWEEP_IMPL");   // 1 = one pixel per thread
     impl = v ? atoi(v) : 2;
   }
-  if (impl == 2 && sweep2_supported(a.block)) return launch_sweep2(a, s);
+  if (impl == 3 && sweep3_supported(a.block)) return launch_sweep3(a, s);
+  if (impl >= 2 && sweep2_supported(a.block)) return launch_sweep2(a, s);
   return a.dir > 0 ? launch_dir<1>(a, s) : launch_dir<-1>(a, s);
 }
 
