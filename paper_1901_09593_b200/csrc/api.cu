@@ -248,9 +248,16 @@ int enqueue(mshbm_ctx* ctx, Plan& p, cudaStream_t s, std::vector<StageEvents>* t
   CK(cudaMemsetAsync(p.counters, 0,
                      sizeof(unsigned long long) * (p.K + 1) * kCntSlots * kCntCopies, s));
   if (!p.user) {
-    CK(launch_f32_to_f64(p.in_l, p.in_r, p.H, p.W, p.ld_in, p.lv[0].L, p.lv[0].R, p.lv[0].ld, s));
+    if (p.K == 0) {
+      CK(launch_f32_to_f64(p.in_l, p.in_r, p.H, p.W, p.ld_in, p.lv[0].L, p.lv[0].R, p.lv[0].ld,
+                           s));
+    } else {
+      // level 1 straight from the fp32 input; also writes the fp64 level 0
+      CK(launch_downsample_f32(p.in_l, p.in_r, p.H, p.W, p.ld_in, p.lv[1].L, p.lv[1].R,
+                               p.lv[1].ld, p.lv[0].L, p.lv[0].R, p.lv[0].ld, s));
+    }
     ++n;
-    for (int k = 1; k <= p.K; ++k) {
+    for (int k = 2; k <= p.K; ++k) {
       const LevelBuf& a = p.lv[k - 1];
       LevelBuf& b = p.lv[k];
       CK(launch_downsample(a.L, a.R, a.h, a.w, a.ld, b.L, b.R, b.ld, s));

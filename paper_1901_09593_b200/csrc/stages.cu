@@ -33,13 +33,17 @@ __global__ void f32_to_f64_kernel(const float* a, const float* b, int h, int w,
 // gaussian_downsample (pyramid.py:65-81): (1,4,6,4,1)/16 along axis 0, then
 // axis 1, replicate borders, keep even rows/cols.  Only the kept samples are
 // computed: out(I,J) = sum_b k_b sum_a k_a X(2I+a-2, 2J+b-2) (clamped).
-__global__ void downsample_kernel(const double* in0, const double* in1, int h,
-                                  int w, int64_t ldi, double* out0,
-                                  double* out1, int64_t ldo, int oh, int ow) {
+// COPY: level 0 from the fp32 input -- the same kernel also writes the exact
+// fp64 copy of its 2x2 input block (the level-0 image), so the pipeline needs
+// no separate conversion pass.
+template <typename T, bool COPY>
+__global__ void downsample_kernel(const T* in0, const T* in1, int h, int w, int64_t ldi,
+                                  double* out0, double* out1, int64_t ldo, int oh, int ow,
+                                  double* cp0, double* cp1, int64_t ldc) {
   const int J = blockIdx.x * blockDim.x + threadIdx.x;
   const int I = blockIdx.y * blockDim.y + threadIdx.y;
   if (J >= ow || I >= oh) return;
-  const double* in = blockIdx.z ? in1 : in0;
+  const T* in = blockIdx.z ? in1 : in0;
   double* out = blockIdx.z ? out1 : out0;
   const double k[5] = {1.0 / 16.0, 4.0 / 16.0, 6.0 / 16.0, 4.0 / 16.0, 1.0 / 16.0};
   int rows[5];
@@ -51,10 +55,20 @@ __global__ void downsample_kernel(const double* in0, const double* in1, int h,
     const int col = clampi(2 * J + b - 2, 0, w - 1);
     double v = 0.0;
 #pragma unroll
-    for (int a = 0; a < 5; ++a) v += k[a] * in[(int64_t)rows[a] * ldi + col];
+    for (int a = 0; a < 5; ++a) v += k[a] * (double)in[(int64_t)rows[a] * ldi + col];
     acc += k[b] * v;
   }
   out[(int64_t)I * ldo + J] = acc;
+  if constexpr (COPY) {
+    double* cp = blockIdx.z ? cp1 : cp0;
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int b = 0; b < 2; ++b) {
+        const int y = 2 * I + a, x = 2 * J + b;
+        if (y < h && x < w) cp[(int64_t)y * ldc + x] = (double)in[(int64_t)y * ldi + x];
+      }
+  }
 }
 
 // ------------------------------------------------------------------ K2
@@ -494,51 +508,105 @@ __global__ void __launch_bounds__(kTX * kTY) stats_tiled_kernel(const double* im
 }
 
 // prior_eval with the 4x4 spline support of the block staged in smem
+constexpr int kPY = 32;   // fine rows per prior_eval block (4 per thread)
+
 __global__ void __launch_bounds__(kTX * kTY) prior_eval_tiled_kernel(
     const int16_t* dco, int64_t ldd, int ch, int cw, const double* coef, int64_t ldc, int h,
     int w, int d, int r, double beta, int* wc, int64_t ldw, unsigned long long* counters,
     RowBand band, double ry, double rx) {
-  constexpr int CR = 12, CC = 24;
+  // 32 fine rows x 32 columns need <= 21 x 21 coefficients (ratio <= 0.52)
+  constexpr int CR = 22, CC = 24;
   __shared__ double Cs[CR][CC];
+  // spline weights depend only on the row (y) or the column (x): computed
+  // once per block row / column; Wx tap-major so lanes read consecutive words
+  __shared__ double Wy[kPY][4], Wx[4][kTX];
+  __shared__ int Iy[kPY], Ix[kTX];
   const int nh = ch + 2 * kNpad, nw = cw + 2 * kNpad;
-  const int i0 = band.lo + blockIdx.y * kTY, j0 = blockIdx.x * kTX;
+  const int i0 = band.lo + blockIdx.y * kPY, j0 = blockIdx.x * kTX;
   const int ylo = (int)floor(((double)i0 + 0.5) * ry - 0.5 + kNpad) - 1;
   const int xlo = (int)floor(((double)j0 + 0.5) * rx - 0.5 + kNpad) - 1;
   const int tid = threadIdx.y * kTX + threadIdx.x;
-  for (int t = tid; t < CR * CC; t += kTX * kTY) {
-    const int a = t / CC, b = t - a * CC;
-    Cs[a][b] = coef[(int64_t)clampi(ylo + a, 0, nh - 1) * ldc + clampi(xlo + b, 0, nw - 1)];
+  {
+    constexpr int kPer = (CR * CC + kTX * kTY - 1) / (kTX * kTY);
+    double v[kPer];
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+      const int t = tid + kTX * kTY * k;
+      const int a = t / CC, b = t - a * CC;
+      v[k] = t < CR * CC ? coef[(int64_t)clampi(ylo + a, 0, nh - 1) * ldc +
+                                clampi(xlo + b, 0, nw - 1)]
+                         : 0.0;
+    }
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+      const int t = tid + kTX * kTY * k;
+      if (t < CR * CC) Cs[t / CC][t % CC] = v[k];
+    }
+  }
+  if (tid < kTX) {
+    const double x = ((double)(j0 + tid) + 0.5) * rx - 0.5 + kNpad;
+    const double fx = floor(x);
+    double wt[4];
+    bspline_w(x - fx, wt);
+#pragma unroll
+    for (int b = 0; b < 4; ++b) Wx[b][tid] = wt[b];
+    Ix[tid] = (int)fx - 1 - xlo;
+  } else if (tid < kTX + kPY) {
+    const int rr = tid - kTX;
+    const double y = ((double)(i0 + rr) + 0.5) * ry - 0.5 + kNpad;
+    const double fy = floor(y);
+    bspline_w(y - fy, Wy[rr]);
+    Iy[rr] = (int)fy - 1 - ylo;
   }
   __syncthreads();
-  const int i = i0 + threadIdx.y, j = j0 + threadIdx.x;
-  const bool in = i < band.hi && i < h && j < w;
-  bool trusted = false;
-  int center = 0;
-  if (in) {
-    const double y = ((double)i + 0.5) * ry - 0.5 + kNpad;
-    const double x = ((double)j + 0.5) * rx - 0.5 + kNpad;
-    const double fy = floor(y), fx = floor(x);
-    double wy[4], wx[4];
-    bspline_w(y - fy, wy);
-    bspline_w(x - fx, wx);
-    const int iy = (int)fy - 1 - ylo, ix = (int)fx - 1 - xlo;   // within the tile
-    double chat = 0.0;
+  const int j = j0 + threadIdx.x;
+  double wx[4];
 #pragma unroll
-    for (int a = 0; a < 4; ++a) {
-      double rr = 0.0;
+  for (int b = 0; b < 4; ++b) wx[b] = Wx[b][threadIdx.x];
+  const int ix = Ix[threadIdx.x];
+  unsigned ntr = 0;
+  unsigned long long wsum = 0, wmax = 0;
 #pragma unroll
-      for (int b = 0; b < 4; ++b) rr += wx[b] * Cs[iy + a][ix + b];
-      chat += wy[a] * rr;
+  for (int q = 0; q < kPY / kTY; ++q) {
+    const int ty = threadIdx.y + kTY * q;
+    const int i = i0 + ty;
+    if (i < band.hi && i < h && j < w) {
+      const double* wy = Wy[ty];
+      const int iy = Iy[ty];   // within the tile
+      double chat = 0.0;
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        double rr = 0.0;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) rr += wx[b] * Cs[iy + a][ix + b];
+        chat += wy[a] * rr;
+      }
+      chat = fmin(fmax(chat, -1.0), 1.0);
+      const int center = 2 * (int)dco[(int64_t)(i >> 1) * ldd + (j >> 1)];
+      const bool ok = (center + r >= 0) && (center - r <= d);
+      const bool trusted = (chat > beta) && ok;
+      wc[(int64_t)i * ldw + j] = trusted ? center : kWcNone;
+      if (trusted && i >= band.cnt_lo && i < band.cnt_hi) {
+        const unsigned long long ws =
+            (unsigned long long)(min(center + r, d) - max(center - r, 0) + 1);
+        ntr += 1;
+        wsum += ws;
+        wmax = ws > wmax ? ws : wmax;
+      }
     }
-    chat = fmin(fmax(chat, -1.0), 1.0);
-    center = 2 * (int)dco[(int64_t)(i >> 1) * ldd + (j >> 1)];
-    const bool ok = (center + r >= 0) && (center - r <= d);
-    trusted = (chat > beta) && ok;
-    wc[(int64_t)i * ldw + j] = trusted ? center : kWcNone;
   }
-  const bool counted = i >= band.cnt_lo && i < band.cnt_hi;
-  count_trusted(trusted && counted, center, r, d, counters);
+  const int slot[3] = {kCntTrusted, kCntTrustedEvals, kCntWindowMax};
+  const unsigned long long val[3] = {ntr, wsum, wmax};
+  const bool mx[3] = {false, false, true};
+  block_accumulate<3>(counters, slot, val, mx);
 }
+
+// Sorting network for 24 keys: Batcher's odd-even merge sort for 32 inputs
+// with the comparators that touch inputs 24..31 removed (those would hold
+// +inf sentinels and never move).  Generated and checked (random inputs,
+// 0/1 principle) by tools/median_net.py.
+constexpr int kMedNetLen = 132;
+__device__ constexpr unsigned char kMedNet[2 * kMedNetLen] = {0,1,2,3,4,5,6,7,8,9,10,11,12,13,14,15,16,17,18,19,20,21,22,23,0,2,1,3,4,6,5,7,8,10,9,11,12,14,13,15,16,18,17,19,20,22,21,23,1,2,5,6,9,10,13,14,17,18,21,22,0,4,1,5,2,6,3,7,8,12,9,13,10,14,11,15,16,20,17,21,18,22,19,23,2,4,3,5,10,12,11,13,18,20,19,21,1,2,3,4,5,6,9,10,11,12,13,14,17,18,19,20,21,22,0,8,1,9,2,10,3,11,4,12,5,13,6,14,7,15,4,8,5,9,6,10,7,11,2,4,3,5,6,8,7,9,10,12,11,13,18,20,19,21,1,2,3,4,5,6,7,8,9,10,11,12,13,14,17,18,19,20,21,22,0,16,1,17,2,18,3,19,4,20,5,21,6,22,7,23,8,16,9,17,10,18,11,19,12,20,13,21,14,22,15,23,4,8,5,9,6,10,7,11,12,16,13,17,14,18,15,19,2,4,3,5,6,8,7,9,10,12,11,13,14,16,15,17,18,20,19,21,1,2,3,4,5,6,7,8,9,10,11,12,13,14,15,16,17,18,19,20,21,22};
 
 // selective median (pipeline) with the 5x5 neighbourhood staged in smem
 __global__ void __launch_bounds__(kTX * kTY) median_tiled_kernel(
@@ -593,33 +661,28 @@ __global__ void __launch_bounds__(kTX * kTY) median_tiled_kernel(
     const int ty = py + 2, tx = px + 2;
     const int16_t d0 = Ds[ty][tx];
     int16_t res = d0;
-    // qualifying neighbours in static slots (others = +inf sentinel), a
-    // 32-wide bitonic network, then the lower median (n-1)/2
-    int v[32];
+    // the 24 neighbour slots (centre excluded), +inf sentinels for the
+    // non-qualifying ones, sorted by a fixed 132-comparator network (Batcher's
+    // odd-even merge sort for 32 inputs restricted to 24; kMedNet), then the
+    // lower median (n-1)/2
+    int v[24];
     int n = 0;
 #pragma unroll
-    for (int t = 0; t < 32; ++t) {
-      const int di = t / 5 - 2, dj = t % 5 - 2;
-      bool q = false;
-      if (t < 25 && t != 12) q = (double)Cs[ty + di][tx + dj] > alpha;
+    for (int t = 0; t < 24; ++t) {
+      const int u = t < 12 ? t : t + 1;          // skip the centre (slot 12)
+      const int di = u / 5 - 2, dj = u % 5 - 2;
+      const bool q = (double)Cs[ty + di][tx + dj] > alpha;
       v[t] = q ? (int)Ds[ty + di][tx + dj] : 0x7fffffff;
       n += q;
     }
     if (n > 0) {
 #pragma unroll
-      for (int kk = 2; kk <= 32; kk <<= 1)
-#pragma unroll
-        for (int jj = kk >> 1; jj > 0; jj >>= 1)
-#pragma unroll
-          for (int t = 0; t < 32; ++t) {
-            const int l = t ^ jj;
-            if (l > t) {
-              const int a = v[t], b = v[l];
-              const bool up = (t & kk) == 0;
-              v[t] = up ? min(a, b) : max(a, b);
-              v[l] = up ? max(a, b) : min(a, b);
-            }
-          }
+      for (int c = 0; c < kMedNetLen; ++c) {
+        const int i0 = kMedNet[2 * c], i1 = kMedNet[2 * c + 1];
+        const int x = v[i0], y = v[i1];
+        v[i0] = min(x, y);
+        v[i1] = max(x, y);
+      }
       const int m = (n - 1) >> 1;
       int pick = v[0];
 #pragma unroll
@@ -731,8 +794,19 @@ cudaError_t launch_downsample(const double* in0, const double* in1, int h,
                               int64_t ld_out, cudaStream_t s) {
   const int oh = (h + 1) / 2, ow = (w + 1) / 2;
   dim3 blk(32, 8);
-  downsample_kernel<<<grid2d(ow, oh, blk, in1 ? 2 : 1), blk, 0, s>>>(
-      in0, in1, h, w, ld_in, out0, out1, ld_out, oh, ow);
+  downsample_kernel<double, false><<<grid2d(ow, oh, blk, in1 ? 2 : 1), blk, 0, s>>>(
+      in0, in1, h, w, ld_in, out0, out1, ld_out, oh, ow, nullptr, nullptr, 0);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_downsample_f32(const float* in0, const float* in1, int h, int w,
+                                  int64_t ld_in, double* out0, double* out1, int64_t ld_out,
+                                  double* copy0, double* copy1, int64_t ld_copy,
+                                  cudaStream_t s) {
+  const int oh = (h + 1) / 2, ow = (w + 1) / 2;
+  dim3 blk(32, 8);
+  downsample_kernel<float, true><<<grid2d(ow, oh, blk, 2), blk, 0, s>>>(
+      in0, in1, h, w, ld_in, out0, out1, ld_out, oh, ow, copy0, copy1, ld_copy);
   return cudaGetLastError();
 }
 
@@ -793,7 +867,7 @@ cudaError_t launch_prior_eval(const int16_t* dcoarse, int64_t ldd, int ch,
                               int64_t ldw, unsigned long long* counters,
                               RowBand rows, cudaStream_t s) {
   dim3 blk(32, 8);
-  const dim3 g((w + 31) / 32, (rows.hi - rows.lo + 7) / 8);
+  const dim3 g((w + 31) / 32, (rows.hi - rows.lo + kPY - 1) / kPY);
   prior_eval_tiled_kernel<<<g, blk, 0, s>>>(dcoarse, ldd, ch, cw, coef, ldc, h, w, d, radius,
                                             beta, wc, ldw, counters, rows, (double)ch / (double)h,
                                             (double)cw / (double)w);
