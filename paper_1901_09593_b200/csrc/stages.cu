@@ -609,48 +609,73 @@ constexpr int kMedNetLen = 132;
 __device__ constexpr unsigned char kMedNet[2 * kMedNetLen] = {0,1,2,3,4,5,6,7,8,9,10,11,12,13,14,15,16,17,18,19,20,21,22,23,0,2,1,3,4,6,5,7,8,10,9,11,12,14,13,15,16,18,17,19,20,22,21,23,1,2,5,6,9,10,13,14,17,18,21,22,0,4,1,5,2,6,3,7,8,12,9,13,10,14,11,15,16,20,17,21,18,22,19,23,2,4,3,5,10,12,11,13,18,20,19,21,1,2,3,4,5,6,9,10,11,12,13,14,17,18,19,20,21,22,0,8,1,9,2,10,3,11,4,12,5,13,6,14,7,15,4,8,5,9,6,10,7,11,2,4,3,5,6,8,7,9,10,12,11,13,18,20,19,21,1,2,3,4,5,6,7,8,9,10,11,12,13,14,17,18,19,20,21,22,0,16,1,17,2,18,3,19,4,20,5,21,6,22,7,23,8,16,9,17,10,18,11,19,12,20,13,21,14,22,15,23,4,8,5,9,6,10,7,11,12,16,13,17,14,18,15,19,2,4,3,5,6,8,7,9,10,12,11,13,14,16,15,17,18,20,19,21,1,2,3,4,5,6,7,8,9,10,11,12,13,14,15,16,17,18,19,20,21,22};
 
 // selective median (pipeline) with the 5x5 neighbourhood staged in smem
+constexpr int kMY = 32;   // rows per median block (4 per thread)
+
 __global__ void __launch_bounds__(kTX * kTY) median_tiled_kernel(
     const int16_t* d, const float* c, const uint8_t* low, int64_t ld, int h, int w,
     double alpha, int16_t* out, unsigned long long* counters, RowBand band) {
-  constexpr int TR = kTY + 4, TC = kTX + 4;
+  constexpr int TR = kMY + 4, TC = kTX + 4;
   __shared__ float Cs[TR][TC];
   __shared__ int16_t Ds[TR][TC];
   __shared__ uint8_t Lw[TR][TC];
-  const int x0 = blockIdx.x * kTX, y0 = band.lo + blockIdx.y * kTY;
+  const int x0 = blockIdx.x * kTX, y0 = band.lo + blockIdx.y * kMY;
   const int tid = threadIdx.y * kTX + threadIdx.x;
-  for (int t = tid; t < TR * TC; t += kTX * kTY) {
-    const int a = t / TC, b = t - a * TC;
-    const int gy = y0 - 2 + a, gx = x0 - 2 + b;
-    if (gy >= 0 && gy < h && gx >= 0 && gx < w) {
-      const int64_t o = (int64_t)gy * ld + gx;
-      Cs[a][b] = c[o];
-      Ds[a][b] = d[o];
-      Lw[a][b] = low[o];
-    } else {
-      Cs[a][b] = -2.f;     // below any legal alpha: never qualifies (matcher.py:345)
-      Ds[a][b] = 0;
-      Lw[a][b] = 0;
+  {
+    // all of a thread's loads in flight before the stores
+    constexpr int kPer = (TR * TC + kTX * kTY - 1) / (kTX * kTY);
+    float cv[kPer];
+    int16_t dv[kPer];
+    uint8_t lv[kPer];
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+      const int t = tid + kTX * kTY * k;
+      const int a = t / TC, b = t - a * TC;
+      const int gy = y0 - 2 + a, gx = x0 - 2 + b;
+      cv[k] = -2.f;     // below any legal alpha: never qualifies (matcher.py:345)
+      dv[k] = 0;
+      lv[k] = 0;
+      if (t < TR * TC && gy >= 0 && gy < h && gx >= 0 && gx < w) {
+        const int64_t o = (int64_t)gy * ld + gx;
+        cv[k] = c[o];
+        dv[k] = d[o];
+        lv[k] = low[o];
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+      const int t = tid + kTX * kTY * k;
+      if (t < TR * TC) {
+        const int a = t / TC, b = t - a * TC;
+        Cs[a][b] = cv[k];
+        Ds[a][b] = dv[k];
+        Lw[a][b] = lv[k];
+      }
     }
   }
-  __shared__ int list[kTX * kTY];
+  __shared__ short list[kMY * kTX];
   __shared__ int nlist;
   if (tid == 0) nlist = 0;
   __syncthreads();
-  const int i = y0 + threadIdx.y, j = x0 + threadIdx.x;
-  const bool in = i < band.hi && i < h && j < w;
-  const bool counted_here = i >= band.cnt_lo && i < band.cnt_hi;
-  bool needed = false;
-  if (in) {
-    const int ty = threadIdx.y + 2, tx = threadIdx.x + 2;
+  const int j = x0 + threadIdx.x;
+  unsigned nneeded = 0;
 #pragma unroll
-    for (int di = -1; di <= 1; ++di)
+  for (int q = 0; q < kMY / kTY; ++q) {
+    const int py = threadIdx.y + kTY * q;
+    const int i = y0 + py;
+    if (i < band.hi && i < h && j < w) {
+      const int ty = py + 2, tx = threadIdx.x + 2;
+      bool needed = false;
 #pragma unroll
-      for (int dj = -1; dj <= 1; ++dj) needed |= Lw[ty + di][tx + dj] != 0;
-    // low-confidence pixels go to a block-local work list; the others keep
-    // their disparity.  The sorting network then runs only for listed
-    // pixels, packed densely into warps.
-    if ((double)Cs[ty][tx] <= alpha) list[atomicAdd(&nlist, 1)] = tid;
-    else out[(int64_t)i * ld + j] = Ds[ty][tx];
+      for (int di = -1; di <= 1; ++di)
+#pragma unroll
+        for (int dj = -1; dj <= 1; ++dj) needed |= Lw[ty + di][tx + dj] != 0;
+      nneeded += (needed && i >= band.cnt_lo && i < band.cnt_hi) ? 1u : 0u;
+      // low-confidence pixels go to a block-local work list; the others
+      // keep their disparity.  The sorting network then runs only for
+      // listed pixels, packed densely into warps.
+      if ((double)Cs[ty][tx] <= alpha) list[atomicAdd(&nlist, 1)] = (short)(py * kTX + threadIdx.x);
+      else out[(int64_t)i * ld + j] = Ds[ty][tx];
+    }
   }
   __syncthreads();
   unsigned nchanged = 0;
@@ -694,7 +719,7 @@ __global__ void __launch_bounds__(kTX * kTY) median_tiled_kernel(
     nchanged += (res != d0 && gi >= band.cnt_lo && gi < band.cnt_hi) ? 1u : 0u;
   }
   const int slot[2] = {kCntMedianReplaced, kCntNeeded};
-  const unsigned long long val[2] = {nchanged, (needed && counted_here) ? 1ull : 0ull};
+  const unsigned long long val[2] = {nchanged, nneeded};
   const bool mx[2] = {false, false};
   block_accumulate<2>(counters, slot, val, mx);
 }
@@ -899,7 +924,7 @@ cudaError_t launch_median_pipeline(const int16_t* d, const float* c,
                                    unsigned long long* counters, RowBand rows,
                                    cudaStream_t s) {
   dim3 blk(32, 8);
-  const dim3 g((w + 31) / 32, (rows.hi - rows.lo + 7) / 8);
+  const dim3 g((w + 31) / 32, (rows.hi - rows.lo + kMY - 1) / kMY);
   median_tiled_kernel<<<g, blk, 0, s>>>(d, c, low, ld, h, w, alpha, out, counters, rows);
   return cudaGetLastError();
 }
