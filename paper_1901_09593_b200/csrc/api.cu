@@ -186,7 +186,7 @@ void carve(Plan& p, Carver& cv) {
     l.c = cv.take<float>(n);
     l.low = cv.take<uint8_t>(n);
     l.ldc = round_up(l.w + 24, 32);
-    l.coef = cv.take<double>((size_t)l.ldc * (l.h + 24) * 2);   // + IIR scratch
+    l.coef = cv.take<double>((size_t)l.ldc * (l.h + 24));
     l.pc = staging_margin(l.d, l.b);
     l.ldp = round_up(l.w + 2 * l.pc, 32);
     l.Rp = cv.take<float>((size_t)l.ldp * l.h);
@@ -195,6 +195,12 @@ void carve(Plan& p, Carver& cv) {
 }
 
 int build_plan(mshbm_ctx* ctx, Plan& p) {
+  for (const LevelBuf& l : p.lv) {
+    // the sweep addresses its staging arrays with 32-bit element offsets
+    const int64_t ldp = round_up(l.w + 2 * staging_margin(l.d, l.b), 32);
+    if (ldp * l.h >= ((int64_t)1 << 31))
+      return fail(ctx, MSHBM_ERR_UNSUPPORTED, "level too large for 32-bit staging offsets");
+  }
   Carver probe;
   carve(p, probe);
   CK(cudaMalloc(&p.arena, probe.off + 256));

@@ -279,23 +279,62 @@ sweep2_kernel(const SweepArgs a) {
   // prefetch registers.  Warp w copies rows w, w+NR, ...
   const float* __restrict__ Rp = a.Rp + a.pc;
   const float2* __restrict__ Mp = a.Mp + a.pc;
+  // per-thread source offsets of the rows this warp copies, computed once
+  // (row clamp, pitch multiply, lane); each chunk only adds its z shift
+  constexpr int KR = (RR + NR - 1) / NR, KM = (NROW + NR - 1) / NR;
+  constexpr int UR = (RW + 31) / 32, UM = (SW + 31) / 32;
+  // Kept in registers, except at b = 7 (2 CTAs at the 128-register cap,
+  // where they would spill): there in shared memory, warp-uniform broadcast
+  // loads, no registers held across the sweep (measured best per b).
+  constexpr bool kOffReg = (B != 7);
+  constexpr int KO = KR + KM;
+  __shared__ int s_off[kOffReg ? 1 : NR][KO];
+  int r_off[KO];
+#pragma unroll
+  for (int k = 0; k < KO; ++k)
+    r_off[k] = k < KR
+        ? clampi(y0 - 1 - H2 + wp + NR * k, 0, H - 1) * (int)a.ldp + (x0 - 1 - H2)
+        : clampi(y0 - 1 + wp + NR * (k - KR), 0, H - 1) * (int)a.ldp + (x0 - 1);
+  if constexpr (!kOffReg) {
+    if (lane == 0) {
+#pragma unroll
+      for (int k = 0; k < KO; ++k) s_off[wp][k] = r_off[k];
+    }
+    __syncwarp();
+  }
+  auto off = [&](int k) { return kOffReg ? r_off[k] : s_off[wp][k]; };
   auto issue = [&](int buf, int z0) {
-    const int s0 = DIR > 0 ? (x0 - 1 - H2 - z0 - (ZC - 1)) : (x0 - 1 - H2 + z0);
-    for (int rr = wp; rr < RR; rr += NR) {
-      const float* src = Rp + (int64_t)clampi(y0 - 1 - H2 + rr, 0, H - 1) * a.ldp + s0;
-      if constexpr (PK == 1) {
-        for (int e = lane; e < RW; e += 32) {
-          cp_async4(&Rs[2 * buf][rr][e], src + e);
-          cp_async4(&Rs[2 * buf + 1][rr][e], src + e + 1);
+    const int zs = (DIR > 0 ? (-z0 - (ZC - 1)) : z0) + lane;
+#pragma unroll
+    for (int k = 0; k < KR; ++k) {
+      const int rr = wp + NR * k;
+      if (rr < RR) {
+        const float* src = Rp + (off(k) + zs);
+#pragma unroll
+        for (int u = 0; u < UR; ++u) {
+          const int e = lane + 32 * u;
+          if (e < RW) {
+            if constexpr (PK == 1) {
+              cp_async4(&Rs[2 * buf][rr][e], src + 32 * u);
+              cp_async4(&Rs[2 * buf + 1][rr][e], src + 32 * u + 1);
+            } else {
+              cp_async4(&Rs[buf][rr][e], src + 32 * u);
+            }
+          }
         }
-      } else {
-        for (int e = lane; e < RW; e += 32) cp_async4(&Rs[buf][rr][e], src + e);
       }
     }
-    const int q0 = DIR > 0 ? (x0 - 1 - z0 - (ZC - 1)) : (x0 - 1 + z0);
-    for (int rr = wp; rr < NROW; rr += NR) {
-      const float2* src = Mp + (int64_t)clampi(y0 - 1 + rr, 0, H - 1) * a.ldp + q0;
-      for (int e = lane; e < SW; e += 32) cp_async8(&Ms[buf][rr][e], src + e);
+#pragma unroll
+    for (int k = 0; k < KM; ++k) {
+      const int rr = wp + NR * k;
+      if (rr < NROW) {
+        const float2* src = Mp + (off(KR + k) + zs);
+#pragma unroll
+        for (int u = 0; u < UM; ++u) {
+          const int e = lane + 32 * u;
+          if (e < SW) cp_async8(&Ms[buf][rr][e], src + 32 * u);
+        }
+      }
     }
     cp_async_commit();
   };
