@@ -39,7 +39,13 @@ typedef enum {
   MSHBM_ERR_CONFIG = 2,
   MSHBM_ERR_CUDA = 3,
   MSHBM_ERR_NOMEM = 4,
-  MSHBM_ERR_UNSUPPORTED = 5
+  MSHBM_ERR_UNSUPPORTED = 5,
+  /* codec errors (formats.py exception classes) */
+  MSHBM_ERR_DECODE = 10,      /* DecodeError */
+  MSHBM_ERR_MALFORMED = 11,   /* MalformedHeaderError */
+  MSHBM_ERR_TRUNCATED = 12,   /* TruncatedPayloadError */
+  MSHBM_ERR_MAXVAL = 13,      /* UnsupportedMaxvalError */
+  MSHBM_ERR_MISSING_KEY = 14  /* MissingKeyError */
 } mshbm_status;
 
 enum { MSHBM_SIGN_MIDDLEBURY = 0, MSHBM_SIGN_PAPER = 1 };
@@ -220,6 +226,43 @@ int mshbm_evaluate(mshbm_ctx* ctx, const double* disparity, const double* gt_val
                    const uint8_t* gt_invalid, int64_t n, double scale,
                    const double* taus, int64_t* counts, double* abs_err_sum,
                    void* stream);
+
+/* ---- wire formats (formats.py:123-278) ---------------- *
+ * Host-side codecs over in-memory file bytes; errors set mshbm_last_error(NULL)
+ * with the reference's messages and return the MSHBM_ERR_* decode codes. */
+typedef struct {
+  int32_t width, height, maxval, channels; /* channels 1 (P2/P5) or 3 (P3/P6) */
+  int32_t ascii;                           /* P2/P3 */
+  int32_t itemsize;                        /* binary bytes per sample (maxval > 255: 2, BE) */
+  int64_t payload_offset;                  /* first payload byte (binary) / token (ASCII) */
+} mshbm_pnm_header;
+
+typedef struct {
+  int32_t width, height;
+  double scale;                            /* < 0 little endian, > 0 big endian */
+  int64_t payload_offset;
+} mshbm_pfm_header;
+
+/* read_pnm header checks (formats.py:123-175) */
+int mshbm_pnm_parse(const uint8_t* buf, int64_t len, mshbm_pnm_header* hdr);
+/* read_pnm samples -> grayscale in [0, 1], fp64 host (formats.py:150-190) */
+int mshbm_pnm_decode(const uint8_t* buf, int64_t len, const mshbm_pnm_header* hdr,
+                     double* gray, int64_t ld);
+/* binary PNM payload -> fp32 grayscale on the device (raw samples cross
+ * PCIe); synchronises `stream` to report out-of-range samples */
+int mshbm_pnm_upload(const uint8_t* buf, int64_t len, const mshbm_pnm_header* hdr,
+                     float* d_gray, int64_t ld, void* stream);
+/* read_pfm (formats.py:193-232): header, then rows flipped to top-down,
+ * non-finite samples -> NaN values and invalid = 1 */
+int mshbm_pfm_parse(const uint8_t* buf, int64_t len, mshbm_pfm_header* hdr);
+int mshbm_pfm_decode(const uint8_t* buf, int64_t len, const mshbm_pfm_header* hdr,
+                     double* values, uint8_t* invalid, int64_t ld);
+/* write_pfm / write_pgm (formats.py:235-278): return the encoded size in
+ * bytes (writing only when cap suffices), or -MSHBM_ERR_VALUE */
+int64_t mshbm_pfm_encode(const double* values, int32_t h, int32_t w, int64_t ld, double scale,
+                         uint8_t* out, int64_t cap);
+int64_t mshbm_pgm_encode(const double* values, int32_t h, int32_t w, int64_t ld,
+                         int32_t maxval, double scale_max, uint8_t* out, int64_t cap);
 
 /* ---- diagnostics ------------------------------------------------------- */
 /* FP32 FFMA throughput of `device` (8 CTAs/SM x 256 threads, 8 independent

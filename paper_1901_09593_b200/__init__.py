@@ -3,8 +3,9 @@ hot path (``/root/reference/pkg/src/pyrstereo``: pyramid, cost engine,
 matcher).  ``import paper_1901_09593_b200 as pyrstereo`` exposes the same
 names for the disparity path; the work runs in libmshbm.so (sm_100a CUDA)
 through the C ABI in include/mshbm.h.  The naive full-search baseline and
-scoring (``baseline_bm``, ``evaluate``) also run on the GPU; codecs and the
-CLI are out of scope.
+scoring (``baseline_bm``, ``evaluate``) also run on the GPU, and the wire
+formats (PGM/PPM/PFM, calib.txt) are native codecs with a device upload
+path; the CLI is out of scope.
 """
 
 from .matcher import (
@@ -49,6 +50,21 @@ from .zncc import (
 
 from . import sharding  # noqa: E402
 from .synthetic import interior_mask, shifted_pair  # noqa: E402
+from .formats import (  # noqa: E402
+    CalibInfo,
+    DecodeError,
+    MalformedHeaderError,
+    MissingKeyError,
+    TruncatedPayloadError,
+    UnsupportedMaxvalError,
+    load_pnm_device,
+    read_calib,
+    read_pfm,
+    read_pnm,
+    write_disparity_pfm,
+    write_pfm,
+    write_pgm,
+)
 from .scoring import (  # noqa: E402
     BAD_THRESHOLDS,
     ComparisonSummary,
@@ -71,5 +87,7 @@ __all__ = [
     "run_pipeline", "run_pipeline_band", "run_pipeline_device", "select_with_prior", "selective_median",
     "upsample_prior", "zncc", "BAD_THRESHOLDS", "ComparisonSummary", "EvalReport",
     "GroundTruthDisparity", "baseline_bm", "compare", "evaluate", "interior_mask",
-    "shifted_pair",
+    "shifted_pair", "CalibInfo", "DecodeError", "MalformedHeaderError", "MissingKeyError",
+    "TruncatedPayloadError", "UnsupportedMaxvalError", "load_pnm_device", "read_calib",
+    "read_pfm", "read_pnm", "write_disparity_pfm", "write_pfm", "write_pgm",
 ]

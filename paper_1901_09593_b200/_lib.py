@@ -22,6 +22,24 @@ FLAG_TIMING = 1
 FLAG_NO_GRAPH = 2
 
 
+MSHBM_ERR_DECODE = 10
+MSHBM_ERR_MALFORMED = 11
+MSHBM_ERR_TRUNCATED = 12
+MSHBM_ERR_MAXVAL = 13
+MSHBM_ERR_MISSING_KEY = 14
+
+
+class PnmHeader(C.Structure):
+    _fields_ = [("width", C.c_int32), ("height", C.c_int32), ("maxval", C.c_int32),
+                ("channels", C.c_int32), ("ascii", C.c_int32), ("itemsize", C.c_int32),
+                ("payload_offset", C.c_int64)]
+
+
+class PfmHeader(C.Structure):
+    _fields_ = [("width", C.c_int32), ("height", C.c_int32), ("scale", C.c_double),
+                ("payload_offset", C.c_int64)]
+
+
 class Config(C.Structure):
     _fields_ = [("d_max", C.c_int32), ("levels", C.c_int32), ("block", C.c_int32),
                 ("radius", C.c_int32), ("alpha", C.c_double), ("beta", C.c_double),
@@ -76,6 +94,13 @@ SIGNATURES = {
     "mshbm_refine_level": (C.c_int, [P, P, P, D, P, P, P, P]),
     "mshbm_selective_median": (C.c_int, [P, P, P, I32, I32, D, P, P, P]),
     "mshbm_upsample_prior": (C.c_int, [P, P, P, I32, I32, I32, I32, P, P, P]),
+    "mshbm_pnm_parse": (C.c_int, [P, I64, C.POINTER(PnmHeader)]),
+    "mshbm_pnm_decode": (C.c_int, [P, I64, C.POINTER(PnmHeader), P, I64]),
+    "mshbm_pnm_upload": (C.c_int, [P, I64, C.POINTER(PnmHeader), P, I64, P]),
+    "mshbm_pfm_parse": (C.c_int, [P, I64, C.POINTER(PfmHeader)]),
+    "mshbm_pfm_decode": (C.c_int, [P, I64, C.POINTER(PfmHeader), P, P, I64]),
+    "mshbm_pfm_encode": (I64, [P, I32, I32, I64, D, P, I64]),
+    "mshbm_pgm_encode": (I64, [P, I32, I32, I64, I32, D, P, I64]),
     "mshbm_evaluate": (C.c_int, [P, P, P, P, I64, D, C.POINTER(D), C.POINTER(I64), C.POINTER(D),
                                  P]),
     "mshbm_probe_fp32_peak": (C.c_int, [C.c_int, C.c_int, C.POINTER(D), C.POINTER(D)]),

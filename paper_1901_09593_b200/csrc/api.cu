@@ -21,6 +21,15 @@ namespace {
 
 thread_local std::string g_err;
 
+}  // namespace
+
+namespace mshbm {
+// error text for calls without a context (codecs, create)
+void set_global_error(const std::string& msg) { g_err = msg; }
+}  // namespace mshbm
+
+namespace {
+
 int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
 
 struct LevelBuf {
@@ -529,6 +538,11 @@ const char* mshbm_status_string(int s) {
     case MSHBM_ERR_CUDA: return "cuda error";
     case MSHBM_ERR_NOMEM: return "out of memory";
     case MSHBM_ERR_UNSUPPORTED: return "unsupported";
+    case MSHBM_ERR_DECODE: return "decode error";
+    case MSHBM_ERR_MALFORMED: return "malformed header";
+    case MSHBM_ERR_TRUNCATED: return "truncated payload";
+    case MSHBM_ERR_MAXVAL: return "unsupported maxval";
+    case MSHBM_ERR_MISSING_KEY: return "missing key";
     default: return "unknown";
   }
 }

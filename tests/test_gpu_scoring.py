@@ -200,3 +200,37 @@ def test_hierarchy_vs_baseline_on_easy_pairs(gpu):
     s = gpu.compare(ours, base)
     assert s.eval_ratio is not None and s.eval_ratio < 0.25
     assert s.deltas["avg_abs_err"] <= 0.1
+
+
+# ---------------------------------------------------------------- codecs
+def test_pnm_device_upload_matches_host_decode(gpu, gold, tmp_path):
+    import torch
+    g = np.load(os.path.join(GOLDEN, "formats.npz"))
+    for name in ("p5", "p6_16", "p6_8", "pgm16", "p2"):
+        p = tmp_path / name
+        p.write_bytes(bytes(g[f"file_{name}"]))
+        dev = gpu.load_pnm_device(p)
+        assert dev.is_cuda and dev.dtype == torch.float32
+        ref = g[f"dec_{name}"].astype(np.float32)
+        np.testing.assert_allclose(dev.cpu().numpy(), ref, rtol=0, atol=1e-7)
+    bad = tmp_path / "bad.pgm"
+    bad.write_bytes(b"P5\n2 2\n100\n" + bytes([0, 50, 100, 255]))
+    with pytest.raises(gpu.DecodeError):
+        gpu.load_pnm_device(bad)
+
+
+def test_pipeline_from_pgm_files(gpu, tmp_path):
+    """File -> device decode -> pipeline -> PFM, against the host-array path."""
+    left, right = gpu.shifted_pair(96, 128, 6, np.random.default_rng(8), cutoff=0.1)
+    gpu.write_pgm(left, tmp_path / "l.pgm", maxval=65535)
+    gpu.write_pgm(right, tmp_path / "r.pgm", maxval=65535)
+    cfg = gpu.MatchConfig(d_max=16, levels=2, block=5)
+    lh, rh = gpu.read_pnm(tmp_path / "l.pgm"), gpu.read_pnm(tmp_path / "r.pgm")
+    d_host, c_host, _ = gpu.run_pipeline(lh, rh, cfg)
+    ld, rd = gpu.load_pnm_device(tmp_path / "l.pgm"), gpu.load_pnm_device(tmp_path / "r.pgm")
+    d_dev, c_dev, _ = gpu.run_pipeline_device(ld, rd, cfg)
+    np.testing.assert_array_equal(d_dev.cpu().numpy().astype(np.float64), d_host)
+    np.testing.assert_array_equal(c_dev.cpu().numpy().astype(np.float64), c_host)
+    gpu.write_disparity_pfm(d_dev, tmp_path / "d.pfm")
+    back = gpu.read_pfm(tmp_path / "d.pfm")
+    np.testing.assert_array_equal(back.values, d_host)

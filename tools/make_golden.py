@@ -273,12 +273,89 @@ def scoring_cases():
     save("scoring.npz", **out)
 
 
+def formats_cases():
+    """formats.py codecs: files written by the reference writers and
+    hand-built PNM variants, with the reference readers' decoded arrays;
+    malformed inputs with the reference's exception class."""
+    import tempfile
+    from pyrstereo import formats as F
+    out = {}
+    tmp = tempfile.mkdtemp()
+    rng = np.random.default_rng(41)
+    files = {}
+    v = rng.random((9, 13))
+    v[2, 3] = np.nan
+    for name, kw in [("pfm_le", dict(scale=-1.0)), ("pfm_be", dict(scale=1.0)),
+                     ("pfm_s2", dict(scale=-2.5))]:
+        F.write_pfm(v, os.path.join(tmp, name), **kw)
+    dsp = rng.uniform(0, 70, (11, 6))
+    dsp[0, 0] = np.nan
+    dsp[1, 1] = np.inf
+    dsp[2, 2] = -5.0
+    dsp[3, 3] = 1e9
+    F.write_pgm(v, os.path.join(tmp, "pgm8"))
+    F.write_pgm(dsp, os.path.join(tmp, "pgm_preview"), scale_max=70.0)
+    F.write_pgm(v, os.path.join(tmp, "pgm16"), maxval=4095)
+    F.write_pgm(np.array([[0.5 / 255, 1.5 / 255, 2.5 / 255, 253.5 / 255]]),
+                os.path.join(tmp, "pgm_half"))
+    for name in ("pfm_le", "pfm_be", "pfm_s2", "pgm8", "pgm_preview", "pgm16", "pgm_half"):
+        files[name] = open(os.path.join(tmp, name), "rb").read()
+    img = rng.integers(0, 256, (7, 10))
+    rgb = rng.integers(0, 1024, (5, 6, 3))
+    files["p5"] = b"P5\n# comment\n10 7\n255\n" + img.astype("u1").tobytes()
+    files["p2"] = (b"P2\n10 7 255\n" + " ".join(str(x) for x in img.ravel()).encode() + b"\n")
+    files["p6_16"] = b"P6 6 5\n1023\n" + rgb.astype(">u2").tobytes()
+    files["p3"] = (b"P3\n6 5\n# c\n1023\n" + " ".join(str(x) for x in rgb.ravel()).encode())
+    files["p6_8"] = b"P6\n6 5\n255\n" + (rgb % 256).astype("u1").tobytes()
+    for name, data in files.items():
+        out[f"file_{name}"] = np.frombuffer(data, dtype=np.uint8)
+        path = os.path.join(tmp, name)
+        open(path, "wb").write(data)
+        if name.startswith("pfm"):
+            g = F.read_pfm(path)
+            out[f"dec_{name}"] = g.values
+            out[f"inv_{name}"] = g.invalid
+        else:
+            out[f"dec_{name}"] = F.read_pnm(path)
+    out["src_v"] = v
+    out["src_dsp"] = dsp
+    bad = [b"P7\n2 2\n255\n" + bytes(4), b"P5\n2 x\n255\n" + bytes(4),
+           b"P5\n2 2\n255\n" + bytes(3), b"P2\n2 2\n255\n1 2 3\n",
+           b"P5\n2 2\n0\n" + bytes(4), b"P5\n2 2\n70000\n" + bytes(16), b"P5\n2 2\n255",
+           b"P2\n2 2\n100\n1 2 3 101\n", b"P5\n2 2\n100\n" + bytes([0, 50, 100, 255]),
+           b"P5\n0 2\n255\n" + bytes(4), b"P2\n2 2\n9\n1 x 3 4\n", b"P5 2 2 255" + bytes(4),
+           b"", b"# only a comment\n",
+           b"PF\n1 1\n-1.0\n" + bytes(12), b"Pf\n1 1\n0.0\n" + bytes(4),
+           b"Pf\n2 2\n-1.0\n" + bytes(8), b"Pf\n2 2\nabc\n" + bytes(16),
+           b"Pf\n-2 2\n-1.0\n" + bytes(16), b"Pf\n1 1\n-1.0" + bytes(4)]
+    kinds, msgs = [], []
+    for k, data in enumerate(bad):
+        path = os.path.join(tmp, f"bad{k}")
+        open(path, "wb").write(data)
+        reader = F.read_pfm if data.startswith(b"P") and data[1:2] in (b"f", b"F") else F.read_pnm
+        try:
+            reader(path)
+            kinds.append("none")
+            msgs.append("")
+        except Exception as e:   # noqa: BLE001
+            kinds.append(type(e).__name__)
+            msgs.append(str(e))
+        out[f"bad_{k}"] = np.frombuffer(data, dtype=np.uint8)
+    out["bad_kind"] = np.array(kinds)
+    out["bad_msg"] = np.array(msgs)
+    save("formats.npz", **out)
+
+
 def main():
     os.makedirs(OUT, exist_ok=True)
     if sys.argv[1:] == ["scoring"]:
         scoring_cases()
         return
+    if sys.argv[1:] == ["formats"]:
+        formats_cases()
+        return
     scoring_cases()
+    formats_cases()
     stage_cases()
     rng = np.random.default_rng(16)
     left, right = ref.shifted_pair(64, 64, 6, rng, cutoff=0.05)
