@@ -9,6 +9,7 @@ import glob
 import os
 import subprocess
 import sys
+from concurrent.futures import ThreadPoolExecutor
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
@@ -43,13 +44,17 @@ def build(force: bool = False, verbose: bool = False) -> str:
     """Compile every .cu under csrc/ into libmshbm.so (sm_100a)."""
     if not force and not _stale():
         return LIB
-    objs = []
-    logs = []
-    for src in sources():
+    def compile_one(src):
         obj = os.path.join(CSRC, os.path.basename(src)[:-3] + ".o")
         cmd = [nvcc(), *ARCH, *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"),
                "-dc", src, "-o", obj]
-        r = subprocess.run(cmd, capture_output=True, text=True)
+        return src, obj, subprocess.run(cmd, capture_output=True, text=True)
+
+    # one nvcc per translation unit, in parallel (sweep2.cu dominates)
+    with ThreadPoolExecutor(max_workers=max(1, min(len(sources()), os.cpu_count() or 1))) as ex:
+        results = list(ex.map(compile_one, sources()))
+    objs, logs = [], []
+    for src, obj, r in results:
         logs.append(r.stdout + r.stderr)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed for {src}:\n{r.stdout}\n{r.stderr}")
