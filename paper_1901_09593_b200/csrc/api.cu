@@ -39,6 +39,8 @@ struct LevelBuf {
   double* R = nullptr;
   float* muR = nullptr;
   float* isR = nullptr;
+  float* muL = nullptr;     // left window statistics (sweep4 levels, b >= 5)
+  float* isL = nullptr;
   int* wc = nullptr;
   int16_t* dsel = nullptr;
   int16_t* dmed = nullptr;
@@ -189,6 +191,10 @@ void carve(Plan& p, Carver& cv) {
     l.R = cv.take<double>(n);
     l.muR = cv.take<float>(n);
     l.isR = cv.take<float>(n);
+    if (l.b >= 5) {
+      l.muL = cv.take<float>(n);
+      l.isL = cv.take<float>(n);
+    }
     l.wc = cv.take<int>(n);
     l.dsel = cv.take<int16_t>(n);
     l.dmed = cv.take<int16_t>(n);
@@ -289,8 +295,12 @@ int enqueue(mshbm_ctx* ctx, Plan& p, cudaStream_t s, std::vector<StageEvents>* t
     cudaStream_t t = (fork && k < p.K) ? side : s;
     CK(launch_stats_f32(l.R, l.h, l.w, l.ld, l.b, cfg.sigma_eps, l.muR, l.isR, l.ld, t));
     CK(launch_prep_staging(l.R, l.ld, l.muR, l.isR, l.ld, l.h, l.w, l.pc, l.Rp, l.Mp, l.ldp, t));
-    if (fork && k < p.K) CK(cudaEventRecord(evs[k], side));
     n += 2;
+    if (l.muL) {
+      CK(launch_stats_f32(l.L, l.h, l.w, l.ld, l.b, cfg.sigma_eps, l.muL, l.isL, l.ld, t));
+      ++n;
+    }
+    if (fork && k < p.K) CK(cudaEventRecord(evs[k], side));
   }
   for (int k = p.K; k >= 0; --k) {
     LevelBuf& l = p.lv[k];
@@ -313,6 +323,7 @@ int enqueue(mshbm_ctx* ctx, Plan& p, cudaStream_t s, std::vector<StageEvents>* t
     SweepArgs a{};
     a.L = l.L; a.R = l.R; a.ld = l.ld;
     a.muR = l.muR; a.isR = l.isR; a.lds = l.ld;
+    a.muL = l.muL; a.isL = l.isL;
     a.H = l.h; a.W = l.w; a.d = l.d; a.block = l.b; a.dir = dir;
     a.sigma_eps = cfg.sigma_eps;
     a.wc = k < p.K ? l.wc : nullptr; a.ldw = l.ld; a.radius = cfg.radius;

@@ -26,6 +26,8 @@ struct SweepArgs {
   const float* muR;     // box mean of R (fp32)
   const float* isR;     // 1/sigma_R, 0 where degenerate (fp32)
   int64_t lds;
+  const float* muL;     // box mean / 1/sigma of L (stride lds); sweep4 only
+  const float* isL;
   int H, W, d, block, dir;   // dir: +1 middlebury (q = j - z), -1 paper
   double sigma_eps;
   const int* wc;        // window centre per pixel or kWcNone; nullptr = none
@@ -56,6 +58,9 @@ bool sweep2_supported(int b);
 bool sweep3_supported(int b);
 cudaError_t launch_sweep3(const SweepArgs& a, cudaStream_t s);
 cudaError_t launch_sweep2(const SweepArgs& a, cudaStream_t s);
+// disparities-across-lanes variant (sweep4.cu): pipeline mode, b in {5,7,9,11}
+bool sweep4_supported(const SweepArgs& a);
+cudaError_t launch_sweep4(const SweepArgs& a, cudaStream_t s);
 
 // Column margin of the padded staging arrays for search bound d, block b.
 inline int staging_margin(int d, int b) { return (d + 16 + b + 40 + 3) / 4 * 4; }

@@ -471,6 +471,12 @@ cudaError_t launch_sweep(const SweepArgs& a, cudaStream_t s, int* n_launch) {
     const char* v = getenv("MSHBM_SWEEP_IMPL");   // 1 = one pixel per thread
     impl = v ? atoi(v) : 2;
   }
+  static int use4 = -1;
+  if (use4 < 0) {
+    const char* v = getenv("MSHBM_SWEEP4");   // 0 = keep sweep2 at b >= 5
+    use4 = v ? atoi(v) : 1;
+  }
+  if (use4 && impl >= 2 && sweep4_supported(a)) return launch_sweep4(a, s);
   if (impl == 3 && sweep3_supported(a.block)) return launch_sweep3(a, s);
   if (impl >= 2 && sweep2_supported(a.block)) return launch_sweep2(a, s);
   return a.dir > 0 ? launch_dir<1>(a, s) : launch_dir<-1>(a, s);

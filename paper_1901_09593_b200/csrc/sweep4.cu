@@ -1,0 +1,470 @@
+// Dense fused ZNCC sweep with the disparities across lanes (level 0, b >= 5).
+//
+// sweep2 gives every thread a pixel pair and loops over z, so each pixel pays
+// its own b x b cross-sum (b^2 + b + 1 FMAs per two pixels).  Here lane l of
+// warp w owns one disparity z = zp + 32 w + l for a whole CTA tile of TW x TH
+// output pixels and streams the tile's rows top to bottom.  Window sums then
+// become separable sliding sums held in registers:
+//   V[c]  = sum over the b window rows of L'(r, c) * R'(r, c -+ z)   (per tile column)
+//           slid one row per step: + new row product - old row product
+//   S[u]  = sum of V over the b columns of cost column u            (sliding)
+// about 2 FMAs + 2 adds per (pixel, z) instead of ~b^2 / 2.  L' = L - cL with
+// a per-CTA constant cL and R' = R - c (per-level constant, prep_staging);
+// each pixel's window is re-centred exactly with its own sum of L':
+//   sum (L' - mean L')(R' ) = S - (sum L') * (muR(q) - c).
+// Winner-take-all runs across lanes: the half-range cost c' = sat(c/2 + 1/2)
+// (as in sweep2) + 1 lies in [1, 2], so its float bits are monotone and fit
+// 24 bits; key = (bits - 0x3F800000 + 1) << 5 | (31 - lane) and one REDUX.MAX
+// gives the warp's first maximum (smallest z on ties).  Per pixel, the warps'
+// winners meet in a 64-bit shared-memory atomicMax keyed (value, ~z).  The
+// 3x3-summed refinement cost is a sliding 3-row / 3-column sum of c' in
+// registers, reduced the same way.  The prior window (trusted pixels) masks
+// the keys of lanes outside [c - r, c + r]; untrusted pixels use [0, d].
+//
+// Reference semantics: matcher.py:184-193 (full search), 263-320 (prior
+// window), 196-233 (3x3-summed refinement); zncc.py:271-287 (cost).
+#include <stdlib.h>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace mshbm {
+
+namespace {
+
+constexpr unsigned kFull = 0xffffffffu;
+constexpr int kTW = 16;          // output columns per CTA
+constexpr int kNWMax = 8;        // warps (x 32 disparities) per CTA and pass
+
+__device__ __forceinline__ float fma_sat(float a, float b, float c) {
+  float r;
+  asm("fma.rn.sat.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+
+// ---- mbarrier + 1-D bulk copies (TMA engine) for the row staging
+__device__ __forceinline__ unsigned smem_addr(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_addr(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes,
+                                         unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(bar))
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// Shared-memory layout (runtime TH, warps per pass and key slots).
+template <int B>
+struct S4Layout {
+  static constexpr int NV = kTW + B + 1;        // V columns (TW + 2 cost columns + b - 1)
+  static constexpr int NVP = (NV + 3) & ~3;     // row pitch (float4 broadcast loads)
+  static constexpr int NC = kTW + 2;            // cost columns (1-pixel halo for 3x3 sums)
+  static constexpr int RB = B + 2;              // R ring rows (b + 1 live + 1 in flight)
+  int th, rwp, mwp, nzw;
+  size_t o_bar, o_lt, o_pp, o_wn, o_rr, o_mr, o_sk, o_rk, bytes;
+  __host__ __device__ S4Layout(int th_, int nw, int nzw_) : th(th_), nzw(nzw_) {
+    // ring rows start 16-byte aligned in global memory: up to 3 (R) / 1 (Mp)
+    // extra leading elements, and the copy is rounded up to 16 bytes
+    rwp = (NV + 32 * nw - 1 + 3 + 3 + 3) & ~3;
+    mwp = (NC + 32 * nw - 1 + 1 + 1 + 1) & ~1;
+    size_t o = 0;
+    o_bar = o; o += 16;
+    o_pp = o; o += sizeof(float4) * (th + 2) * (NC / 2);
+    o_wn = o; o += sizeof(int2) * th * kTW;
+    o_mr = o; o += sizeof(float2) * 2 * mwp;
+    o = (o + 15) & ~(size_t)15;
+    o_lt = o; o += sizeof(float) * (th + B + 1) * NVP;
+    o_rr = o; o += sizeof(float) * RB * rwp;
+    o = (o + 15) & ~(size_t)15;
+    o_sk = o; o += sizeof(unsigned) * nzw * th * kTW;
+    o_rk = o; o += sizeof(unsigned) * nzw * th * kTW;
+    bytes = o;
+  }
+};
+
+// One row step: cost row k (image row y0 - 1 + k).  Xin = 3-sums of row
+// k - 1, Xout <- 3-sums of row k, Y = 3-sums of rows k-2 + k-1 on entry and
+// rows k-1 + k on exit.  Lane 0 stores the warp's winner key per pixel:
+// selection for output row k - 1 into sk, refinement for row k - 2 into rk.
+template <int B>
+__device__ __forceinline__ void row_step(
+    const int k, const int th, float (&V)[S4Layout<B>::NV], const float (&Xin)[kTW],
+    float (&Xout)[kTW], float (&Y)[kTW], const float4* __restrict__ Pp,
+    const int4* __restrict__ Wn, const float2* __restrict__ mrow, const int z,
+    const float half, const unsigned laneK, const bool lane0, unsigned* __restrict__ sk,
+    unsigned* __restrict__ rk) {
+  using SL = S4Layout<B>;
+  constexpr int NC = SL::NC;
+  // horizontal window sums S[u] = V[u] + ... + V[u + B - 1] (sliding)
+  float cp[NC];
+  {
+    float acc = 0.f;
+#pragma unroll
+    for (int c = 0; c < B; ++c) acc += V[c];
+    cp[0] = acc;
+#pragma unroll
+    for (int u = 1; u < NC; ++u) {
+      acc = (acc + V[u + B - 1]) - V[u - 1];
+      cp[u] = acc;
+    }
+  }
+  // half-range cost c' = sat((S - sumL' * (muR(q) - c)) * kL * 0.5/sigma_R + 1/2);
+  // NaN scale (degenerate or out-of-image windows, right centre outside the
+  // image) saturates to 0, i.e. c = -1; out-of-image pixels read 0 in 3x3
+  // sums.  Lanes with z > d use half = -1e30, so their c' is 0 as well: they
+  // never beat a smaller z (ties go to the smaller z) and need no mask.
+  const float4* prow = Pp + k * (NC / 2);
+#pragma unroll
+  for (int u2 = 0; u2 < NC / 2; ++u2) {
+    const float4 pp = prow[u2];   // (sumL', kL) of cost columns 2 u2 and 2 u2 + 1
+    const float2 m0 = mrow[2 * u2], m1 = mrow[2 * u2 + 1];
+    cp[2 * u2] = fma_sat(fmaf(-pp.x, m0.x, cp[2 * u2]) * pp.y, m0.y, half);
+    cp[2 * u2 + 1] = fma_sat(fmaf(-pp.z, m1.x, cp[2 * u2 + 1]) * pp.w, m1.y, half);
+  }
+  // selection winner-take-all for output row k - 1: keys of lanes outside
+  // the pixel's window [lo, lo + span] are 0
+  if (k >= 1 && k <= th) {
+    const int4* wrow = Wn + (k - 1) * (kTW / 2);
+#pragma unroll
+    for (int p2 = 0; p2 < kTW / 2; ++p2) {
+      const int4 win = wrow[p2];   // (lo, span) of pixels 2 p2 and 2 p2 + 1
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int p = 2 * p2 + h;
+        const int lo = h ? win.z : win.x, span = h ? win.w : win.y;
+        const unsigned key = (unsigned)(z - lo) <= (unsigned)span
+                                 ? (__float_as_uint(cp[p + 1] + 1.0f) << 5) + laneK
+                                 : 0u;
+        const unsigned r = __reduce_max_sync(kFull, key);
+        if (lane0) sk[(k - 1) * kTW + p] = r;
+      }
+    }
+  }
+  // 3x3 sums: horizontal 3-sums of this row, vertical with the two rows above
+#pragma unroll
+  for (int p = 0; p < kTW; ++p) Xout[p] = (cp[p] + cp[p + 1]) + cp[p + 2];
+  if (k >= 2) {
+#pragma unroll
+    for (int p = 0; p < kTW; ++p) {
+      const float n = Y[p] + Xout[p];
+      const unsigned key = (__float_as_uint(fmaf(n, 0.0625f, 1.0f)) << 5) + laneK;
+      const unsigned r = __reduce_max_sync(kFull, key);
+      if (lane0) rk[(k - 2) * kTW + p] = r;
+    }
+  }
+#pragma unroll
+  for (int p = 0; p < kTW; ++p) Y[p] = Xin[p] + Xout[p];
+}
+
+template <int B, int DIR>
+__global__ void __launch_bounds__(kNWMax * 32, 2) sweep4_kernel(const SweepArgs a, const int th) {
+  using SL = S4Layout<B>;
+  constexpr int H2 = B / 2, NV = SL::NV, NVP = SL::NVP, NC = SL::NC, RB = SL::RB;
+  extern __shared__ float4 smem4[];
+  char* smem = reinterpret_cast<char*>(smem4);
+  const int nw = blockDim.x >> 5;
+  const int d = a.d;
+  const int nslot = ((d + 32 * nw) / (32 * nw)) * nw;   // passes x warps
+  const SL lay(th, nw, nslot);
+  unsigned long long* bar = reinterpret_cast<unsigned long long*>(smem + lay.o_bar);
+  unsigned* sK = reinterpret_cast<unsigned*>(smem + lay.o_sk);
+  unsigned* rK = reinterpret_cast<unsigned*>(smem + lay.o_rk);
+  float4* Pp = reinterpret_cast<float4*>(smem + lay.o_pp);
+  int2* Wn = reinterpret_cast<int2*>(smem + lay.o_wn);
+  float2* Mr = reinterpret_cast<float2*>(smem + lay.o_mr);
+  float* Lt = reinterpret_cast<float*>(smem + lay.o_lt);
+  float* Rr = reinterpret_cast<float*>(smem + lay.o_rr);
+
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int lane = tid & 31, wp = tid >> 5;
+  const int x0 = blockIdx.x * kTW;
+  const int y0 = a.rows.lo + blockIdx.y * th;
+  const int H = a.H, W = a.W;
+  const float qnan = __int_as_float(0x7fc00000);
+
+  // ---- prologue: winner slots, left tile L' = L - cL, window bounds
+  if (tid == 0) mbar_init(bar, 1);
+  for (int t = tid; t < nslot * th * kTW; t += nt) sK[t] = 0u, rK[t] = 0u;
+  const double cL = (double)a.muL[(int64_t)clampi(y0 + th / 2, 0, H - 1) * a.lds +
+                                  clampi(x0 + kTW / 2, 0, W - 1)];
+  for (int t = tid; t < (th + B + 1) * NV; t += nt) {
+    const int rr = t / NV, c = t - rr * NV;
+    const int y = clampi(y0 - 1 - H2 + rr, 0, H - 1), x = clampi(x0 - 1 - H2 + c, 0, W - 1);
+    Lt[rr * NVP + c] = (float)(a.L[(int64_t)y * a.ld + x] - cL);
+  }
+  for (int t = tid; t < th * kTW; t += nt) {
+    const int o = t / kTW, p = t - o * kTW;
+    const int y = y0 + o, x = x0 + p;
+    int2 win = make_int2(0, d);   // (lo, span): untrusted = the full range
+    if (a.wc != nullptr && y < H && x < W) {
+      const int c = a.wc[(int64_t)y * a.ldw + x];
+      if (c != kWcNone) {
+        const int lo = max(c - a.radius, 0);
+        win = make_int2(lo, min(c + a.radius, d) - lo);
+      }
+    }
+    Wn[t] = win;
+  }
+  __syncthreads();
+  // per cost pixel: the sum of L' over its window (fp64 of the fp32 values,
+  // so the centring cancels the rounding of L') and kL = 1/(b^2 sigma_L)
+  for (int t = tid; t < (th + 2) * NC; t += nt) {
+    const int k = t / NC, u = t - k * NC;
+    const int y = y0 - 1 + k, x = x0 - 1 + u;
+    double s = 0.0;
+#pragma unroll
+    for (int r = 0; r < B; ++r) {
+      const float* lr = Lt + (k + r) * NVP + u;
+#pragma unroll
+      for (int c = 0; c < B; ++c) s += (double)lr[c];
+    }
+    float kL = qnan;
+    if (y >= 0 && y < H && x >= 0 && x < W) {
+      const float is = a.isL[(int64_t)y * a.lds + x];
+      if (is > 0.f) kL = is * (1.0f / (float)(B * B));
+    }
+    float* pf = reinterpret_cast<float*>(Pp) + 2 * t;
+    pf[0] = (float)s;
+    pf[1] = kL;
+  }
+
+  const float* __restrict__ Rp = a.Rp + a.pc;
+  const float2* __restrict__ Mp = a.Mp + a.pc;
+  unsigned phase = 0;
+  for (int zp = 0, pass = 0; zp <= d; zp += 32 * nw, ++pass) {
+    // warps of this pass that hold at least one z <= d
+    const int nwp = min(nw, (d - zp) / 32 + 1);
+    const int zlo = zp + 32 * wp;
+    const int z = zlo + lane;
+    // every z of the warp has its right centre outside the image for every
+    // cost column of the tile: costs are all -1 there, and lower warps hold
+    // smaller z with costs >= -1, so skipping the warp is exact (its key
+    // slots stay 0 = no candidate)
+    const bool active = wp < nwp && (DIR > 0 ? (zlo <= x0 + kTW) : (zlo <= W - x0));
+    const int span = 32 * nwp - 1;
+    // image column of ring element 0 (R ring: tile V columns, Mp ring: cost
+    // columns), moved down to a 16-byte boundary of the padded row
+    int rc0 = DIR > 0 ? (x0 - 1 - H2 - zp - span) : (x0 - 1 - H2 + zp);
+    int mc0 = DIR > 0 ? (x0 - 1 - zp - span) : (x0 - 1 + zp);
+    const int rmis = (a.pc + rc0) & 3, mmis = (a.pc + mc0) & 1;
+    rc0 -= rmis;
+    mc0 -= mmis;
+    const unsigned rbytes = (unsigned)(((NV + span + rmis + 3) & ~3) * sizeof(float));
+    const unsigned mbytes = (unsigned)(((NC + span + mmis + 1) & ~1) * sizeof(float2));
+    // lane base into the rings: element index of column c for this z
+    const int lb = (DIR > 0 ? (span - (z - zp)) : (z - zp)) + rmis;
+    const int mb = (DIR > 0 ? (span - (z - zp)) : (z - zp)) + mmis;
+
+    auto stage_r = [&](int rr) {
+      const int y = clampi(y0 - 1 - H2 + rr, 0, H - 1);
+      bulk_g2s(Rr + (rr % RB) * lay.rwp, Rp + ((int64_t)y * a.ldp + rc0), rbytes, bar);
+    };
+    auto stage_m = [&](int k) {
+      const int y = clampi(y0 - 1 + k, 0, H - 1);
+      bulk_g2s(Mr + (k & 1) * lay.mwp, Mp + ((int64_t)y * a.ldp + mc0), mbytes, bar);
+    };
+    __syncthreads();   // previous pass done with the rings (and the prologue)
+    if (tid == 0) {
+      fence_proxy_async();
+      mbar_expect_tx(bar, (B + 1) * rbytes + mbytes);
+      for (int rr = 0; rr <= B; ++rr) stage_r(rr);
+      stage_m(0);
+    }
+    mbar_wait(bar, phase);
+    phase ^= 1u;
+
+    float V[NV];
+    if (active) {
+#pragma unroll
+      for (int c = 0; c < NV; ++c) V[c] = 0.f;
+#pragma unroll
+      for (int r = 0; r < B; ++r) {
+        const float4* lr = reinterpret_cast<const float4*>(Lt + r * NVP);
+        const float* rrow = Rr + r * lay.rwp + lb;
+#pragma unroll
+        for (int c4 = 0; c4 < NVP / 4; ++c4) {
+          const float4 l4 = lr[c4];
+          const float lv[4] = {l4.x, l4.y, l4.z, l4.w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int c = 4 * c4 + e;
+            if (c < NV) V[c] = fmaf(lv[e], rrow[c], V[c]);
+          }
+        }
+      }
+    }
+    const unsigned laneK = (unsigned)(31 - lane) + 32u - (0x3F800000u << 5);
+    const float half = z <= d ? 0.5f : -1.0e30f;
+    const bool lane0 = lane == 0;
+    unsigned* sk = sK + (pass * nw + wp) * th * kTW;
+    unsigned* rk = rK + (pass * nw + wp) * th * kTW;
+    float X1[kTW], X2[kTW], Y[kTW];
+#pragma unroll
+    for (int p = 0; p < kTW; ++p) X1[p] = 0.f, X2[p] = 0.f, Y[p] = 0.f;
+
+    auto step = [&](int k, float (&Xin)[kTW], float (&Xout)[kTW]) {
+      if (k > 0) {
+        mbar_wait(bar, phase);
+        phase ^= 1u;
+        __syncthreads();   // every warp done with step k - 1 (ring slots reused below)
+      }
+      // prefetch: R row k + B + 1 (slides V at step k + 1), Mp row k + 1
+      if (tid == 0 && k + 1 <= th + 1) {
+        fence_proxy_async();
+        const bool rrow = k + B + 1 <= th + B;
+        mbar_expect_tx(bar, (rrow ? rbytes : 0u) + mbytes);
+        if (rrow) stage_r(k + B + 1);
+        stage_m(k + 1);
+      }
+      if (active) {
+        const float2* mrow = Mr + (k & 1) * lay.mwp + mb;
+        row_step<B>(k, th, V, Xin, Xout, Y, Pp, reinterpret_cast<const int4*>(Wn), mrow, z, half,
+                    laneK, lane0, sk, rk);
+        // slide V down one row: + row k + B, - row k
+        if (k <= th) {
+          const float4* lin = reinterpret_cast<const float4*>(Lt + (k + B) * NVP);
+          const float4* lout = reinterpret_cast<const float4*>(Lt + k * NVP);
+          const float* rin = Rr + ((k + B) % RB) * lay.rwp + lb;
+          const float* rout = Rr + (k % RB) * lay.rwp + lb;
+#pragma unroll
+          for (int c4 = 0; c4 < NVP / 4; ++c4) {
+            const float4 i4 = lin[c4], o4 = lout[c4];
+            const float iv[4] = {i4.x, i4.y, i4.z, i4.w}, ov[4] = {o4.x, o4.y, o4.z, o4.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const int c = 4 * c4 + e;
+              if (c < NV) V[c] = fmaf(iv[e], rin[c], fmaf(-ov[e], rout[c], V[c]));
+            }
+          }
+        }
+      }
+    };
+#pragma unroll 1
+    for (int k = 0; k < th + 2; k += 2) {
+      step(k, X1, X2);
+      step(k + 1, X2, X1);
+    }
+  }
+  __syncthreads();
+
+  // ---- epilogue: merge the warps' winners (lower warp = smaller z first on
+  // ties), then the reference's gates, per output pixel
+  unsigned nlow = 0;
+  for (int t = tid; t < th * kTW; t += nt) {
+    const int o = t / kTW, p = t - o * kTW;
+    const int i = y0 + o, j = x0 + p;
+    if (i >= H || j >= W) continue;
+    unsigned bs = 0u, br = 0u;
+    int zs = -1, nbz = 0;
+    for (int w = 0; w < nslot; ++w) {
+      const unsigned ks = sK[w * th * kTW + t], kr = rK[w * th * kTW + t];
+      if ((ks >> 5) > (bs >> 5)) bs = ks, zs = 32 * w + 31 - (int)(ks & 31u);
+      if ((kr >> 5) > (br >> 5)) br = kr, nbz = 32 * w + 31 - (int)(kr & 31u);
+    }
+    bool trusted = false;
+    int lo = 0;
+    if (a.wc != nullptr) {
+      const int c = a.wc[(int64_t)i * a.ldw + j];
+      if (c != kWcNone) trusted = true, lo = max(c - a.radius, 0);
+    }
+    float cs = -1.f;
+    if (zs >= 0) {
+      const float c2 = __uint_as_float((bs >> 5) - 1u + 0x3F800000u);
+      cs = 2.f * c2 - 3.f;   // c = 2 c' - 1, c' = c2 - 1
+    } else {
+      zs = trusted ? lo : 0;   // window beyond the image: all -1, smallest legal z
+    }
+    const float n1 = __uint_as_float((br >> 5) - 1u + 0x3F800000u);
+    const float nsum = (n1 - 1.0f) * 16.0f;
+    const int members = ((i > 0) + 1 + (i < H - 1)) * ((j > 0) + 1 + (j < W - 1));
+    const float nbc = 2.f * nsum / (float)members - 1.f;
+    const bool low = (double)cs <= a.alpha;
+    const int64_t off = (int64_t)i * a.ldo + j;
+    a.dout[off] = (int16_t)(low ? nbz : zs);
+    a.cout[off] = low ? nbc : cs;
+    a.low[off] = (uint8_t)low;
+    nlow += (low && i >= a.rows.cnt_lo && i < a.rows.cnt_hi) ? 1u : 0u;
+  }
+  const int slot[1] = {kCntRefined};
+  const unsigned long long val[1] = {nlow};
+  const bool mx[1] = {false};
+  block_accumulate<1>(a.counters, slot, val, mx);
+}
+
+int g_th = -1;
+int sweep4_th() {
+  if (g_th < 0) {
+    const char* v = getenv("MSHBM_SWEEP4_TH");
+    g_th = v ? atoi(v) : 32;
+    if (g_th < 2 || (g_th & 1)) g_th = 32;
+  }
+  return g_th;
+}
+
+template <int B, int DIR>
+cudaError_t launch4(const SweepArgs& a, cudaStream_t s) {
+  const int th = sweep4_th();
+  const int nzw = (a.d + 1 + 31) / 32;
+  const int passes = (nzw + kNWMax - 1) / kNWMax;
+  const int nw = (nzw + passes - 1) / passes;
+  const S4Layout<B> lay(th, nw, passes * nw);
+  static size_t configured = 0;
+  if (configured < lay.bytes) {
+    cudaError_t e = cudaFuncSetAttribute(sweep4_kernel<B, DIR>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)lay.bytes);
+    if (e != cudaSuccess) return e;
+    configured = lay.bytes;
+  }
+  // CTA rows on the whole-image grid (row bands bit-identical to whole runs)
+  SweepArgs b = a;
+  b.rows.lo = (a.rows.lo / th) * th;
+  dim3 grid((a.W + kTW - 1) / kTW, (b.rows.hi - b.rows.lo + th - 1) / th);
+  sweep4_kernel<B, DIR><<<grid, 32 * nw, lay.bytes, s>>>(b, th);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+bool sweep4_supported(const SweepArgs& a) {
+  return a.mode == kSweepPipeline && a.muL != nullptr && a.isL != nullptr &&
+         (a.block == 5 || a.block == 7 || a.block == 9 || a.block == 11) && a.d >= 1 &&
+         a.d <= 4095 && a.d <= 32767;
+}
+
+cudaError_t launch_sweep4(const SweepArgs& a, cudaStream_t s) {
+  const bool mb = a.dir > 0;
+  switch (a.block) {
+    case 5: return mb ? launch4<5, 1>(a, s) : launch4<5, -1>(a, s);
+    case 7: return mb ? launch4<7, 1>(a, s) : launch4<7, -1>(a, s);
+    case 9: return mb ? launch4<9, 1>(a, s) : launch4<9, -1>(a, s);
+    case 11: return mb ? launch4<11, 1>(a, s) : launch4<11, -1>(a, s);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace mshbm
