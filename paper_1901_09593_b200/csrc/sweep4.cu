@@ -83,9 +83,9 @@ struct S4Layout {
   static constexpr int NV = kTW + B + 1;        // V columns (TW + 2 cost columns + b - 1)
   static constexpr int NVP = (NV + 3) & ~3;     // row pitch (float4 broadcast loads)
   static constexpr int NC = kTW + 2;            // cost columns (1-pixel halo for 3x3 sums)
-  static constexpr int RB = B + 2;              // R ring rows (b + 1 live + 1 in flight)
+  static constexpr int RB = B + 4;              // R ring rows (b + 2 live + 2 in flight)
   int th, rwp, mwp, nzw;
-  size_t o_bar, o_lt, o_pp, o_wn, o_rr, o_mr, o_sk, o_rk, bytes;
+  size_t o_bar, o_lt, o_pp, o_wn, o_rr, o_mr, o_sk, o_rk, o_hs, bytes;
   __host__ __device__ S4Layout(int th_, int nw, int nzw_) : th(th_), nzw(nzw_) {
     // ring rows start 16-byte aligned in global memory: up to 3 (R) / 1 (Mp)
     // extra leading elements, and the copy is rounded up to 16 bytes
@@ -95,13 +95,15 @@ struct S4Layout {
     o_bar = o; o += 16;
     o_pp = o; o += sizeof(float4) * (th + 2) * (NC / 2);
     o_wn = o; o += sizeof(int2) * th * kTW;
-    o_mr = o; o += sizeof(float2) * 2 * mwp;
+    o_mr = o; o += sizeof(float2) * 4 * mwp;
     o = (o + 15) & ~(size_t)15;
     o_lt = o; o += sizeof(float) * (th + B + 1) * NVP;
     o_rr = o; o += sizeof(float) * RB * rwp;
     o = (o + 15) & ~(size_t)15;
     o_sk = o; o += sizeof(unsigned) * nzw * th * kTW;
     o_rk = o; o += sizeof(unsigned) * nzw * th * kTW;
+    o = (o + 15) & ~(size_t)15;
+    o_hs = o; o += sizeof(double) * (th + B + 1) * NC;   // prologue only
     bytes = o;
   }
 };
@@ -119,17 +121,24 @@ __device__ __forceinline__ void row_step(
     unsigned* __restrict__ rk) {
   using SL = S4Layout<B>;
   constexpr int NC = SL::NC;
-  // horizontal window sums S[u] = V[u] + ... + V[u + B - 1] (sliding)
+  // horizontal window sums S[u] = V[u] + ... + V[u + B - 1]: sliding, as two
+  // independent chains (u < NC/2 from S[0], u >= NC/2 from S[NC/2]) over the
+  // differences D[u] = V[u + B - 1] - V[u - 1], so the dependent FADD chain is
+  // NC/2 deep instead of 2 NC
   float cp[NC];
   {
-    float acc = 0.f;
+    constexpr int M = NC / 2;
+    float a0 = 0.f, a1 = 0.f;
 #pragma unroll
-    for (int c = 0; c < B; ++c) acc += V[c];
-    cp[0] = acc;
+    for (int c = 0; c < B; ++c) a0 += V[c], a1 += V[M + c];
+    cp[0] = a0;
+    cp[M] = a1;
 #pragma unroll
-    for (int u = 1; u < NC; ++u) {
-      acc = (acc + V[u + B - 1]) - V[u - 1];
-      cp[u] = acc;
+    for (int u = 1; u < M; ++u) {
+      a0 += V[u + B - 1] - V[u - 1];
+      a1 += V[M + u + B - 1] - V[M + u - 1];
+      cp[u] = a0;
+      cp[M + u] = a1;
     }
   }
   // half-range cost c' = sat((S - sumL' * (muR(q) - c)) * kL * 0.5/sigma_R + 1/2);
@@ -188,7 +197,12 @@ __global__ void __launch_bounds__(kNWMax * 32, 2) sweep4_kernel(const SweepArgs 
   char* smem = reinterpret_cast<char*>(smem4);
   const int nw = blockDim.x >> 5;
   const int d = a.d;
-  const int nslot = ((d + 32 * nw) / (32 * nw)) * nw;   // passes x warps
+  // d a multiple of 32: the lanes cover z < d and the tail disparity z = d
+  // (which would cost a whole warp with one useful lane) is evaluated once
+  // per tile after the sweep, as a separable box sum
+  const bool tail = (d & 31) == 0;
+  const int nz = tail ? d : d + 1;                          // disparities on lanes
+  const int nslot = ((nz + 32 * nw - 1) / (32 * nw)) * nw;  // passes x warps
   const SL lay(th, nw, nslot);
   unsigned long long* bar = reinterpret_cast<unsigned long long*>(smem + lay.o_bar);
   unsigned* sK = reinterpret_cast<unsigned*>(smem + lay.o_sk);
@@ -230,18 +244,25 @@ __global__ void __launch_bounds__(kNWMax * 32, 2) sweep4_kernel(const SweepArgs 
     Wn[t] = win;
   }
   __syncthreads();
-  // per cost pixel: the sum of L' over its window (fp64 of the fp32 values,
-  // so the centring cancels the rounding of L') and kL = 1/(b^2 sigma_L)
+  // per cost pixel: the sum of L' over its window (fp64 sums of the fp32
+  // values, so the centring cancels the rounding of L'), separable through
+  // per-row horizontal sums, and kL = 1/(b^2 sigma_L)
+  double* Hs = reinterpret_cast<double*>(smem + lay.o_hs);
+  for (int t = tid; t < (th + B + 1) * NC; t += nt) {
+    const int rr = t / NC, u = t - rr * NC;
+    const float* lr = Lt + rr * NVP + u;
+    double s = 0.0;
+#pragma unroll
+    for (int c = 0; c < B; ++c) s += (double)lr[c];
+    Hs[t] = s;
+  }
+  __syncthreads();
   for (int t = tid; t < (th + 2) * NC; t += nt) {
     const int k = t / NC, u = t - k * NC;
     const int y = y0 - 1 + k, x = x0 - 1 + u;
     double s = 0.0;
 #pragma unroll
-    for (int r = 0; r < B; ++r) {
-      const float* lr = Lt + (k + r) * NVP + u;
-#pragma unroll
-      for (int c = 0; c < B; ++c) s += (double)lr[c];
-    }
+    for (int r = 0; r < B; ++r) s += Hs[(k + r) * NC + u];
     float kL = qnan;
     if (y >= 0 && y < H && x >= 0 && x < W) {
       const float is = a.isL[(int64_t)y * a.lds + x];
@@ -255,9 +276,9 @@ __global__ void __launch_bounds__(kNWMax * 32, 2) sweep4_kernel(const SweepArgs 
   const float* __restrict__ Rp = a.Rp + a.pc;
   const float2* __restrict__ Mp = a.Mp + a.pc;
   unsigned phase = 0;
-  for (int zp = 0, pass = 0; zp <= d; zp += 32 * nw, ++pass) {
+  for (int zp = 0, pass = 0; zp < nz; zp += 32 * nw, ++pass) {
     // warps of this pass that hold at least one z <= d
-    const int nwp = min(nw, (d - zp) / 32 + 1);
+    const int nwp = min(nw, (nz - 1 - zp) / 32 + 1);
     const int zlo = zp + 32 * wp;
     const int z = zlo + lane;
     // every z of the warp has its right centre outside the image for every
@@ -285,14 +306,15 @@ __global__ void __launch_bounds__(kNWMax * 32, 2) sweep4_kernel(const SweepArgs 
     };
     auto stage_m = [&](int k) {
       const int y = clampi(y0 - 1 + k, 0, H - 1);
-      bulk_g2s(Mr + (k & 1) * lay.mwp, Mp + ((int64_t)y * a.ldp + mc0), mbytes, bar);
+      bulk_g2s(Mr + (k & 3) * lay.mwp, Mp + ((int64_t)y * a.ldp + mc0), mbytes, bar);
     };
     __syncthreads();   // previous pass done with the rings (and the prologue)
     if (tid == 0) {
       fence_proxy_async();
-      mbar_expect_tx(bar, (B + 1) * rbytes + mbytes);
-      for (int rr = 0; rr <= B; ++rr) stage_r(rr);
+      mbar_expect_tx(bar, (B + 2) * rbytes + 2 * mbytes);
+      for (int rr = 0; rr <= B + 1; ++rr) stage_r(rr);
       stage_m(0);
+      stage_m(1);
     }
     mbar_wait(bar, phase);
     phase ^= 1u;
@@ -318,7 +340,7 @@ __global__ void __launch_bounds__(kNWMax * 32, 2) sweep4_kernel(const SweepArgs 
       }
     }
     const unsigned laneK = (unsigned)(31 - lane) + 32u - (0x3F800000u << 5);
-    const float half = z <= d ? 0.5f : -1.0e30f;
+    const float half = z < nz ? 0.5f : -1.0e30f;
     const bool lane0 = lane == 0;
     unsigned* sk = sK + (pass * nw + wp) * th * kTW;
     unsigned* rk = rK + (pass * nw + wp) * th * kTW;
@@ -326,22 +348,12 @@ __global__ void __launch_bounds__(kNWMax * 32, 2) sweep4_kernel(const SweepArgs 
 #pragma unroll
     for (int p = 0; p < kTW; ++p) X1[p] = 0.f, X2[p] = 0.f, Y[p] = 0.f;
 
+    // Rows are consumed in pairs of steps: one mbarrier wait and one CTA
+    // barrier per pair; the ring holds the pair's b + 2 R rows and 2 Mp rows
+    // plus the next pair's, prefetched by one thread with bulk copies.
     auto step = [&](int k, float (&Xin)[kTW], float (&Xout)[kTW]) {
-      if (k > 0) {
-        mbar_wait(bar, phase);
-        phase ^= 1u;
-        __syncthreads();   // every warp done with step k - 1 (ring slots reused below)
-      }
-      // prefetch: R row k + B + 1 (slides V at step k + 1), Mp row k + 1
-      if (tid == 0 && k + 1 <= th + 1) {
-        fence_proxy_async();
-        const bool rrow = k + B + 1 <= th + B;
-        mbar_expect_tx(bar, (rrow ? rbytes : 0u) + mbytes);
-        if (rrow) stage_r(k + B + 1);
-        stage_m(k + 1);
-      }
       if (active) {
-        const float2* mrow = Mr + (k & 1) * lay.mwp + mb;
+        const float2* mrow = Mr + (k & 3) * lay.mwp + mb;
         row_step<B>(k, th, V, Xin, Xout, Y, Pp, reinterpret_cast<const int4*>(Wn), mrow, z, half,
                     laneK, lane0, sk, rk);
         // slide V down one row: + row k + B, - row k
@@ -365,11 +377,55 @@ __global__ void __launch_bounds__(kNWMax * 32, 2) sweep4_kernel(const SweepArgs 
     };
 #pragma unroll 1
     for (int k = 0; k < th + 2; k += 2) {
+      if (k > 0) {
+        mbar_wait(bar, phase);
+        phase ^= 1u;
+        __syncthreads();   // every warp done with the previous pair (its slots are reused)
+      }
+      if (tid == 0 && k + 2 <= th + 1) {
+        fence_proxy_async();
+        const int nr = (k + B + 2 <= th + B) + (k + B + 3 <= th + B);
+        mbar_expect_tx(bar, nr * rbytes + 2 * mbytes);
+        if (k + B + 2 <= th + B) stage_r(k + B + 2);
+        if (k + B + 3 <= th + B) stage_r(k + B + 3);
+        stage_m(k + 2);
+        stage_m(k + 3);
+      }
       step(k, X1, X2);
       step(k + 1, X2, X1);
     }
   }
   __syncthreads();
+
+  // ---- tail disparity z = d: half-range costs c'(d) of every cost pixel
+  // (TH + 2 rows x TW + 2 columns) into Ct, from row sums Ht of L' x R'
+  float* Ct = reinterpret_cast<float*>(smem + lay.o_hs);
+  float* Ht = Ct + (th + 2) * NC;
+  if (tail) {
+    const int qd = DIR > 0 ? -d : d;   // right column offset of z = d
+    for (int t = tid; t < (th + B + 1) * NC; t += nt) {
+      const int rr = t / NC, u = t - rr * NC;
+      const int y = clampi(y0 - 1 - H2 + rr, 0, H - 1);
+      const float* rrow = Rp + ((int64_t)y * a.ldp + (x0 - 1 - H2 + u + qd));
+      const float* lr = Lt + rr * NVP + u;
+      float acc = 0.f;
+#pragma unroll
+      for (int c = 0; c < B; ++c) acc = fmaf(lr[c], __ldg(rrow + c), acc);
+      Ht[t] = acc;
+    }
+    __syncthreads();
+    for (int t = tid; t < (th + 2) * NC; t += nt) {
+      const int k = t / NC, u = t - k * NC;
+      float S = 0.f;
+#pragma unroll
+      for (int r = 0; r < B; ++r) S += Ht[(k + r) * NC + u];
+      const float* pf = reinterpret_cast<const float*>(Pp) + 2 * t;
+      const int yc = clampi(y0 - 1 + k, 0, H - 1);
+      const float2 m = Mp[(int64_t)yc * a.ldp + (x0 - 1 + u + qd)];
+      Ct[t] = fma_sat(fmaf(-pf[0], m.x, S) * pf[1], m.y, 0.5f);
+    }
+    __syncthreads();
+  }
 
   // ---- epilogue: merge the warps' winners (lower warp = smaller z first on
   // ties), then the reference's gates, per output pixel
@@ -386,18 +442,27 @@ __global__ void __launch_bounds__(kNWMax * 32, 2) sweep4_kernel(const SweepArgs 
       if ((kr >> 5) > (br >> 5)) br = kr, nbz = 32 * w + 31 - (int)(kr & 31u);
     }
     bool trusted = false;
-    int lo = 0;
+    int lo = 0, hi = d;
     if (a.wc != nullptr) {
       const int c = a.wc[(int64_t)i * a.ldw + j];
-      if (c != kWcNone) trusted = true, lo = max(c - a.radius, 0);
+      if (c != kWcNone) trusted = true, lo = max(c - a.radius, 0), hi = min(c + a.radius, d);
     }
-    float cs = -1.f;
-    if (zs >= 0) {
-      const float c2 = __uint_as_float((bs >> 5) - 1u + 0x3F800000u);
-      cs = 2.f * c2 - 3.f;   // c = 2 c' - 1, c' = c2 - 1
-    } else {
-      zs = trusted ? lo : 0;   // window beyond the image: all -1, smallest legal z
+    if (zs < 0) {
+      // no candidate on an active warp: the window lies where every right
+      // centre is outside the image, all -1 (value 1), smallest legal z
+      bs = 1u << 5;
+      zs = trusted ? lo : 0;
     }
+    if (tail) {   // z = d last: it wins only if strictly better
+      const float* ct = Ct + o * NC + p;
+      const unsigned vd = __float_as_uint(ct[NC + 1] + 1.0f) - 0x3F800000u + 1u;
+      if (hi == d && vd > (bs >> 5)) bs = vd << 5, zs = d;
+      const float nsum = (((ct[0] + ct[1]) + ct[2]) + ((ct[NC] + ct[NC + 1]) + ct[NC + 2])) +
+                         ((ct[2 * NC] + ct[2 * NC + 1]) + ct[2 * NC + 2]);
+      const unsigned vn = __float_as_uint(fmaf(nsum, 0.0625f, 1.0f)) - 0x3F800000u + 1u;
+      if (vn > (br >> 5)) br = vn << 5, nbz = d;
+    }
+    const float cs = 2.f * __uint_as_float((bs >> 5) - 1u + 0x3F800000u) - 3.f;  // c = 2 c' - 1
     const float n1 = __uint_as_float((br >> 5) - 1u + 0x3F800000u);
     const float nsum = (n1 - 1.0f) * 16.0f;
     const int members = ((i > 0) + 1 + (i < H - 1)) * ((j > 0) + 1 + (j < W - 1));
@@ -428,7 +493,7 @@ int sweep4_th() {
 template <int B, int DIR>
 cudaError_t launch4(const SweepArgs& a, cudaStream_t s) {
   const int th = sweep4_th();
-  const int nzw = (a.d + 1 + 31) / 32;
+  const int nzw = ((a.d & 31) == 0 ? a.d : a.d + 1 + 31) / 32;   // tail z = d off the lanes
   const int passes = (nzw + kNWMax - 1) / kNWMax;
   const int nw = (nzw + passes - 1) / passes;
   const S4Layout<B> lay(th, nw, passes * nw);
@@ -451,7 +516,9 @@ cudaError_t launch4(const SweepArgs& a, cudaStream_t s) {
 }  // namespace
 
 bool sweep4_supported(const SweepArgs& a) {
-  return a.mode == kSweepPipeline && a.muL != nullptr && a.isL != nullptr &&
+  // small levels (C1's 450 x 375) leave most SMs idle with one-disparity-
+  // per-lane tiles; sweep2's pixel-pair threads are faster there (measured)
+  return (int64_t)a.H * a.W >= 400000 && a.mode == kSweepPipeline && a.muL != nullptr && a.isL != nullptr &&
          (a.block == 5 || a.block == 7 || a.block == 9 || a.block == 11) && a.d >= 1 &&
          a.d <= 4095 && a.d <= 32767;
 }
