@@ -78,12 +78,12 @@ __device__ __forceinline__ void fence_proxy_async() {
 }
 
 // Shared-memory layout (runtime TH, warps per pass and key slots).
-template <int B>
+template <int B, int G = 2>
 struct S4Layout {
   static constexpr int NV = kTW + B + 1;        // V columns (TW + 2 cost columns + b - 1)
   static constexpr int NVP = (NV + 3) & ~3;     // row pitch (float4 broadcast loads)
   static constexpr int NC = kTW + 2;            // cost columns (1-pixel halo for 3x3 sums)
-  static constexpr int RB = B + 4;              // R ring rows (b + 2 live + 2 in flight)
+  static constexpr int RB = B + 2 * G;          // R ring rows (b + G live + G in flight)
   int th, rwp, mwp, nzw;
   size_t o_bar, o_lt, o_pp, o_wn, o_rr, o_mr, o_sk, o_rk, o_hs, bytes;
   __host__ __device__ S4Layout(int th_, int nw, int nzw_) : th(th_), nzw(nzw_) {
@@ -95,7 +95,7 @@ struct S4Layout {
     o_bar = o; o += 16;
     o_pp = o; o += sizeof(float4) * (th + 2) * (NC / 2);
     o_wn = o; o += sizeof(int2) * th * kTW;
-    o_mr = o; o += sizeof(float2) * 4 * mwp;
+    o_mr = o; o += sizeof(float2) * 2 * G * mwp;
     o = (o + 15) & ~(size_t)15;
     o_lt = o; o += sizeof(float) * (th + B + 1) * NVP;
     o_rr = o; o += sizeof(float) * RB * rwp;
@@ -189,9 +189,9 @@ __device__ __forceinline__ void row_step(
   for (int p = 0; p < kTW; ++p) Y[p] = Xin[p] + Xout[p];
 }
 
-template <int B, int DIR>
+template <int B, int DIR, int G>
 __global__ void __launch_bounds__(kNWMax * 32, 2) sweep4_kernel(const SweepArgs a, const int th) {
-  using SL = S4Layout<B>;
+  using SL = S4Layout<B, G>;
   constexpr int H2 = B / 2, NV = SL::NV, NVP = SL::NVP, NC = SL::NC, RB = SL::RB;
   extern __shared__ float4 smem4[];
   char* smem = reinterpret_cast<char*>(smem4);
@@ -306,15 +306,15 @@ __global__ void __launch_bounds__(kNWMax * 32, 2) sweep4_kernel(const SweepArgs 
     };
     auto stage_m = [&](int k) {
       const int y = clampi(y0 - 1 + k, 0, H - 1);
-      bulk_g2s(Mr + (k & 3) * lay.mwp, Mp + ((int64_t)y * a.ldp + mc0), mbytes, bar);
+      bulk_g2s(Mr + (k % (2 * G)) * lay.mwp, Mp + ((int64_t)y * a.ldp + mc0), mbytes, bar);
     };
     __syncthreads();   // previous pass done with the rings (and the prologue)
     if (tid == 0) {
       fence_proxy_async();
-      mbar_expect_tx(bar, (B + 2) * rbytes + 2 * mbytes);
-      for (int rr = 0; rr <= B + 1; ++rr) stage_r(rr);
-      stage_m(0);
-      stage_m(1);
+      const int nr0 = min(B + G, th + B + 1), nm0 = min(G, th + 2);
+      mbar_expect_tx(bar, nr0 * rbytes + nm0 * mbytes);
+      for (int rr = 0; rr < nr0; ++rr) stage_r(rr);
+      for (int k = 0; k < nm0; ++k) stage_m(k);
     }
     mbar_wait(bar, phase);
     phase ^= 1u;
@@ -353,7 +353,7 @@ __global__ void __launch_bounds__(kNWMax * 32, 2) sweep4_kernel(const SweepArgs 
     // plus the next pair's, prefetched by one thread with bulk copies.
     auto step = [&](int k, float (&Xin)[kTW], float (&Xout)[kTW]) {
       if (active) {
-        const float2* mrow = Mr + (k & 3) * lay.mwp + mb;
+        const float2* mrow = Mr + (k % (2 * G)) * lay.mwp + mb;
         row_step<B>(k, th, V, Xin, Xout, Y, Pp, reinterpret_cast<const int4*>(Wn), mrow, z, half,
                     laneK, lane0, sk, rk);
         // slide V down one row: + row k + B, - row k
@@ -376,23 +376,27 @@ __global__ void __launch_bounds__(kNWMax * 32, 2) sweep4_kernel(const SweepArgs 
       }
     };
 #pragma unroll 1
-    for (int k = 0; k < th + 2; k += 2) {
+    for (int k = 0; k < th + 2; k += G) {
       if (k > 0) {
         mbar_wait(bar, phase);
         phase ^= 1u;
-        __syncthreads();   // every warp done with the previous pair (its slots are reused)
+        __syncthreads();   // every warp done with the previous group (its slots are reused)
       }
-      if (tid == 0 && k + 2 <= th + 1) {
+      if (tid == 0 && k + G <= th + 1) {
         fence_proxy_async();
-        const int nr = (k + B + 2 <= th + B) + (k + B + 3 <= th + B);
-        mbar_expect_tx(bar, nr * rbytes + 2 * mbytes);
-        if (k + B + 2 <= th + B) stage_r(k + B + 2);
-        if (k + B + 3 <= th + B) stage_r(k + B + 3);
-        stage_m(k + 2);
-        stage_m(k + 3);
+        const int r0 = k + B + G, r1 = min(k + B + 2 * G, th + B + 1);
+        const int m0 = k + G, m1 = min(k + 2 * G, th + 2);
+        mbar_expect_tx(bar, max(r1 - r0, 0) * rbytes + (m1 - m0) * mbytes);
+        for (int rr = r0; rr < r1; ++rr) stage_r(rr);
+        for (int km = m0; km < m1; ++km) stage_m(km);
       }
-      step(k, X1, X2);
-      step(k + 1, X2, X1);
+#pragma unroll
+      for (int g = 0; g < G; g += 2) {
+        if (k + g < th + 2) {
+          step(k + g, X1, X2);
+          step(k + g + 1, X2, X1);
+        }
+      }
     }
   }
   __syncthreads();
@@ -490,16 +494,16 @@ int sweep4_th() {
   return g_th;
 }
 
-template <int B, int DIR>
+template <int B, int DIR, int G>
 cudaError_t launch4(const SweepArgs& a, cudaStream_t s) {
   const int th = sweep4_th();
   const int nzw = ((a.d & 31) == 0 ? a.d : a.d + 1 + 31) / 32;   // tail z = d off the lanes
   const int passes = (nzw + kNWMax - 1) / kNWMax;
   const int nw = (nzw + passes - 1) / passes;
-  const S4Layout<B> lay(th, nw, passes * nw);
+  const S4Layout<B, G> lay(th, nw, passes * nw);
   static size_t configured = 0;
   if (configured < lay.bytes) {
-    cudaError_t e = cudaFuncSetAttribute(sweep4_kernel<B, DIR>,
+    cudaError_t e = cudaFuncSetAttribute(sweep4_kernel<B, DIR, G>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)lay.bytes);
     if (e != cudaSuccess) return e;
@@ -509,7 +513,7 @@ cudaError_t launch4(const SweepArgs& a, cudaStream_t s) {
   SweepArgs b = a;
   b.rows.lo = (a.rows.lo / th) * th;
   dim3 grid((a.W + kTW - 1) / kTW, (b.rows.hi - b.rows.lo + th - 1) / th);
-  sweep4_kernel<B, DIR><<<grid, 32 * nw, lay.bytes, s>>>(b, th);
+  sweep4_kernel<B, DIR, G><<<grid, 32 * nw, lay.bytes, s>>>(b, th);
   return cudaGetLastError();
 }
 
@@ -523,13 +527,29 @@ bool sweep4_supported(const SweepArgs& a) {
          a.d <= 4095 && a.d <= 32767;
 }
 
-cudaError_t launch_sweep4(const SweepArgs& a, cudaStream_t s) {
+int g_group = -1;
+int sweep4_group() {
+  if (g_group < 0) {
+    const char* v = getenv("MSHBM_SWEEP4_G");   // row steps per CTA barrier (2 or 4)
+    g_group = v ? atoi(v) : 2;   // 4 spills at the 128-register cap (measured slower)
+    if (g_group != 2 && g_group != 4) g_group = 2;
+  }
+  return g_group;
+}
+
+template <int B>
+cudaError_t launch4_b(const SweepArgs& a, cudaStream_t s) {
   const bool mb = a.dir > 0;
+  if (sweep4_group() == 2) return mb ? launch4<B, 1, 2>(a, s) : launch4<B, -1, 2>(a, s);
+  return mb ? launch4<B, 1, 4>(a, s) : launch4<B, -1, 4>(a, s);
+}
+
+cudaError_t launch_sweep4(const SweepArgs& a, cudaStream_t s) {
   switch (a.block) {
-    case 5: return mb ? launch4<5, 1>(a, s) : launch4<5, -1>(a, s);
-    case 7: return mb ? launch4<7, 1>(a, s) : launch4<7, -1>(a, s);
-    case 9: return mb ? launch4<9, 1>(a, s) : launch4<9, -1>(a, s);
-    case 11: return mb ? launch4<11, 1>(a, s) : launch4<11, -1>(a, s);
+    case 5: return launch4_b<5>(a, s);
+    case 7: return launch4_b<7>(a, s);
+    case 9: return launch4_b<9>(a, s);
+    case 11: return launch4_b<11>(a, s);
     default: return cudaErrorInvalidValue;
   }
 }
