@@ -25,6 +25,8 @@
 // window), 196-233 (3x3-summed refinement); zncc.py:271-287 (cost).
 #include <stdlib.h>
 
+#include <type_traits>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -154,39 +156,43 @@ __device__ __forceinline__ void row_step(
     cp[2 * u2] = fma_sat(fmaf(-pp.x, m0.x, cp[2 * u2]) * pp.y, m0.y, half);
     cp[2 * u2 + 1] = fma_sat(fmaf(-pp.z, m1.x, cp[2 * u2 + 1]) * pp.w, m1.y, half);
   }
-  // selection winner-take-all for output row k - 1: keys of lanes outside
-  // the pixel's window [lo, lo + span] are 0
-  if (k >= 1 && k <= th) {
+  // per output pixel p, in one pass so the cost row dies as it is consumed:
+  // selection winner-take-all for output row k - 1 (keys of lanes outside the
+  // pixel's window [lo, lo + span] are 0), the 3x3 sums (horizontal 3-sum of
+  // this row + the two rows above in Y) and their winner for row k - 2
+  auto wta = [&](auto sel_t, auto ref_t) {
+    constexpr bool SEL = decltype(sel_t)::value, REF = decltype(ref_t)::value;
     const int4* wrow = Wn + (k - 1) * (kTW / 2);
+    unsigned* srow = sk + (k - 1) * kTW;
+    unsigned* rrow = rk + (k - 2) * kTW;
 #pragma unroll
-    for (int p2 = 0; p2 < kTW / 2; ++p2) {
-      const int4 win = wrow[p2];   // (lo, span) of pixels 2 p2 and 2 p2 + 1
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int p = 2 * p2 + h;
-        const int lo = h ? win.z : win.x, span = h ? win.w : win.y;
+    for (int p = 0; p < kTW; ++p) {
+      if constexpr (SEL) {
+        const int4 win = wrow[p / 2];   // (lo, span) of pixels p & ~1 and p | 1
+        const int lo = (p & 1) ? win.z : win.x, span = (p & 1) ? win.w : win.y;
         const unsigned key = (unsigned)(z - lo) <= (unsigned)span
                                  ? (__float_as_uint(cp[p + 1] + 1.0f) << 5) + laneK
                                  : 0u;
         const unsigned r = __reduce_max_sync(kFull, key);
-        if (lane0) sk[(k - 1) * kTW + p] = r;
+        if (lane0) srow[p] = r;
       }
+      const float h = (cp[p] + cp[p + 1]) + cp[p + 2];
+      if constexpr (REF) {
+        const float n = Y[p] + h;
+        const unsigned key = (__float_as_uint(fmaf(n, 0.0625f, 1.0f)) << 5) + laneK;
+        const unsigned r = __reduce_max_sync(kFull, key);
+        if (lane0) rrow[p] = r;
+      }
+      Y[p] = Xin[p] + h;
+      Xout[p] = h;
     }
-  }
-  // 3x3 sums: horizontal 3-sums of this row, vertical with the two rows above
-#pragma unroll
-  for (int p = 0; p < kTW; ++p) Xout[p] = (cp[p] + cp[p + 1]) + cp[p + 2];
-  if (k >= 2) {
-#pragma unroll
-    for (int p = 0; p < kTW; ++p) {
-      const float n = Y[p] + Xout[p];
-      const unsigned key = (__float_as_uint(fmaf(n, 0.0625f, 1.0f)) << 5) + laneK;
-      const unsigned r = __reduce_max_sync(kFull, key);
-      if (lane0) rk[(k - 2) * kTW + p] = r;
-    }
-  }
-#pragma unroll
-  for (int p = 0; p < kTW; ++p) Y[p] = Xin[p] + Xout[p];
+  };
+  using T1 = std::true_type;
+  using F1 = std::false_type;
+  if (k >= 2 && k <= th) wta(T1{}, T1{});
+  else if (k == 1) wta(T1{}, F1{});
+  else if (k == 0) wta(F1{}, F1{});
+  else wta(F1{}, T1{});
 }
 
 template <int B, int DIR, int G>
