@@ -404,7 +404,7 @@ def run_ours(args, cfg):
     achieved = alg_flops / (sweep_ms * 1e-3) / 1e12
     dense_flops = l0.pixels * (l0.d_max + 1) * flops_per_pde(l0.block)
     per_pair_ms = ms / max(1, wl.pairs_per_step / ws) if wl.kind != "bands" else ms
-    roof = {"bound": "fp32", "kernel": "sweep2_kernel<b=%d> (level 0)" % l0.block,
+    roof = {"bound": "fp32", "kernel": "%s<b=%d> (level 0)" % (sweep_kernel_name(l0), l0.block),
             "achieved": achieved, "peak": tf.value, "unit": "TFLOP/s",
             "frac": achieved / tf.value, "traffic": TRAFFIC.get(cfg.name),
             "peak_source": "measured live: mshbm_probe_fp32_peak FFMA probe on this GPU "
@@ -457,7 +457,16 @@ def run_ours(args, cfg):
 
 # dram__bytes_read.sum + dram__bytes_write.sum of the level-0 sweep launch from
 # the committed ncu --set full captures (profiles/), per config
-TRAFFIC = {"C2": 36137216 + 448000}   # r01_sweep2_c2_ncu.md (ncu --set full, L0 sweep)
+TRAFFIC = {"C2": 43302912 + 723968}   # r01_sweep4_c2_ncu.md (ncu --set full, L0 sweep)
+
+
+def sweep_kernel_name(level) -> str:
+    """The level-0 sweep kernel the library launches (csrc/sweep.cu dispatch:
+    sweep4 for b >= 5 on levels of >= 400k pixels unless MSHBM_SWEEP4=0)."""
+    if (os.environ.get("MSHBM_SWEEP4", "1") != "0" and level.block in (5, 7, 9, 11)
+            and level.height * level.width >= 400000):
+        return "sweep4_kernel"
+    return "sweep2_kernel"
 
 
 def main():
