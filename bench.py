@@ -462,9 +462,10 @@ TRAFFIC = {"C2": 43302912 + 723968}   # r01_sweep4_c2_ncu.md (ncu --set full, L0
 
 def sweep_kernel_name(level) -> str:
     """The level-0 sweep kernel the library launches (csrc/sweep.cu dispatch:
-    sweep4 for b >= 5 on levels of >= 400k pixels unless MSHBM_SWEEP4=0)."""
-    if (os.environ.get("MSHBM_SWEEP4", "1") != "0" and level.block in (5, 7, 9, 11)
-            and level.height * level.width >= 400000):
+    sweep4 for b >= 5 on levels of >= 400k pixels; MSHBM_SWEEP4=0 never, =2 always)."""
+    mode = os.environ.get("MSHBM_SWEEP4", "1")
+    if (mode != "0" and level.block in (5, 7, 9, 11)
+            and (mode == "2" or level.height * level.width >= 400000)):
         return "sweep4_kernel"
     return "sweep2_kernel"
 

@@ -41,6 +41,10 @@ struct LevelBuf {
   float* isR = nullptr;
   float* muL = nullptr;     // left window statistics (sweep4 levels, b >= 5)
   float* isL = nullptr;
+  unsigned* flags = nullptr;  // sweep4 precision-guard tile flags
+  int64_t flags_ld = 0;
+  int* fix_list = nullptr;   // sweep2 fixup jobs (+ count)
+  int* fix_count = nullptr;
   int* wc = nullptr;
   int16_t* dsel = nullptr;
   int16_t* dmed = nullptr;
@@ -194,6 +198,11 @@ void carve(Plan& p, Carver& cv) {
     if (l.b >= 5) {
       l.muL = cv.take<float>(n);
       l.isL = cv.take<float>(n);
+      // one byte per 16-column x (>= 2)-row tile (sweep4_th() >= 2)
+      l.flags_ld = (l.w + 15) / 16;
+      l.flags = cv.take<unsigned>((size_t)l.flags_ld * ((l.h + 1) / 2));
+      l.fix_list = cv.take<int>((size_t)((l.w + 29) / 30) * (l.h / 14 + 2));
+      l.fix_count = cv.take<int>(1);
     }
     l.wc = cv.take<int>(n);
     l.dsel = cv.take<int16_t>(n);
@@ -262,7 +271,8 @@ struct StageEvents {
 // costs also runs on the branch, beside level k's median (evs[K+2+k] =
 // sweep k done, evs[2K+3+(k-1)] = prefilter done, joined by prior k-1).
 int enqueue(mshbm_ctx* ctx, Plan& p, cudaStream_t s, std::vector<StageEvents>* tev,
-            cudaStream_t side = nullptr, cudaEvent_t* evs = nullptr) {
+            cudaStream_t side = nullptr, cudaEvent_t* evs = nullptr,
+            cudaStream_t side2 = nullptr) {
   int n = 0;
   const mshbm_config& cfg = p.cfg;
   const int dir = cfg.sign == MSHBM_SIGN_PAPER ? -1 : 1;
@@ -297,8 +307,19 @@ int enqueue(mshbm_ctx* ctx, Plan& p, cudaStream_t s, std::vector<StageEvents>* t
     CK(launch_prep_staging(l.R, l.ld, l.muR, l.isR, l.ld, l.h, l.w, l.pc, l.Rp, l.Mp, l.ldp, t));
     n += 2;
     if (l.muL) {
-      CK(launch_stats_f32(l.L, l.h, l.w, l.ld, l.b, cfg.sigma_eps, l.muL, l.isL, l.ld, t));
-      ++n;
+      // L statistics + sweep4's precision guard (tile flags), then the job
+      // list of its sweep2 fixup
+      Sweep4Guard g;
+      g.muR = l.muR;
+      g.isR = l.isR;
+      g.tile_h = sweep4_th();
+      g.flags = l.flags;
+      g.flags_ld = l.flags_ld;
+      CK(cudaMemsetAsync(l.flags, 0, sizeof(unsigned) * l.flags_ld * ((l.h + 1) / 2), t));
+      CK(launch_stats_f32(l.L, l.h, l.w, l.ld, l.b, cfg.sigma_eps, l.muL, l.isL, l.ld, t, g));
+      CK(launch_fixup_list(l.flags, l.flags_ld, sweep4_th(), l.h, l.w, l.rows, l.b, l.fix_list,
+                           l.fix_count, t));
+      n += 2;
     }
     if (fork && k < p.K) CK(cudaEventRecord(evs[k], side));
   }
@@ -324,6 +345,8 @@ int enqueue(mshbm_ctx* ctx, Plan& p, cudaStream_t s, std::vector<StageEvents>* t
     a.L = l.L; a.R = l.R; a.ld = l.ld;
     a.muR = l.muR; a.isR = l.isR; a.lds = l.ld;
     a.muL = l.muL; a.isL = l.isL;
+    a.tile_flags = l.flags; a.flags_ld = l.flags_ld;
+    a.fix_list = l.fix_list; a.fix_count = l.fix_count;
     a.H = l.h; a.W = l.w; a.d = l.d; a.block = l.b; a.dir = dir;
     a.sigma_eps = cfg.sigma_eps;
     a.wc = k < p.K ? l.wc : nullptr; a.ldw = l.ld; a.radius = cfg.radius;
@@ -333,16 +356,24 @@ int enqueue(mshbm_ctx* ctx, Plan& p, cudaStream_t s, std::vector<StageEvents>* t
     a.rows = l.rows;
     a.Rp = l.Rp; a.Mp = l.Mp; a.ldp = l.ldp; a.pc = l.pc;
     if (fork && k < p.K) CK(cudaStreamWaitEvent(s, evs[k], 0));
+    const bool s4 = sweep_uses_sweep4(a);
     if (ev) CK(cudaEventRecord(ev->sel0, s));
     CK(launch_sweep(a, s, &n));
     if (ev) CK(cudaEventRecord(ev->sel1, s));
+    if (s4) {   // sweep2 on the tiles sweep4's precision guard left (usually none)
+      CK(launch_sweep4_fixup(a, s));
+      ++n;
+    }
     if (fork && k > 0) {
       // the prefilter of this level's costs (next level's prior) overlaps
       // this level's selective median
       CK(cudaEventRecord(evs[p.K + 2 + k], s));
-      CK(cudaStreamWaitEvent(side, evs[p.K + 2 + k], 0));
-      CK(launch_bspline_prefilter(l.c, nullptr, l.h, l.w, l.ld, l.coef, l.ldc, side));
-      CK(cudaEventRecord(evs[2 * p.K + 3 + (k - 1)], side));
+      // (its own branch: the next level's prior waits for it, and it must not
+      // queue behind the statistics branch's level-0 work)
+      cudaStream_t pf = side2 ? side2 : side;
+      CK(cudaStreamWaitEvent(pf, evs[p.K + 2 + k], 0));
+      CK(launch_bspline_prefilter(l.c, nullptr, l.h, l.w, l.ld, l.coef, l.ldc, pf));
+      CK(cudaEventRecord(evs[2 * p.K + 3 + (k - 1)], pf));
       n += 1;
     }
     if (ev) CK(cudaEventRecord(ev->med0, s));
@@ -404,16 +435,18 @@ int launch_plan(mshbm_ctx* ctx, Plan& p, cudaStream_t s, int flags,
     if (!p.exec) {
       cudaStream_t cs;
       CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
-      cudaStream_t side;
+      cudaStream_t side, side2;
       CK(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+      CK(cudaStreamCreateWithFlags(&side2, cudaStreamNonBlocking));
       std::vector<cudaEvent_t> evs(3 * p.K + 4);
       for (auto& e : evs) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
       cudaGraph_t g;
       CK(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
-      int st = enqueue(ctx, p, cs, nullptr, side, evs.data());
+      int st = enqueue(ctx, p, cs, nullptr, side, evs.data(), side2);
       cudaError_t ce = cudaStreamEndCapture(cs, &g);
       for (auto& e : evs) cudaEventDestroy(e);
       cudaStreamDestroy(side);
+      cudaStreamDestroy(side2);
       cudaStreamDestroy(cs);
       if (st) return st;
       CK(ce);

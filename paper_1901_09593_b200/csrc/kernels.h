@@ -48,10 +48,28 @@ struct SweepArgs {
   const float2* Mp;
   int64_t ldp;
   int pc;
+  // sweep4 precision guard (one byte per 16 x tile_h tile of the level, row
+  // stride flags_ld): sweep4 writes 1 for tiles whose centring amplification
+  // is too high and leaves them; sweep2 with fixup = 1 recomputes only those
+  const unsigned* tile_flags;
+  int64_t flags_ld;
+  int tile_h;
+  int fixup;
+  // fixup list mode: sweep2 walks these job indices (by * fix_nbx + bx)
+  const int* fix_list;
+  const int* fix_count;
+  int fix_nbx;
   // raw outputs (dense H x W): full, window, 3x3-summed winners
   int16_t* fz; float* fc; int16_t* wz; float* wcst; int16_t* nz; float* nc;
 };
 cudaError_t launch_sweep(const SweepArgs& a, cudaStream_t s, int* n_launch);
+// whether launch_sweep runs sweep4 for these arguments; if so the caller must
+// also launch launch_sweep4_fixup (same inputs; may run concurrently)
+bool sweep_uses_sweep4(const SweepArgs& a);
+cudaError_t launch_sweep4_fixup(const SweepArgs& a, cudaStream_t s);
+// job list for launch_sweep4_fixup (after the guard flags, before sweep4)
+cudaError_t launch_fixup_list(const unsigned* flags, int64_t flags_ld, int tile_h, int h, int w,
+                              RowBand rows, int block, int* list, int* count, cudaStream_t s);
 bool sweep_supported_block(int b);
 // two-pixels-per-thread variant (sweep2.cu) for b in {3,5,7,9,11}
 bool sweep2_supported(int b);
@@ -59,8 +77,9 @@ bool sweep3_supported(int b);
 cudaError_t launch_sweep3(const SweepArgs& a, cudaStream_t s);
 cudaError_t launch_sweep2(const SweepArgs& a, cudaStream_t s);
 // disparities-across-lanes variant (sweep4.cu): pipeline mode, b in {5,7,9,11}
-bool sweep4_supported(const SweepArgs& a);
+bool sweep4_supported(const SweepArgs& a, bool force);
 cudaError_t launch_sweep4(const SweepArgs& a, cudaStream_t s);
+int sweep4_th();   // output rows per sweep4 tile (the guard's tile height)
 
 // Column margin of the padded staging arrays for search bound d, block b.
 inline int staging_margin(int d, int b) { return (d + 16 + b + 40 + 3) / 4 * 4; }
@@ -85,11 +104,29 @@ cudaError_t launch_downsample_f32(const float* in0, const float* in1, int h, int
                                   cudaStream_t s);
 
 // ---------------------------------------------------------------- stats
+// sweep4 precision guard, evaluated by the statistics kernel of L (R's
+// statistics already computed).  sweep4 centres L by one constant per
+// 16 x tile_h tile (the L sample at the tile centre) and R by the level
+// constant c = muR at the image centre, so its fp32 rounding error relative
+// to the cost grows with the amplification
+//   A(p) = (|muL(p) - cL| / sigmaL(p) + 3) x (|muR(p) - c| / sigmaR(p) + 3)
+// (measured: cost error ~1.1e-7 A; BASELINE configs A <= 90, the reference's
+// smooth low-contrast [0, 1] fixtures up to ~900).  Tiles with a pixel above
+// kSweep4RiskMax get flags[tile] |= 1 (zeroed before every run); sweep4
+// leaves them to sweep2's per-pixel centring (launch_sweep4_fixup).
+constexpr float kSweep4RiskMax = 200.f;
+struct Sweep4Guard {
+  const float* muR = nullptr;   // stride lds, as the output maps
+  const float* isR = nullptr;
+  int tile_h = 0;
+  unsigned* flags = nullptr;    // nullptr: no guard
+  int64_t flags_ld = 0;
+};
 // fp32 mean / inverse sigma (0 = degenerate) of the b x b replicate-padded
 // window, centred arithmetic in fp64.
 cudaError_t launch_stats_f32(const double* img, int h, int w, int64_t ld,
                              int b, double sigma_eps, float* mu, float* is,
-                             int64_t lds, cudaStream_t s);
+                             int64_t lds, cudaStream_t s, Sweep4Guard g = Sweep4Guard{});
 // fp64 mean / sigma maps (dense) for the CostEngine API
 cudaError_t launch_stats_f64(const double* img, int h, int w, int64_t ld,
                              int b, double* mu, double* sigma, cudaStream_t s);

@@ -453,7 +453,7 @@ template <int B>
 __global__ void __launch_bounds__(kTX * kTY) stats_tiled_kernel(const double* img, int h, int w,
                                                               int64_t ld, double sigma_eps,
                                                               float* mu32, float* is32,
-                                                              int64_t lds) {
+                                                              int64_t lds, Sweep4Guard g) {
   // Separable box sums of x' and x'^2 (x' = x - c, c the tile's first sample,
   // fp64); windows whose shifted variance cancels to < 1e-9 of E[x'^2]
   // (flat or near-flat) recompute it centred from the tile, so flat blocks
@@ -505,6 +505,20 @@ __global__ void __launch_bounds__(kTX * kTY) stats_tiled_kernel(const double* im
   const double sigma = sqrt(fmax(var, 0.0));
   mu32[(int64_t)y * lds + x] = (float)(m1 + c);
   is32[(int64_t)y * lds + x] = sigma >= sigma_eps ? (float)(1.0 / sigma) : 0.f;
+  if (g.flags != nullptr && sigma >= sigma_eps) {
+    // sweep4 precision guard (see Sweep4Guard): this pixel's amplification
+    // against its sweep4 tile's centring constants
+    const int ty = y / g.tile_h, tx = x / 16;
+    const double cL = img[(int64_t)clampi(ty * g.tile_h + g.tile_h / 2, 0, h - 1) * ld +
+                          clampi(tx * 16 + 8, 0, w - 1)];
+    const float ir = g.isR[(int64_t)y * lds + x];
+    if (ir > 0.f) {
+      const float cR = g.muR[(int64_t)(h / 2) * lds + w / 2];
+      const float aL = (float)(fabs(m1 + c - cL) / sigma) + 3.f;
+      const float aR = fabsf(g.muR[(int64_t)y * lds + x] - cR) * ir + 3.f;
+      if (aL * aR > kSweep4RiskMax) atomicOr(&g.flags[(int64_t)ty * g.flags_ld + tx], 1u);
+    }
+  }
 }
 
 // prior_eval with the 4x4 spline support of the block staged in smem
@@ -837,15 +851,15 @@ cudaError_t launch_downsample_f32(const float* in0, const float* in1, int h, int
 
 cudaError_t launch_stats_f32(const double* img, int h, int w, int64_t ld,
                              int b, double sigma_eps, float* mu, float* is,
-                             int64_t lds, cudaStream_t s) {
+                             int64_t lds, cudaStream_t s, Sweep4Guard g) {
   dim3 blk(32, 8);
-  const dim3 g = grid2d(w, h, blk);
+  const dim3 gr = grid2d(w, h, blk);
   switch (b) {
-    case 3: stats_tiled_kernel<3><<<g, blk, 0, s>>>(img, h, w, ld, sigma_eps, mu, is, lds); return cudaGetLastError();
-    case 5: stats_tiled_kernel<5><<<g, blk, 0, s>>>(img, h, w, ld, sigma_eps, mu, is, lds); return cudaGetLastError();
-    case 7: stats_tiled_kernel<7><<<g, blk, 0, s>>>(img, h, w, ld, sigma_eps, mu, is, lds); return cudaGetLastError();
-    case 9: stats_tiled_kernel<9><<<g, blk, 0, s>>>(img, h, w, ld, sigma_eps, mu, is, lds); return cudaGetLastError();
-    case 11: stats_tiled_kernel<11><<<g, blk, 0, s>>>(img, h, w, ld, sigma_eps, mu, is, lds); return cudaGetLastError();
+    case 3: stats_tiled_kernel<3><<<gr, blk, 0, s>>>(img, h, w, ld, sigma_eps, mu, is, lds, g); return cudaGetLastError();
+    case 5: stats_tiled_kernel<5><<<gr, blk, 0, s>>>(img, h, w, ld, sigma_eps, mu, is, lds, g); return cudaGetLastError();
+    case 7: stats_tiled_kernel<7><<<gr, blk, 0, s>>>(img, h, w, ld, sigma_eps, mu, is, lds, g); return cudaGetLastError();
+    case 9: stats_tiled_kernel<9><<<gr, blk, 0, s>>>(img, h, w, ld, sigma_eps, mu, is, lds, g); return cudaGetLastError();
+    case 11: stats_tiled_kernel<11><<<gr, blk, 0, s>>>(img, h, w, ld, sigma_eps, mu, is, lds, g); return cudaGetLastError();
     default: break;
   }
   stats_kernel<false><<<grid2d(w, h, blk), blk, 0, s>>>(img, h, w, ld, b, sigma_eps,

@@ -464,19 +464,56 @@ cudaError_t launch_dir(const SweepArgs& a, cudaStream_t s) {
 
 bool sweep_supported_block(int b) { return b >= 3 && (b & 1) && b <= 63; }
 
+namespace {
+
+int env_int(const char* name, int dflt) {
+  const char* v = getenv(name);
+  return v ? atoi(v) : dflt;
+}
+// MSHBM_SWEEP_IMPL: 1 = one pixel per thread, 2 = sweep2 (default), 3 = sweep3
+int sweep_impl() {
+  static int v = env_int("MSHBM_SWEEP_IMPL", 2);
+  return v;
+}
+// MSHBM_SWEEP4: 0 = sweep2 everywhere, 1 = sweep4 where supported and large
+// enough (default), 2 = sweep4 wherever supported (tests)
+int sweep4_mode() {
+  static int v = env_int("MSHBM_SWEEP4", 1);
+  return v;
+}
+// MSHBM_SWEEP4_GUARD=0 drops the precision guard (measurement only)
+bool sweep4_guard() {
+  static int v = env_int("MSHBM_SWEEP4_GUARD", 1);
+  return v != 0;
+}
+
+}  // namespace
+
+bool sweep_uses_sweep4(const SweepArgs& a) {
+  return sweep4_mode() != 0 && sweep_impl() >= 2 && sweep4_supported(a, sweep4_mode() == 2);
+}
+
+// Tiles the sweep4 precision guard flagged (csrc/stages.cu) are computed by
+// sweep2 in fixup mode: it writes and counts only their pixels, and its CTAs
+// on unflagged tiles return at once.  It reads what sweep4 reads and writes
+// disjoint pixels, so it may run concurrently with sweep4.
+cudaError_t launch_sweep4_fixup(const SweepArgs& a, cudaStream_t s) {
+  if (!sweep4_guard()) return cudaSuccess;
+  SweepArgs b = a;
+  b.tile_h = sweep4_th();
+  b.fixup = 1;
+  return launch_sweep2(b, s);
+}
+
 cudaError_t launch_sweep(const SweepArgs& a, cudaStream_t s, int* n_launch) {
   if (n_launch) ++*n_launch;
-  static int impl = -1;
-  if (impl < 0) {
-    const char* v = getenv("MSHBM_SWEEP_IMPL");   // 1 = one pixel per thread
-    impl = v ? atoi(v) : 2;
+  const int impl = sweep_impl();
+  if (sweep_uses_sweep4(a)) {
+    SweepArgs b = a;
+    b.tile_h = sweep4_th();
+    if (!sweep4_guard()) b.tile_flags = nullptr;
+    return launch_sweep4(b, s);   // + launch_sweep4_fixup (caller's stream choice)
   }
-  static int use4 = -1;
-  if (use4 < 0) {
-    const char* v = getenv("MSHBM_SWEEP4");   // 0 = keep sweep2 at b >= 5
-    use4 = v ? atoi(v) : 1;
-  }
-  if (use4 && impl >= 2 && sweep4_supported(a)) return launch_sweep4(a, s);
   if (impl == 3 && sweep3_supported(a.block)) return launch_sweep3(a, s);
   if (impl >= 2 && sweep2_supported(a.block)) return launch_sweep2(a, s);
   return a.dir > 0 ? launch_dir<1>(a, s) : launch_dir<-1>(a, s);

@@ -15,6 +15,8 @@
 // window), 196-233 (3x3-summed refinement); zncc.py:271-287 (cost).
 #include <stdlib.h>
 
+#include <algorithm>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -248,8 +250,7 @@ __device__ __forceinline__ void chunk2(
 }
 
 template <int B, int DIR, int ZC, int NR, int MINB, int PK>
-__global__ void __launch_bounds__(NR * 32, MINB)
-sweep2_kernel(const SweepArgs a) {
+__device__ __forceinline__ void sweep2_body(const SweepArgs& a, const int bx, const int by) {
   using SM = Sweep2Smem<B, ZC, NR, PK>;
   constexpr int H2 = B / 2;
   constexpr int NT = NR * 32;
@@ -261,8 +262,8 @@ sweep2_kernel(const SweepArgs a) {
 
   const int lane = threadIdx.x & 31;
   const int wp = threadIdx.x >> 5;
-  const int x0 = blockIdx.x * 30;
-  const int y0 = a.rows.lo + blockIdx.y * (NROW - 2);
+  const int x0 = bx * 30;
+  const int y0 = a.rows.lo + by * (NROW - 2);
   const int iA = y0 - 1 + 2 * wp, iB = iA + 1;
   const int j = x0 - 1 + lane;
   const int H = a.H, W = a.W, d = a.d;
@@ -273,6 +274,19 @@ sweep2_kernel(const SweepArgs a) {
   const bool innerA = inA && lanein && wp >= 1;
   const bool innerB = inB && lanein && wp <= NR - 2;
   const float qnan = __int_as_float(0x7fc00000);
+  // sweep4 fixup: only pixels of the tiles sweep4's precision guard flagged
+  auto flagged = [&](int i, int jj) {
+    return a.tile_flags[(int64_t)(i / a.tile_h) * a.flags_ld + jj / 16] != 0;
+  };
+  if (a.fixup) {
+    const int ilo = max(y0, 0), ihi = min(y0 + NROW - 3, H - 1);
+    const int jlo = max(x0, 0), jhi = min(x0 + 29, W - 1);
+    bool any = false;
+    for (int ti = ilo / a.tile_h; ti <= ihi / a.tile_h && !any; ++ti)
+      for (int tj = jlo / 16; tj <= jhi / 16; ++tj)
+        any |= a.tile_flags[(int64_t)ti * a.flags_ld + tj] != 0;
+    if (!any || ilo > ihi || jlo > jhi) return;   // uniform over the CTA
+  }
 
   // ---- staging: cp.async from the padded fp32 arrays (prep_staging) straight
   // into the double-buffered strip; no clamps on columns, no conversion, no
@@ -480,7 +494,7 @@ sweep2_kernel(const SweepArgs a) {
     const float nbc = 2.f * nbv[p] / (float)members - 1.f;
     bool low = false;
     if (a.mode == kSweepPipeline) {
-      if (inner[p]) {
+      if (inner[p] && (!a.fixup || flagged(i, j))) {
         const float cs = trusted[p] ? bw : bf;
         const int zs = trusted[p] ? bestz[2 + p] : bestz[p];
         low = (double)cs <= a.alpha;
@@ -507,6 +521,23 @@ sweep2_kernel(const SweepArgs a) {
   }
 }
 
+// One CTA per 30 x (2 NR - 2) job; in sweep4-fixup list mode a persistent
+// grid walks the job list the list kernel built (only jobs that touch
+// guard-flagged tiles), so an empty list costs one short wave.
+template <int B, int DIR, int ZC, int NR, int MINB, int PK>
+__global__ void __launch_bounds__(NR * 32, MINB) sweep2_kernel(const SweepArgs a) {
+  if (a.fixup && a.fix_list != nullptr) {
+    const int n = *a.fix_count;
+    for (int i = blockIdx.x; i < n; i += gridDim.x) {
+      const int job = a.fix_list[i];
+      sweep2_body<B, DIR, ZC, NR, MINB, PK>(a, job % a.fix_nbx, job / a.fix_nbx);
+      __syncthreads();   // shared memory is reused by the next job
+    }
+  } else {
+    sweep2_body<B, DIR, ZC, NR, MINB, PK>(a, blockIdx.x, blockIdx.y);
+  }
+}
+
 template <int B, int DIR, int ZC, int NR, int MINB, int PK = 0>
 cudaError_t launch2(const SweepArgs& a, cudaStream_t s) {
   constexpr size_t smem = Sweep2Smem<B, ZC, NR, PK>::bytes();
@@ -523,6 +554,10 @@ cudaError_t launch2(const SweepArgs& a, cudaStream_t s) {
   SweepArgs b = a;
   b.rows.lo = (a.rows.lo / (NROW - 2)) * (NROW - 2);
   dim3 grid((a.W + 29) / 30, (b.rows.hi - b.rows.lo + NROW - 3) / (NROW - 2));
+  if (b.fixup && b.fix_list != nullptr) {   // persistent grid over the fixup job list
+    b.fix_nbx = grid.x;
+    grid = dim3(std::min<unsigned>(grid.x * grid.y, 2 * 148), 1);
+  }
   sweep2_kernel<B, DIR, ZC, NR, MINB, PK><<<grid, NR * 32, smem, s>>>(b);
   return cudaGetLastError();
 }
@@ -576,6 +611,42 @@ cudaError_t launch2_dir(const SweepArgs& a, cudaStream_t s) {
 }
 
 }  // namespace
+
+// sweep4 fixup job list: the sweep2 jobs (default variant geometry for b:
+// 30 columns x 2 NR - 2 rows, NR = 16 at b = 5, 8 otherwise) whose output
+// pixels touch a tile the sweep4 guard flagged.  One CTA.
+__global__ void __launch_bounds__(1024) fixup_list_kernel(const unsigned* flags, int64_t flags_ld,
+                                                          int tile_h, int h, int w, int lo,
+                                                          int job_rows, int nbx, int nby,
+                                                          int* list, int* count) {
+  __shared__ int n;
+  if (threadIdx.x == 0) n = 0;
+  __syncthreads();
+  for (int j = threadIdx.x; j < nbx * nby; j += blockDim.x) {
+    const int bx = j % nbx, by = j / nbx;
+    const int y0 = lo + by * job_rows, x0 = bx * 30;
+    const int ilo = max(y0, 0), ihi = min(y0 + job_rows - 1, h - 1);
+    const int jlo = x0, jhi = min(x0 + 29, w - 1);
+    bool any = false;
+    for (int ti = ilo / tile_h; ti <= ihi / tile_h && !any; ++ti)
+      for (int tj = jlo / 16; tj <= jhi / 16; ++tj)
+        any |= flags[(int64_t)ti * flags_ld + tj] != 0;
+    if (any && ilo <= ihi && jlo <= jhi) list[atomicAdd(&n, 1)] = j;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) *count = n;
+}
+
+cudaError_t launch_fixup_list(const unsigned* flags, int64_t flags_ld, int tile_h, int h, int w,
+                              RowBand rows, int block, int* list, int* count, cudaStream_t s) {
+  const int nr = block == 5 ? 16 : 8;   // the sweep2 variant launch2_dir picks
+  const int job_rows = 2 * nr - 2;
+  const int lo = (rows.lo / job_rows) * job_rows;
+  const int nbx = (w + 29) / 30, nby = (rows.hi - lo + job_rows - 1) / job_rows;
+  fixup_list_kernel<<<1, 1024, 0, s>>>(flags, flags_ld, tile_h, h, w, lo, job_rows, nbx,
+                                       std::max(nby, 0), list, count);
+  return cudaGetLastError();
+}
 
 bool sweep2_supported(int b) { return b == 3 || b == 5 || b == 7 || b == 9 || b == 11; }
 

@@ -226,11 +226,19 @@ __global__ void __launch_bounds__(kNWMax * 32, 2) sweep4_kernel(const SweepArgs 
   const int H = a.H, W = a.W;
   const float qnan = __int_as_float(0x7fc00000);
 
+  // Precision guard: the sliding sums multiply tile-centred values, so their
+  // fp32 rounding error relative to the cost scales with the tile's
+  // centring amplification (kernels.h Sweep4Guard, evaluated by the L
+  // statistics kernel on the statistics branch).  Flagged tiles are left to the per-pixel-centred
+  // sweep2 fixup launch (launch_sweep4_fixup), which may run concurrently.
+  if (a.tile_flags != nullptr && a.tile_flags[(int64_t)(y0 / th) * a.flags_ld + blockIdx.x] != 0)
+    return;   // uniform: the whole CTA leaves
   // ---- prologue: winner slots, left tile L' = L - cL, window bounds
   if (tid == 0) mbar_init(bar, 1);
   for (int t = tid; t < nslot * th * kTW; t += nt) sK[t] = 0u, rK[t] = 0u;
-  const double cL = (double)a.muL[(int64_t)clampi(y0 + th / 2, 0, H - 1) * a.lds +
-                                  clampi(x0 + kTW / 2, 0, W - 1)];
+  // centring constant: the L sample at the tile centre (the guard in the L
+  // statistics kernel uses the same one)
+  const double cL = a.L[(int64_t)clampi(y0 + th / 2, 0, H - 1) * a.ld + clampi(x0 + kTW / 2, 0, W - 1)];
   for (int t = tid; t < (th + B + 1) * NV; t += nt) {
     const int rr = t / NV, c = t - rr * NV;
     const int y = clampi(y0 - 1 - H2 + rr, 0, H - 1), x = clampi(x0 - 1 - H2 + c, 0, W - 1);
@@ -315,6 +323,7 @@ __global__ void __launch_bounds__(kNWMax * 32, 2) sweep4_kernel(const SweepArgs 
       bulk_g2s(Mr + (k % (2 * G)) * lay.mwp, Mp + ((int64_t)y * a.ldp + mc0), mbytes, bar);
     };
     __syncthreads();   // previous pass done with the rings (and the prologue)
+
     if (tid == 0) {
       fence_proxy_async();
       const int nr0 = min(B + G, th + B + 1), nm0 = min(G, th + 2);
@@ -490,6 +499,8 @@ __global__ void __launch_bounds__(kNWMax * 32, 2) sweep4_kernel(const SweepArgs 
   block_accumulate<1>(a.counters, slot, val, mx);
 }
 
+}  // namespace
+
 int g_th = -1;
 int sweep4_th() {
   if (g_th < 0) {
@@ -499,6 +510,8 @@ int sweep4_th() {
   }
   return g_th;
 }
+
+namespace {
 
 template <int B, int DIR, int G>
 cudaError_t launch4(const SweepArgs& a, cudaStream_t s) {
@@ -525,12 +538,14 @@ cudaError_t launch4(const SweepArgs& a, cudaStream_t s) {
 
 }  // namespace
 
-bool sweep4_supported(const SweepArgs& a) {
+bool sweep4_supported(const SweepArgs& a, bool force) {
   // small levels (C1's 450 x 375) leave most SMs idle with one-disparity-
-  // per-lane tiles; sweep2's pixel-pair threads are faster there (measured)
-  return (int64_t)a.H * a.W >= 400000 && a.mode == kSweepPipeline && a.muL != nullptr && a.isL != nullptr &&
+  // per-lane tiles; sweep2's pixel-pair threads are faster there (measured).
+  // force (MSHBM_SWEEP4=2) drops the size rule: parity tests on small images
+  return (force || (int64_t)a.H * a.W >= 400000) && a.mode == kSweepPipeline &&
+         a.muL != nullptr && a.isL != nullptr && a.tile_flags != nullptr &&
          (a.block == 5 || a.block == 7 || a.block == 9 || a.block == 11) && a.d >= 1 &&
-         a.d <= 4095 && a.d <= 32767;
+         a.d <= 4095;
 }
 
 int g_group = -1;
