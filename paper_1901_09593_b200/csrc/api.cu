@@ -183,6 +183,18 @@ struct Carver {
   }
 };
 
+// Whether the level-0-style sweep4 will run on this level (then it needs the
+// left statistics, the guard flags and the fixup job list).
+bool level_uses_sweep4(const Plan& p, const LevelBuf& l) {
+  SweepArgs a{};
+  a.H = l.h; a.W = l.w; a.d = l.d; a.block = l.b; a.dir = p.cfg.sign == MSHBM_SIGN_PAPER ? -1 : 1;
+  a.mode = kSweepPipeline;
+  static float f1;
+  static unsigned f2;
+  a.muL = &f1; a.isL = &f1; a.tile_flags = &f2;   // non-null stand-ins for the query
+  return sweep_uses_sweep4(a);
+}
+
 void carve(Plan& p, Carver& cv) {
   const int64_t ldi = round_up(p.W, 32);
   p.ld_in = ldi;
@@ -195,14 +207,15 @@ void carve(Plan& p, Carver& cv) {
     l.R = cv.take<double>(n);
     l.muR = cv.take<float>(n);
     l.isR = cv.take<float>(n);
-    if (l.b >= 5) {
+    if (level_uses_sweep4(p, l)) {
       l.muL = cv.take<float>(n);
       l.isL = cv.take<float>(n);
-      // one byte per 16-column x (>= 2)-row tile (sweep4_th() >= 2)
+      // one word per 16-column x (>= 2)-row tile (sweep4_th() >= 2), then the
+      // fixup job count (zeroed together before every run)
       l.flags_ld = (l.w + 15) / 16;
-      l.flags = cv.take<unsigned>((size_t)l.flags_ld * ((l.h + 1) / 2));
+      l.flags = cv.take<unsigned>((size_t)l.flags_ld * ((l.h + 1) / 2) + 1);
+      l.fix_count = reinterpret_cast<int*>(l.flags + (size_t)l.flags_ld * ((l.h + 1) / 2));
       l.fix_list = cv.take<int>((size_t)((l.w + 29) / 30) * (l.h / 14 + 2));
-      l.fix_count = cv.take<int>(1);
     }
     l.wc = cv.take<int>(n);
     l.dsel = cv.take<int16_t>(n);
@@ -315,7 +328,7 @@ int enqueue(mshbm_ctx* ctx, Plan& p, cudaStream_t s, std::vector<StageEvents>* t
       g.tile_h = sweep4_th();
       g.flags = l.flags;
       g.flags_ld = l.flags_ld;
-      CK(cudaMemsetAsync(l.flags, 0, sizeof(unsigned) * l.flags_ld * ((l.h + 1) / 2), t));
+      CK(cudaMemsetAsync(l.flags, 0, sizeof(unsigned) * (l.flags_ld * ((l.h + 1) / 2) + 1), t));
       CK(launch_stats_f32(l.L, l.h, l.w, l.ld, l.b, cfg.sigma_eps, l.muL, l.isL, l.ld, t, g));
       CK(launch_fixup_list(l.flags, l.flags_ld, sweep4_th(), l.h, l.w, l.rows, l.b, l.fix_list,
                            l.fix_count, t));

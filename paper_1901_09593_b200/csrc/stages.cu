@@ -514,7 +514,7 @@ __global__ void __launch_bounds__(kTX * kTY) stats_tiled_kernel(const double* im
     const float ir = g.isR[(int64_t)y * lds + x];
     if (ir > 0.f) {
       const float cR = g.muR[(int64_t)(h / 2) * lds + w / 2];
-      const float aL = (float)(fabs(m1 + c - cL) / sigma) + 3.f;
+      const float aL = (float)fabs(m1 + c - cL) * (float)(1.0 / sigma) + 3.f;
       const float aR = fabsf(g.muR[(int64_t)y * lds + x] - cR) * ir + 3.f;
       if (aL * aR > kSweep4RiskMax) atomicOr(&g.flags[(int64_t)ty * g.flags_ld + tx], 1u);
     }

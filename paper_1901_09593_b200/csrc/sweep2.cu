@@ -614,27 +614,22 @@ cudaError_t launch2_dir(const SweepArgs& a, cudaStream_t s) {
 
 // sweep4 fixup job list: the sweep2 jobs (default variant geometry for b:
 // 30 columns x 2 NR - 2 rows, NR = 16 at b = 5, 8 otherwise) whose output
-// pixels touch a tile the sweep4 guard flagged.  One CTA.
-__global__ void __launch_bounds__(1024) fixup_list_kernel(const unsigned* flags, int64_t flags_ld,
-                                                          int tile_h, int h, int w, int lo,
-                                                          int job_rows, int nbx, int nby,
-                                                          int* list, int* count) {
-  __shared__ int n;
-  if (threadIdx.x == 0) n = 0;
-  __syncthreads();
-  for (int j = threadIdx.x; j < nbx * nby; j += blockDim.x) {
-    const int bx = j % nbx, by = j / nbx;
-    const int y0 = lo + by * job_rows, x0 = bx * 30;
-    const int ilo = max(y0, 0), ihi = min(y0 + job_rows - 1, h - 1);
-    const int jlo = x0, jhi = min(x0 + 29, w - 1);
-    bool any = false;
-    for (int ti = ilo / tile_h; ti <= ihi / tile_h && !any; ++ti)
-      for (int tj = jlo / 16; tj <= jhi / 16; ++tj)
-        any |= flags[(int64_t)ti * flags_ld + tj] != 0;
-    if (any && ilo <= ihi && jlo <= jhi) list[atomicAdd(&n, 1)] = j;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) *count = n;
+// pixels touch a tile the sweep4 guard flagged.  One thread per job; *count
+// is zeroed with the flags before every run.
+__global__ void __launch_bounds__(256) fixup_list_kernel(const unsigned* flags, int64_t flags_ld,
+                                                         int tile_h, int h, int w, int lo,
+                                                         int job_rows, int nbx, int nby,
+                                                         int* list, int* count) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= nbx * nby) return;
+  const int bx = j % nbx, by = j / nbx;
+  const int y0 = lo + by * job_rows, x0 = bx * 30;
+  const int ilo = max(y0, 0), ihi = min(y0 + job_rows - 1, h - 1);
+  const int jlo = x0, jhi = min(x0 + 29, w - 1);
+  bool any = false;
+  for (int ti = ilo / tile_h; ti <= ihi / tile_h && !any; ++ti)
+    for (int tj = jlo / 16; tj <= jhi / 16; ++tj) any |= flags[(int64_t)ti * flags_ld + tj] != 0;
+  if (any && ilo <= ihi && jlo <= jhi) list[atomicAdd(count, 1)] = j;
 }
 
 cudaError_t launch_fixup_list(const unsigned* flags, int64_t flags_ld, int tile_h, int h, int w,
@@ -642,9 +637,10 @@ cudaError_t launch_fixup_list(const unsigned* flags, int64_t flags_ld, int tile_
   const int nr = block == 5 ? 16 : 8;   // the sweep2 variant launch2_dir picks
   const int job_rows = 2 * nr - 2;
   const int lo = (rows.lo / job_rows) * job_rows;
-  const int nbx = (w + 29) / 30, nby = (rows.hi - lo + job_rows - 1) / job_rows;
-  fixup_list_kernel<<<1, 1024, 0, s>>>(flags, flags_ld, tile_h, h, w, lo, job_rows, nbx,
-                                       std::max(nby, 0), list, count);
+  const int nbx = (w + 29) / 30, nby = std::max((rows.hi - lo + job_rows - 1) / job_rows, 0);
+  if (nbx * nby == 0) return cudaSuccess;
+  fixup_list_kernel<<<(nbx * nby + 255) / 256, 256, 0, s>>>(flags, flags_ld, tile_h, h, w, lo,
+                                                           job_rows, nbx, nby, list, count);
   return cudaGetLastError();
 }
 
