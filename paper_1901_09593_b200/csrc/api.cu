@@ -455,7 +455,12 @@ int launch_plan(mshbm_ctx* ctx, Plan& p, cudaStream_t s, int flags,
       for (auto& e : evs) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
       cudaGraph_t g;
       CK(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
-      int st = enqueue(ctx, p, cs, nullptr, side, evs.data(), side2);
+      // prefilters get their own branch only when the statistics branch
+      // carries sweep4's extra level-0 work (measured: small pipelines are
+      // faster with one branch)
+      bool s4 = false;
+      for (const LevelBuf& l : p.lv) s4 |= l.muL != nullptr;
+      int st = enqueue(ctx, p, cs, nullptr, side, evs.data(), s4 ? side2 : nullptr);
       cudaError_t ce = cudaStreamEndCapture(cs, &g);
       for (auto& e : evs) cudaEventDestroy(e);
       cudaStreamDestroy(side);
