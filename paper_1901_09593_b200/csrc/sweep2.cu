@@ -526,15 +526,19 @@ __device__ __forceinline__ void sweep2_body(const SweepArgs& a, const int bx, co
 // guard-flagged tiles), so an empty list costs one short wave.
 template <int B, int DIR, int ZC, int NR, int MINB, int PK>
 __global__ void __launch_bounds__(NR * 32, MINB) sweep2_kernel(const SweepArgs a) {
-  if (a.fixup && a.fix_list != nullptr) {
-    const int n = *a.fix_count;
-    for (int i = blockIdx.x; i < n; i += gridDim.x) {
+  // one inlined copy of the body (instruction cache): the plain launch is a
+  // one-iteration loop over its own block
+  const bool lm = a.fixup && a.fix_list != nullptr;
+  const int n = lm ? *a.fix_count : 1;
+  for (int i = lm ? (int)blockIdx.x : 0; i < n; i += lm ? (int)gridDim.x : 1) {
+    int bx = blockIdx.x, by = blockIdx.y;
+    if (lm) {
       const int job = a.fix_list[i];
-      sweep2_body<B, DIR, ZC, NR, MINB, PK>(a, job % a.fix_nbx, job / a.fix_nbx);
-      __syncthreads();   // shared memory is reused by the next job
+      bx = job % a.fix_nbx;
+      by = job / a.fix_nbx;
     }
-  } else {
-    sweep2_body<B, DIR, ZC, NR, MINB, PK>(a, blockIdx.x, blockIdx.y);
+    sweep2_body<B, DIR, ZC, NR, MINB, PK>(a, bx, by);
+    if (lm) __syncthreads();   // shared memory is reused by the next job
   }
 }
 
