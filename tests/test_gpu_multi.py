@@ -68,3 +68,29 @@ def test_batch_matches_single_pair_runs(gpu):
         d, c, t = gpu.run_pipeline_device(L[i], R[i], mc)
         assert torch.equal(D[i], d) and torch.equal(Cc[i], c)
         assert traces[i].counts_dict() == t.counts_dict()
+
+
+def test_row_bands_on_smooth_low_contrast_pair(gpu):
+    """The reference's constant-shift fixture (smooth, [0, 1]): under
+    MSHBM_SWEEP4=2 sweep4's precision guard flags tiles of it, so bands also
+    exercise the sweep2 fixup job list (test_gpu_sweep4 runs this file with
+    the override); either way bands must reproduce the whole image."""
+    import torch
+    from mshbm_testutil import load_golden
+    g = load_golden("pipe_shift48_k0.npz")
+    d_max, levels, block, r, _ = (int(v) for v in g["params"])
+    mc = gpu.MatchConfig(d_max=d_max, levels=levels, block=block, radius=r)
+    lt = torch.from_numpy(np.ascontiguousarray(g["left"], dtype=np.float32)).cuda()
+    rt = torch.from_numpy(np.ascontiguousarray(g["right"], dtype=np.float32)).cuda()
+    d, c, tr = gpu.run_pipeline_device(lt, rt, mc)
+    h = lt.shape[0]
+    bands = gpu.sharding.plan_bands(h, 2, levels)
+    parts_d, parts_c, traces = [], [], []
+    for b0, b1 in bands:
+        bd, bc, bt = gpu.run_pipeline_band(lt, rt, mc, b0, b1)
+        parts_d.append(bd)
+        parts_c.append(bc)
+        traces.append(bt)
+    assert torch.equal(torch.cat(parts_d), d)
+    assert torch.equal(torch.cat(parts_c), c)
+    np.testing.assert_array_equal(counts_of(gpu.sharding.merge_traces(traces)), counts_of(tr))
