@@ -15,11 +15,17 @@
 // Winner-take-all runs across lanes: the half-range cost c' = sat(c/2 + 1/2)
 // (as in sweep2) + 1 lies in [1, 2], so its float bits are monotone and fit
 // 24 bits; key = (bits - 0x3F800000 + 1) << 5 | (31 - lane) and one REDUX.MAX
-// gives the warp's first maximum (smallest z on ties).  Per pixel, the warps'
-// winners meet in a 64-bit shared-memory atomicMax keyed (value, ~z).  The
+// gives the warp's first maximum (smallest z on ties); lane 0 stores it per
+// (warp, pixel) and the epilogue merges the warps in z order.  The
 // 3x3-summed refinement cost is a sliding 3-row / 3-column sum of c' in
 // registers, reduced the same way.  The prior window (trusted pixels) masks
 // the keys of lanes outside [c - r, c + r]; untrusted pixels use [0, d].
+//
+// Also: R' / (muR - c, 0.5/sigmaR) rows stream through a shared-memory ring
+// by 1-D bulk copies (one thread, mbarrier completion); z = d for d a
+// multiple of 32 is evaluated once per tile after the sweep (no warp with a
+// single useful lane); tiles flagged by the precision guard (kernels.h
+// Sweep4Guard) are left to the sweep2 fixup.  DESIGN.md section 6.
 //
 // Reference semantics: matcher.py:184-193 (full search), 263-320 (prior
 // window), 196-233 (3x3-summed refinement); zncc.py:271-287 (cost).
