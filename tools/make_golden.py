@@ -161,6 +161,23 @@ def pipeline_case(name, left, right, d_max, levels, block, r, sign="middlebury",
          gates=np.array([alpha, beta]), ref_seconds=np.array(dt))
 
 
+def full_case(name, cfg, seed):
+    """Full-size BASELINE config through the real reference (radius-generalised
+    driver).  The images are not stored: the tests regenerate them with the
+    seeded generator (synthetic.make_pair); only the outputs are kept (cost
+    as float32, well inside the 1e-4 parity tolerance)."""
+    left, right, _ = make_pair(cfg, seed=seed)
+    rcfg = ref.MatchConfig(d_max=cfg.d_max, levels=cfg.levels, block=cfg.block)
+    t0 = time.perf_counter()
+    d, c, tr = pipeline_r(left, right, rcfg, cfg.radius)
+    dt = time.perf_counter() - t0
+    print(f"full_{name}: {left.shape} {dt:.1f}s total_evals={tr.total_evals}")
+    save(f"full_{name}.npz", disparity=d.astype(np.int16), cost=c.astype(np.float32),
+         counts=counts_array(tr), seed=np.array(seed),
+         params=np.array([cfg.d_max, cfg.levels, cfg.block, cfg.radius, 0]),
+         ref_seconds=np.array(dt))
+
+
 def stage_cases():
     rng = np.random.default_rng(20261019)
     out = {}
@@ -353,6 +370,10 @@ def main():
         return
     if sys.argv[1:] == ["formats"]:
         formats_cases()
+        return
+    if sys.argv[1:] == ["full"]:   # full-size C2 and one C4 pair (minutes)
+        full_case("C2", CONFIGS["C2"], CONFIGS["C2"].seed)
+        full_case("C4", CONFIGS["C4"], CONFIGS["C4"].seed)
         return
     scoring_cases()
     formats_cases()
