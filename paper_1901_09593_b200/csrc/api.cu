@@ -57,6 +57,9 @@ struct LevelBuf {
   int64_t ldp = 0;
   int pc = 0;
   RowBand rows{0, 0, 0, 0};  // sweep/prior/median rows and counted rows
+  // rows of the level image (img) and of its statistics / staging arrays (st)
+  // the rows above need: whole level, or a row band's share plus halos
+  int img_lo = 0, img_hi = 0, st_lo = 0, st_hi = 0;
 };
 
 struct PlanKey {
@@ -82,6 +85,7 @@ struct Plan {
   float* in_r = nullptr;
   int64_t ld_in = 0;
   unsigned long long* counters = nullptr;
+  float* cR = nullptr;        // right-image offset c of every level (centre sample)
   void* arena = nullptr;
   cudaGraphExec_t exec = nullptr;
   int launches = 0;
@@ -201,6 +205,7 @@ void carve(Plan& p, Carver& cv) {
   p.in_l = cv.take<float>((size_t)ldi * p.H);
   p.in_r = cv.take<float>((size_t)ldi * p.H);
   p.counters = cv.take<unsigned long long>((size_t)(p.K + 1) * kCntSlots * kCntCopies);
+  p.cR = cv.take<float>(1);
   for (auto& l : p.lv) {
     const size_t n = (size_t)l.ld * l.h;
     l.L = cv.take<double>(n);
@@ -270,6 +275,24 @@ void plan_rows(Plan& p, int b0, int b1) {
     l.rows.cnt_lo = own_lo;
     l.rows.cnt_hi = own_hi;
   }
+  // Statistics and staging rows: the sweep's CTA grids (sweep2 jobs of <= 30
+  // rows, sweep4 tiles of 32) and window halos reach <= 37 rows beyond its
+  // rows; the image rows add the statistics kernel's tile alignment and
+  // window (<= 13), and every level must also hold the rows the next coarser
+  // level's 5-tap downsample reads (2 x its rows +- 2).  Whole-image plans
+  // get whole levels.
+  for (int k = K; k >= 0; --k) {
+    LevelBuf& l = p.lv[k];
+    l.st_lo = std::max(0, l.rows.lo - 40);
+    l.st_hi = std::min(l.h, l.rows.hi + 40);
+    l.img_lo = std::max(0, l.rows.lo - 56);
+    l.img_hi = std::min(l.h, l.rows.hi + 56);
+    if (k < K) {
+      const LevelBuf& c = p.lv[k + 1];
+      l.img_lo = std::max(0, std::min(l.img_lo, 2 * c.img_lo - 3));
+      l.img_hi = std::min(l.h, std::max(l.img_hi, 2 * c.img_hi + 3));
+    }
+  }
 }
 
 struct StageEvents {
@@ -297,17 +320,26 @@ int enqueue(mshbm_ctx* ctx, Plan& p, cudaStream_t s, std::vector<StageEvents>* t
                            s));
     } else {
       // level 1 straight from the fp32 input; also writes the fp64 level 0
-      CK(launch_downsample_f32(p.in_l, p.in_r, p.H, p.W, p.ld_in, p.lv[1].L, p.lv[1].R,
-                               p.lv[1].ld, p.lv[0].L, p.lv[0].R, p.lv[0].ld, s));
+      // (rows 2 i, 2 i + 1 of every level-1 row i computed)
+      const LevelBuf& l0 = p.lv[0];
+      const LevelBuf& l1 = p.lv[1];
+      CK(launch_downsample_f32(p.in_l, p.in_r, p.H, p.W, p.ld_in, l1.L, l1.R, l1.ld, l0.L, l0.R,
+                               l0.ld, s, std::min(l1.img_lo, l0.img_lo / 2),
+                               std::max(l1.img_hi, (l0.img_hi + 1) / 2)));
     }
     ++n;
     for (int k = 2; k <= p.K; ++k) {
       const LevelBuf& a = p.lv[k - 1];
       LevelBuf& b = p.lv[k];
-      CK(launch_downsample(a.L, a.R, a.h, a.w, a.ld, b.L, b.R, b.ld, s));
+      CK(launch_downsample(a.L, a.R, a.h, a.w, a.ld, b.L, b.R, b.ld, s, b.img_lo, b.img_hi));
       ++n;
     }
   }
+  // the right offset c of every level: the level-0 right sample at the
+  // image centre (whole input on every rank, so row bands agree)
+  CK(launch_centre_sample(p.user ? nullptr : p.in_r, p.user ? p.lv[0].R : nullptr,
+                          p.user ? p.lv[0].ld : p.ld_in, p.H, p.W, p.cR, s));
+  ++n;
   const bool fork = side != nullptr && evs != nullptr && p.K > 0;
   if (fork) {
     CK(cudaEventRecord(evs[p.K + 1], s));
@@ -316,8 +348,10 @@ int enqueue(mshbm_ctx* ctx, Plan& p, cudaStream_t s, std::vector<StageEvents>* t
   for (int k = p.K; k >= 0; --k) {
     LevelBuf& l = p.lv[k];
     cudaStream_t t = (fork && k < p.K) ? side : s;
-    CK(launch_stats_f32(l.R, l.h, l.w, l.ld, l.b, cfg.sigma_eps, l.muR, l.isR, l.ld, t));
-    CK(launch_prep_staging(l.R, l.ld, l.muR, l.isR, l.ld, l.h, l.w, l.pc, l.Rp, l.Mp, l.ldp, t));
+    CK(launch_stats_f32(l.R, l.h, l.w, l.ld, l.b, cfg.sigma_eps, l.muR, l.isR, l.ld, t,
+                        Sweep4Guard{}, l.st_lo, l.st_hi));
+    CK(launch_prep_staging(l.R, l.ld, l.muR, l.isR, l.ld, l.h, l.w, l.pc, l.Rp, l.Mp, l.ldp, t,
+                           l.st_lo, l.st_hi, p.cR));
     n += 2;
     if (l.muL) {
       // L statistics + sweep4's precision guard (tile flags), then the job
@@ -325,11 +359,13 @@ int enqueue(mshbm_ctx* ctx, Plan& p, cudaStream_t s, std::vector<StageEvents>* t
       Sweep4Guard g;
       g.muR = l.muR;
       g.isR = l.isR;
+      g.cR = p.cR;
       g.tile_h = sweep4_th();
       g.flags = l.flags;
       g.flags_ld = l.flags_ld;
       CK(cudaMemsetAsync(l.flags, 0, sizeof(unsigned) * (l.flags_ld * ((l.h + 1) / 2) + 1), t));
-      CK(launch_stats_f32(l.L, l.h, l.w, l.ld, l.b, cfg.sigma_eps, l.muL, l.isL, l.ld, t, g));
+      CK(launch_stats_f32(l.L, l.h, l.w, l.ld, l.b, cfg.sigma_eps, l.muL, l.isL, l.ld, t, g,
+                          l.st_lo, l.st_hi));
       CK(launch_fixup_list(l.flags, l.flags_ld, sweep4_th(), l.h, l.w, l.rows, l.b, l.fix_list,
                            l.fix_count, t));
       n += 2;
@@ -346,7 +382,9 @@ int enqueue(mshbm_ctx* ctx, Plan& p, cudaStream_t s, std::vector<StageEvents>* t
       if (fork) {
         CK(cudaStreamWaitEvent(s, evs[2 * p.K + 3 + k], 0));   // prefilter of level k+1
       } else {
-        CK(launch_bspline_prefilter(c.c, nullptr, c.h, c.w, c.ld, c.coef, c.ldc, s));
+        int r0, r1;
+        prior_coef_rows(c.h, l.h, l.rows, &r0, &r1);
+        CK(launch_bspline_prefilter(c.c, nullptr, c.h, c.w, c.ld, c.coef, c.ldc, s, r0, r1));
         n += 1;
       }
       CK(launch_prior_eval(c.dmed, c.ld, c.h, c.w, c.coef, c.ldc, l.h, l.w, l.d, cfg.radius,
@@ -385,7 +423,9 @@ int enqueue(mshbm_ctx* ctx, Plan& p, cudaStream_t s, std::vector<StageEvents>* t
       // queue behind the statistics branch's level-0 work)
       cudaStream_t pf = side2 ? side2 : side;
       CK(cudaStreamWaitEvent(pf, evs[p.K + 2 + k], 0));
-      CK(launch_bspline_prefilter(l.c, nullptr, l.h, l.w, l.ld, l.coef, l.ldc, pf));
+      int r0, r1;   // the coefficient rows the next finer level's prior reads
+      prior_coef_rows(l.h, p.lv[k - 1].h, p.lv[k - 1].rows, &r0, &r1);
+      CK(launch_bspline_prefilter(l.c, nullptr, l.h, l.w, l.ld, l.coef, l.ldc, pf, r0, r1));
       CK(cudaEventRecord(evs[2 * p.K + 3 + (k - 1)], pf));
       n += 1;
     }

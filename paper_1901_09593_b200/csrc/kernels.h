@@ -85,29 +85,38 @@ int sweep4_th();   // output rows per sweep4 tile (the guard's tile height)
 inline int staging_margin(int d, int b) { return (d + 16 + b + 40 + 3) / 4 * 4; }
 // Rp = fl32(R - c) (replicate-padded columns), Mp = (muR - c, isR > 0 ? isR :
 // NaN) inside the image and (0, NaN) in the margins; c = muR at the centre.
+// Rows [y0, y1) only (y1 < 0: all) for row bands.  cR: device pointer to the
+// right offset c (pipeline: launch_centre_sample); nullptr: muR at the centre.
 cudaError_t launch_prep_staging(const double* R, int64_t ld, const float* muR, const float* isR,
                                 int64_t lds, int h, int w, int pc, float* Rp, float2* Mp,
-                                int64_t ldp, cudaStream_t s);
+                                int64_t ldp, cudaStream_t s, int y0 = 0, int y1 = -1,
+                                const float* cR = nullptr);
+// *out = level-0 right sample at the image centre (fp32 input or fp64 level)
+cudaError_t launch_centre_sample(const float* in32, const double* in64, int64_t ld, int h,
+                                 int w, float* out, cudaStream_t s);
 
 // ---------------------------------------------------------------- pyramid
 cudaError_t launch_f32_to_f64(const float* a, const float* b, int h, int w,
                               int64_t ld_in, double* oa, double* ob,
                               int64_t ld_out, cudaStream_t s);
 // two images at once when in1/out1 are non-null
+// (output rows [i0, i1) only, i1 < 0: all)
 cudaError_t launch_downsample(const double* in0, const double* in1, int h,
                               int w, int64_t ld_in, double* out0, double* out1,
-                              int64_t ld_out, cudaStream_t s);
+                              int64_t ld_out, cudaStream_t s, int i0 = 0, int i1 = -1);
 // level 1 from the fp32 input, writing the exact fp64 level-0 copy as well
+// (rows 2 i0 .. 2 i1 of it)
 cudaError_t launch_downsample_f32(const float* in0, const float* in1, int h, int w,
                                   int64_t ld_in, double* out0, double* out1, int64_t ld_out,
                                   double* copy0, double* copy1, int64_t ld_copy,
-                                  cudaStream_t s);
+                                  cudaStream_t s, int i0 = 0, int i1 = -1);
 
 // ---------------------------------------------------------------- stats
 // sweep4 precision guard, evaluated by the statistics kernel of L (R's
 // statistics already computed).  sweep4 centres L by one constant per
 // 16 x tile_h tile (the L sample at the tile centre) and R by the level
-// constant c = muR at the image centre, so its fp32 rounding error relative
+// constant c (the level-0 right sample at the image centre), so its fp32
+// rounding error relative
 // to the cost grows with the amplification
 //   A(p) = (|muL(p) - cL| / sigmaL(p) + 3) x (|muR(p) - c| / sigmaR(p) + 3)
 // (measured: cost error ~1.1e-7 A; BASELINE configs A <= 90, the reference's
@@ -118,6 +127,7 @@ constexpr float kSweep4RiskMax = 200.f;
 struct Sweep4Guard {
   const float* muR = nullptr;   // stride lds, as the output maps
   const float* isR = nullptr;
+  const float* cR = nullptr;    // the right offset c (prep_staging's)
   int tile_h = 0;
   unsigned* flags = nullptr;    // nullptr: no guard
   int64_t flags_ld = 0;
@@ -126,7 +136,8 @@ struct Sweep4Guard {
 // window, centred arithmetic in fp64.
 cudaError_t launch_stats_f32(const double* img, int h, int w, int64_t ld,
                              int b, double sigma_eps, float* mu, float* is,
-                             int64_t lds, cudaStream_t s, Sweep4Guard g = Sweep4Guard{});
+                             int64_t lds, cudaStream_t s, Sweep4Guard g = Sweep4Guard{},
+                             int y0 = 0, int y1 = -1);   // rows [y0, y1) (tile-aligned)
 // fp64 mean / sigma maps (dense) for the CostEngine API
 cudaError_t launch_stats_f64(const double* img, int h, int w, int64_t ld,
                              int b, double* mu, double* sigma, cudaStream_t s);
@@ -136,7 +147,11 @@ cudaError_t launch_stats_f64(const double* img, int h, int w, int64_t ld,
 // ((ch+24) x (cw+24), stride ldc); exactly one of c32 / c64 non-null.
 cudaError_t launch_bspline_prefilter(const float* c32, const double* c64,
                                      int ch, int cw, int64_t ldcin,
-                                     double* coef, int64_t ldc, cudaStream_t s);
+                                     double* coef, int64_t ldc, cudaStream_t s, int r0 = 0,
+                                     int r1 = -1);   // padded coefficient rows [r0, r1)
+// padded coefficient rows the prior of fine rows `rows` (h fine rows, ch
+// coarse rows) reads: the 4 spline taps of every fine row, +-2 rows margin
+void prior_coef_rows(int ch, int h, RowBand rows, int* r0, int* r1);
 // pipeline prior: window centres from the coarse disparity + spline coef
 cudaError_t launch_prior_eval(const int16_t* dcoarse, int64_t ldd, int ch,
                               int cw, const double* coef, int64_t ldc, int h,

@@ -39,10 +39,11 @@ __global__ void f32_to_f64_kernel(const float* a, const float* b, int h, int w,
 template <typename T, bool COPY>
 __global__ void downsample_kernel(const T* in0, const T* in1, int h, int w, int64_t ldi,
                                   double* out0, double* out1, int64_t ldo, int oh, int ow,
-                                  double* cp0, double* cp1, int64_t ldc) {
+                                  double* cp0, double* cp1, int64_t ldc, int i0, int i1) {
+  // output rows [i0, i1) only (row bands compute the rows their levels need)
   const int J = blockIdx.x * blockDim.x + threadIdx.x;
-  const int I = blockIdx.y * blockDim.y + threadIdx.y;
-  if (J >= ow || I >= oh) return;
+  const int I = i0 + blockIdx.y * blockDim.y + threadIdx.y;
+  if (J >= ow || I >= oh || I >= i1) return;
   const T* in = blockIdx.z ? in1 : in0;
   double* out = blockIdx.z ? out1 : out0;
   const double k[5] = {1.0 / 16.0, 4.0 / 16.0, 6.0 / 16.0, 4.0 / 16.0, 1.0 / 16.0};
@@ -78,9 +79,9 @@ __global__ void downsample_kernel(const T* in0, const T* in1, int h, int w, int6
 template <bool F64>
 __global__ void stats_kernel(const double* img, int h, int w, int64_t ld,
                              int b, double sigma_eps, float* mu32, float* is32,
-                             double* mu64, double* sg64, int64_t lds) {
+                             double* mu64, double* sg64, int64_t lds, int y_base = 0) {
   const int x = blockIdx.x * blockDim.x + threadIdx.x;
-  const int y = blockIdx.y * blockDim.y + threadIdx.y;
+  const int y = y_base + blockIdx.y * blockDim.y + threadIdx.y;
   if (x >= w || y >= h) return;
   const int h2 = b / 2;
   double s = 0.0;
@@ -152,13 +153,14 @@ __device__ __forceinline__ int reflect_index(int p, int n) {
 template <typename T>
 __global__ void __launch_bounds__(256) bspline_fir_kernel(const T* cin, int ch, int cw,
                                                           int64_t ldcin, double* coef,
-                                                          int64_t ldc) {
+                                                          int64_t ldc, int ty0) {
   extern __shared__ double smem_d[];
   T (*S)[kFE + 1] = reinterpret_cast<T (*)[kFE + 1]>(smem_d);        // [kFE][kFE+1] input
   double (*Tm)[kFE + 1] = reinterpret_cast<double (*)[kFE + 1]>(
       smem_d + (sizeof(T) * kFE * (kFE + 1) + 7) / 8);                 // [kFT][kFE+1] axis-0 pass
   const int nh = ch + 2 * kNpad, nw = cw + 2 * kNpad;
-  const int y0 = blockIdx.y * kFT, x0 = blockIdx.x * kFT;
+  // tile rows ty0.. (row bands: only the coefficient rows their prior reads)
+  const int y0 = (ty0 + blockIdx.y) * kFT, x0 = blockIdx.x * kFT;
   const int lane = threadIdx.x & 31, ty = threadIdx.x >> 5;   // 8 warps
   // stage the doubly extended padded input: P[y][x] = cost[clamp(y-12)][clamp(x-12)].
   // All of a thread's loads are issued before any store, so their latency
@@ -453,7 +455,8 @@ template <int B>
 __global__ void __launch_bounds__(kTX * kTY) stats_tiled_kernel(const double* img, int h, int w,
                                                               int64_t ld, double sigma_eps,
                                                               float* mu32, float* is32,
-                                                              int64_t lds, Sweep4Guard g) {
+                                                              int64_t lds, Sweep4Guard g,
+                                                              int y_base) {
   // Separable box sums of x' and x'^2 (x' = x - c, c the tile's first sample,
   // fp64); windows whose shifted variance cancels to < 1e-9 of E[x'^2]
   // (flat or near-flat) recompute it centred from the tile, so flat blocks
@@ -461,7 +464,9 @@ __global__ void __launch_bounds__(kTX * kTY) stats_tiled_kernel(const double* im
   constexpr int H2 = B / 2, TR = kTY + B - 1, TC = kTX + B - 1;
   __shared__ double T[TR][TC];
   __shared__ double H1[TR][kTX], H2s[TR][kTX];
-  const int x0 = blockIdx.x * kTX, y0 = blockIdx.y * kTY;
+  // tiles stay on the whole-image grid (y_base is a multiple of kTY), so the
+  // per-tile shift c, and with it every output bit, matches whole-level runs
+  const int x0 = blockIdx.x * kTX, y0 = y_base + blockIdx.y * kTY;
   const int tid = threadIdx.y * kTX + threadIdx.x;
   const double c = img[(int64_t)clampi(y0, 0, h - 1) * ld + clampi(x0, 0, w - 1)];
 #pragma unroll 4
@@ -513,7 +518,7 @@ __global__ void __launch_bounds__(kTX * kTY) stats_tiled_kernel(const double* im
                           clampi(tx * 16 + 8, 0, w - 1)];
     const float ir = g.isR[(int64_t)y * lds + x];
     if (ir > 0.f) {
-      const float cR = g.muR[(int64_t)(h / 2) * lds + w / 2];
+      const float cR = *g.cR;
       const float aL = (float)fabs(m1 + c - cL) * (float)(1.0 / sigma) + 3.f;
       const float aR = fabsf(g.muR[(int64_t)y * lds + x] - cR) * ir + 3.f;
       if (aL * aR > kSweep4RiskMax) atomicOr(&g.flags[(int64_t)ty * g.flags_ld + tx], 1u);
@@ -741,11 +746,14 @@ __global__ void __launch_bounds__(kTX * kTY) median_tiled_kernel(
 // ------------------------------------------------------------------ staging
 __global__ void prep_staging_kernel(const double* R, int64_t ld, const float* muR,
                                     const float* isR, int64_t lds, int h, int w, int pc,
-                                    float* Rp, float2* Mp, int64_t ldp) {
+                                    float* Rp, float2* Mp, int64_t ldp, int y0, int y1,
+                                    const float* cR) {
   const int xp = blockIdx.x * blockDim.x + threadIdx.x;   // padded column
-  const int y = blockIdx.y * blockDim.y + threadIdx.y;
-  if (y >= h || xp >= w + 2 * pc) return;
-  const float c = muR[(int64_t)(h / 2) * lds + w / 2];
+  const int y = y0 + blockIdx.y * blockDim.y + threadIdx.y;
+  if (y >= h || y >= y1 || xp >= w + 2 * pc) return;
+  // the level's right offset: the pipeline's constant (valid in any row
+  // band), else (stage API, whole level) the box mean at the image centre
+  const float c = cR ? *cR : muR[(int64_t)(h / 2) * lds + w / 2];
   const int x = xp - pc;
   const int xc = clampi(x, 0, w - 1);
   Rp[(int64_t)y * ldp + xp] = (float)(R[(int64_t)y * ld + xc] - (double)c);
@@ -821,49 +829,72 @@ cudaError_t launch_evaluate(const double* d, const double* gt, const uint8_t* gt
 
 cudaError_t launch_prep_staging(const double* R, int64_t ld, const float* muR, const float* isR,
                                 int64_t lds, int h, int w, int pc, float* Rp, float2* Mp,
-                                int64_t ldp, cudaStream_t s) {
+                                int64_t ldp, cudaStream_t s, int y0, int y1, const float* cR) {
+  if (y1 < 0 || y1 > h) y1 = h;
+  if (y1 <= y0) return cudaSuccess;
   dim3 blk(64, 4);
-  prep_staging_kernel<<<grid2d(w + 2 * pc, h, blk), blk, 0, s>>>(R, ld, muR, isR, lds, h, w, pc,
-                                                                  Rp, Mp, ldp);
+  prep_staging_kernel<<<grid2d(w + 2 * pc, y1 - y0, blk), blk, 0, s>>>(
+      R, ld, muR, isR, lds, h, w, pc, Rp, Mp, ldp, y0, y1, cR);
+  return cudaGetLastError();
+}
+
+// The pipeline's right-image offset c (every level): the level-0 right
+// sample at the image centre, so any row band sees the same constant.
+__global__ void centre_sample_kernel(const float* in32, const double* in64, int64_t ld, int h,
+                                     int w, float* out) {
+  const int64_t o = (int64_t)(h / 2) * ld + w / 2;
+  *out = in32 ? in32[o] : (float)in64[o];
+}
+
+cudaError_t launch_centre_sample(const float* in32, const double* in64, int64_t ld, int h,
+                                 int w, float* out, cudaStream_t s) {
+  centre_sample_kernel<<<1, 1, 0, s>>>(in32, in64, ld, h, w, out);
   return cudaGetLastError();
 }
 
 cudaError_t launch_downsample(const double* in0, const double* in1, int h,
                               int w, int64_t ld_in, double* out0, double* out1,
-                              int64_t ld_out, cudaStream_t s) {
+                              int64_t ld_out, cudaStream_t s, int i0, int i1) {
   const int oh = (h + 1) / 2, ow = (w + 1) / 2;
+  if (i1 < 0 || i1 > oh) i1 = oh;
+  if (i1 <= i0) return cudaSuccess;
   dim3 blk(32, 8);
-  downsample_kernel<double, false><<<grid2d(ow, oh, blk, in1 ? 2 : 1), blk, 0, s>>>(
-      in0, in1, h, w, ld_in, out0, out1, ld_out, oh, ow, nullptr, nullptr, 0);
+  downsample_kernel<double, false><<<grid2d(ow, i1 - i0, blk, in1 ? 2 : 1), blk, 0, s>>>(
+      in0, in1, h, w, ld_in, out0, out1, ld_out, oh, ow, nullptr, nullptr, 0, i0, i1);
   return cudaGetLastError();
 }
 
 cudaError_t launch_downsample_f32(const float* in0, const float* in1, int h, int w,
                                   int64_t ld_in, double* out0, double* out1, int64_t ld_out,
                                   double* copy0, double* copy1, int64_t ld_copy,
-                                  cudaStream_t s) {
+                                  cudaStream_t s, int i0, int i1) {
   const int oh = (h + 1) / 2, ow = (w + 1) / 2;
+  if (i1 < 0 || i1 > oh) i1 = oh;
+  if (i1 <= i0) return cudaSuccess;
   dim3 blk(32, 8);
-  downsample_kernel<float, true><<<grid2d(ow, oh, blk, 2), blk, 0, s>>>(
-      in0, in1, h, w, ld_in, out0, out1, ld_out, oh, ow, copy0, copy1, ld_copy);
+  downsample_kernel<float, true><<<grid2d(ow, i1 - i0, blk, 2), blk, 0, s>>>(
+      in0, in1, h, w, ld_in, out0, out1, ld_out, oh, ow, copy0, copy1, ld_copy, i0, i1);
   return cudaGetLastError();
 }
 
 cudaError_t launch_stats_f32(const double* img, int h, int w, int64_t ld,
                              int b, double sigma_eps, float* mu, float* is,
-                             int64_t lds, cudaStream_t s, Sweep4Guard g) {
+                             int64_t lds, cudaStream_t s, Sweep4Guard g, int y0, int y1) {
+  if (y1 < 0 || y1 > h) y1 = h;
+  if (y1 <= y0) return cudaSuccess;
   dim3 blk(32, 8);
-  const dim3 gr = grid2d(w, h, blk);
+  const int yb = (y0 / kTY) * kTY;   // whole-image tile grid
+  const dim3 gr = grid2d(w, y1 - yb, blk);
   switch (b) {
-    case 3: stats_tiled_kernel<3><<<gr, blk, 0, s>>>(img, h, w, ld, sigma_eps, mu, is, lds, g); return cudaGetLastError();
-    case 5: stats_tiled_kernel<5><<<gr, blk, 0, s>>>(img, h, w, ld, sigma_eps, mu, is, lds, g); return cudaGetLastError();
-    case 7: stats_tiled_kernel<7><<<gr, blk, 0, s>>>(img, h, w, ld, sigma_eps, mu, is, lds, g); return cudaGetLastError();
-    case 9: stats_tiled_kernel<9><<<gr, blk, 0, s>>>(img, h, w, ld, sigma_eps, mu, is, lds, g); return cudaGetLastError();
-    case 11: stats_tiled_kernel<11><<<gr, blk, 0, s>>>(img, h, w, ld, sigma_eps, mu, is, lds, g); return cudaGetLastError();
+    case 3: stats_tiled_kernel<3><<<gr, blk, 0, s>>>(img, h, w, ld, sigma_eps, mu, is, lds, g, yb); return cudaGetLastError();
+    case 5: stats_tiled_kernel<5><<<gr, blk, 0, s>>>(img, h, w, ld, sigma_eps, mu, is, lds, g, yb); return cudaGetLastError();
+    case 7: stats_tiled_kernel<7><<<gr, blk, 0, s>>>(img, h, w, ld, sigma_eps, mu, is, lds, g, yb); return cudaGetLastError();
+    case 9: stats_tiled_kernel<9><<<gr, blk, 0, s>>>(img, h, w, ld, sigma_eps, mu, is, lds, g, yb); return cudaGetLastError();
+    case 11: stats_tiled_kernel<11><<<gr, blk, 0, s>>>(img, h, w, ld, sigma_eps, mu, is, lds, g, yb); return cudaGetLastError();
     default: break;
   }
-  stats_kernel<false><<<grid2d(w, h, blk), blk, 0, s>>>(img, h, w, ld, b, sigma_eps,
-                                                         mu, is, nullptr, nullptr, lds);
+  stats_kernel<false><<<gr, blk, 0, s>>>(img, h, w, ld, b, sigma_eps, mu, is, nullptr, nullptr,
+                                          lds, yb);
   return cudaGetLastError();
 }
 
@@ -877,7 +908,7 @@ cudaError_t launch_stats_f64(const double* img, int h, int w, int64_t ld,
 
 template <typename T>
 cudaError_t launch_fir(const T* cin, int ch, int cw, int64_t ldcin, double* coef, int64_t ldc,
-                       cudaStream_t s) {
+                       cudaStream_t s, int r0, int r1) {
   const int nh = ch + 2 * kNpad, nw = cw + 2 * kNpad;
   constexpr size_t smem = (sizeof(T) * kFE * (kFE + 1) + 7) / 8 * 8 +
                           sizeof(double) * kFT * (kFE + 1);
@@ -888,16 +919,28 @@ cudaError_t launch_fir(const T* cin, int ch, int cw, int64_t ldcin, double* coef
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  const dim3 grid((nw + kFT - 1) / kFT, (nh + kFT - 1) / kFT);
-  bspline_fir_kernel<T><<<grid, 256, smem, s>>>(cin, ch, cw, ldcin, coef, ldc);
+  // coefficient rows [r0, r1) of the padded grid (r1 < 0: all), whole tiles
+  if (r1 < 0 || r1 > nh) r1 = nh;
+  r0 = std::max(r0, 0);
+  if (r1 <= r0) return cudaSuccess;
+  const int t0 = r0 / kFT, t1 = (r1 + kFT - 1) / kFT;
+  const dim3 grid((nw + kFT - 1) / kFT, t1 - t0);
+  bspline_fir_kernel<T><<<grid, 256, smem, s>>>(cin, ch, cw, ldcin, coef, ldc, t0);
   return cudaGetLastError();
 }
 
 cudaError_t launch_bspline_prefilter(const float* c32, const double* c64,
                                      int ch, int cw, int64_t ldcin,
-                                     double* coef, int64_t ldc, cudaStream_t s) {
-  return c32 ? launch_fir(c32, ch, cw, ldcin, coef, ldc, s)
-             : launch_fir(c64, ch, cw, ldcin, coef, ldc, s);
+                                     double* coef, int64_t ldc, cudaStream_t s, int r0, int r1) {
+  return c32 ? launch_fir(c32, ch, cw, ldcin, coef, ldc, s, r0, r1)
+             : launch_fir(c64, ch, cw, ldcin, coef, ldc, s, r0, r1);
+}
+
+void prior_coef_rows(int ch, int h, RowBand rows, int* r0, int* r1) {
+  const double ry = (double)ch / (double)h;
+  const int lo = std::max(rows.lo, 0), hi = std::max(rows.hi, lo + 1);
+  *r0 = (int)floor(((double)lo + 0.5) * ry - 0.5 + kNpad) - 1 - 2;
+  *r1 = (int)floor(((double)(hi - 1) + 0.5) * ry - 0.5 + kNpad) + 3 + 2;
 }
 
 cudaError_t launch_prior_eval(const int16_t* dcoarse, int64_t ldd, int ch,
