@@ -84,7 +84,7 @@ int sweep4_th();   // output rows per sweep4 tile (the guard's tile height)
 // Column margin of the padded staging arrays for search bound d, block b.
 inline int staging_margin(int d, int b) { return (d + 16 + b + 40 + 3) / 4 * 4; }
 // Rp = fl32(R - c) (replicate-padded columns), Mp = (muR - c, isR > 0 ? isR :
-// NaN) inside the image and (0, NaN) in the margins; c = muR at the centre.
+// NaN) inside the image and (0, NaN) in the margins; c: see cR below.
 // Rows [y0, y1) only (y1 < 0: all) for row bands.  cR: device pointer to the
 // right offset c (pipeline: launch_centre_sample); nullptr: muR at the centre.
 cudaError_t launch_prep_staging(const double* R, int64_t ld, const float* muR, const float* isR,
