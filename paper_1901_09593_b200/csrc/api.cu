@@ -256,8 +256,15 @@ int build_plan(mshbm_ctx* ctx, Plan& p) {
 
 // Row ranges per level for a level-0 band [b0, b1) (whole image: b0=0,
 // b1=H).  Level k sweeps rows S_k; level k+1 must provide exact disparities
-// for rows S_k/2 and exact costs within the 66-row reach of the tiled
+// for rows S_k/2 and exact costs within the kCoarseHalo-row reach of the tiled
 // spline prefilter + support around them.
+// Coarse-level halo (rows of level k+1 beyond half of level k's rows): the
+// finer level's prior reads the spline coefficients of rows [lo/2 - 2,
+// hi/2 + 3] (+12 padded), each a 57-tap FIR (+-28 rows) of the coarse costs,
+// and the 2x NN disparity of rows [lo/2, hi/2] from the coarse median (+-2
+// rows of sweep output): <= 33 rows, 40 with margin.
+constexpr int kCoarseHalo = 40;
+
 void plan_rows(Plan& p, int b0, int b1) {
   const int K = p.K;
   for (int k = 0; k <= K; ++k) {
@@ -269,8 +276,8 @@ void plan_rows(Plan& p, int b0, int b1) {
       l.rows.hi = std::min(l.h, b1 + 2);
     } else {
       const RowBand& f = p.lv[k - 1].rows;
-      l.rows.lo = std::max(0, (f.lo >> 1) - 66);
-      l.rows.hi = std::min(l.h, (f.hi >> 1) + 67);
+      l.rows.lo = std::max(0, (f.lo >> 1) - kCoarseHalo);
+      l.rows.hi = std::min(l.h, (f.hi >> 1) + kCoarseHalo + 1);
     }
     l.rows.cnt_lo = own_lo;
     l.rows.cnt_hi = own_hi;
