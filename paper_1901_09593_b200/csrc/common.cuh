@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <utility>
+
 #define MSHBM_DEV __device__ __forceinline__
 
 namespace mshbm {
@@ -11,6 +13,28 @@ namespace mshbm {
 constexpr int kWcNone = -2147483647 - 1;   // "untrusted" window centre
 
 MSHBM_DEV int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
+
+// Programmatic dependent launch: a kernel launched with launch_pdl may be
+// scheduled while its stream predecessor is still finishing; it must call
+// pdl_wait() before touching any memory the predecessor reads or writes
+// (every pipeline kernel does so first thing; a no-op without PDL).
+MSHBM_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t s, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 
 // Warp-wide sum of a 64-bit counter.
 MSHBM_DEV unsigned long long warp_sum_u64(unsigned long long v) {

@@ -40,6 +40,7 @@ template <typename T, bool COPY>
 __global__ void downsample_kernel(const T* in0, const T* in1, int h, int w, int64_t ldi,
                                   double* out0, double* out1, int64_t ldo, int oh, int ow,
                                   double* cp0, double* cp1, int64_t ldc, int i0, int i1) {
+  pdl_wait();
   // output rows [i0, i1) only (row bands compute the rows their levels need)
   const int J = blockIdx.x * blockDim.x + threadIdx.x;
   const int I = i0 + blockIdx.y * blockDim.y + threadIdx.y;
@@ -533,6 +534,7 @@ __global__ void __launch_bounds__(kTX * kTY) prior_eval_tiled_kernel(
     const int16_t* dco, int64_t ldd, int ch, int cw, const double* coef, int64_t ldc, int h,
     int w, int d, int r, double beta, int* wc, int64_t ldw, unsigned long long* counters,
     RowBand band, double ry, double rx) {
+  pdl_wait();
   // 32 fine rows x 32 columns need <= 21 x 21 coefficients (ratio <= 0.52)
   constexpr int CR = 22, CC = 24;
   __shared__ double Cs[CR][CC];
@@ -633,6 +635,7 @@ constexpr int kMY = 32;   // rows per median block (4 per thread)
 __global__ void __launch_bounds__(kTX * kTY) median_tiled_kernel(
     const int16_t* d, const float* c, const uint8_t* low, int64_t ld, int h, int w,
     double alpha, int16_t* out, unsigned long long* counters, RowBand band) {
+  pdl_wait();
   constexpr int TR = kMY + 4, TC = kTX + 4;
   __shared__ float Cs[TR][TC];
   __shared__ int16_t Ds[TR][TC];
@@ -842,6 +845,7 @@ cudaError_t launch_prep_staging(const double* R, int64_t ld, const float* muR, c
 // sample at the image centre, so any row band sees the same constant.
 __global__ void centre_sample_kernel(const float* in32, const double* in64, int64_t ld, int h,
                                      int w, float* out) {
+  pdl_wait();
   const int64_t o = (int64_t)(h / 2) * ld + w / 2;
   *out = in32 ? in32[o] : (float)in64[o];
 }
@@ -859,9 +863,9 @@ cudaError_t launch_downsample(const double* in0, const double* in1, int h,
   if (i1 < 0 || i1 > oh) i1 = oh;
   if (i1 <= i0) return cudaSuccess;
   dim3 blk(32, 8);
-  downsample_kernel<double, false><<<grid2d(ow, i1 - i0, blk, in1 ? 2 : 1), blk, 0, s>>>(
-      in0, in1, h, w, ld_in, out0, out1, ld_out, oh, ow, nullptr, nullptr, 0, i0, i1);
-  return cudaGetLastError();
+  return launch_pdl(downsample_kernel<double, false>, grid2d(ow, i1 - i0, blk, in1 ? 2 : 1), blk,
+                    0, s, in0, in1, h, w, ld_in, out0, out1, ld_out, oh, ow, (double*)nullptr,
+                    (double*)nullptr, (int64_t)0, i0, i1);
 }
 
 cudaError_t launch_downsample_f32(const float* in0, const float* in1, int h, int w,
@@ -872,9 +876,8 @@ cudaError_t launch_downsample_f32(const float* in0, const float* in1, int h, int
   if (i1 < 0 || i1 > oh) i1 = oh;
   if (i1 <= i0) return cudaSuccess;
   dim3 blk(32, 8);
-  downsample_kernel<float, true><<<grid2d(ow, i1 - i0, blk, 2), blk, 0, s>>>(
-      in0, in1, h, w, ld_in, out0, out1, ld_out, oh, ow, copy0, copy1, ld_copy, i0, i1);
-  return cudaGetLastError();
+  return launch_pdl(downsample_kernel<float, true>, grid2d(ow, i1 - i0, blk, 2), blk, 0, s, in0,
+                    in1, h, w, ld_in, out0, out1, ld_out, oh, ow, copy0, copy1, ld_copy, i0, i1);
 }
 
 cudaError_t launch_stats_f32(const double* img, int h, int w, int64_t ld,
@@ -950,10 +953,9 @@ cudaError_t launch_prior_eval(const int16_t* dcoarse, int64_t ldd, int ch,
                               RowBand rows, cudaStream_t s) {
   dim3 blk(32, 8);
   const dim3 g((w + 31) / 32, (rows.hi - rows.lo + kPY - 1) / kPY);
-  prior_eval_tiled_kernel<<<g, blk, 0, s>>>(dcoarse, ldd, ch, cw, coef, ldc, h, w, d, radius,
-                                            beta, wc, ldw, counters, rows, (double)ch / (double)h,
-                                            (double)cw / (double)w);
-  return cudaGetLastError();
+  return launch_pdl(prior_eval_tiled_kernel, g, blk, 0, s, dcoarse, ldd, ch, cw, coef, ldc, h, w,
+                    d, radius, beta, wc, ldw, counters, rows, (double)ch / (double)h,
+                    (double)cw / (double)w);
 }
 
 cudaError_t launch_prior_maps(const double* d_hat, const double* c_hat, int h,
@@ -982,7 +984,9 @@ cudaError_t launch_median_pipeline(const int16_t* d, const float* c,
                                    cudaStream_t s) {
   dim3 blk(32, 8);
   const dim3 g((w + 31) / 32, (rows.hi - rows.lo + kMY - 1) / kMY);
-  median_tiled_kernel<<<g, blk, 0, s>>>(d, c, low, ld, h, w, alpha, out, counters, rows);
+  cudaError_t e = launch_pdl(median_tiled_kernel, g, blk, 0, s, d, c, low, ld, h, w, alpha, out,
+                             counters, rows);
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 

@@ -526,6 +526,7 @@ __device__ __forceinline__ void sweep2_body(const SweepArgs& a, const int bx, co
 // guard-flagged tiles), so an empty list costs one short wave.
 template <int B, int DIR, int ZC, int NR, int MINB, int PK>
 __global__ void __launch_bounds__(NR * 32, MINB) sweep2_kernel(const SweepArgs a) {
+  pdl_wait();
   // one inlined copy of the body (instruction cache): the plain launch is a
   // one-iteration loop over its own block
   const bool lm = a.fixup && a.fix_list != nullptr;
@@ -562,8 +563,7 @@ cudaError_t launch2(const SweepArgs& a, cudaStream_t s) {
     b.fix_nbx = grid.x;
     grid = dim3(std::min<unsigned>(grid.x * grid.y, 2 * 148), 1);
   }
-  sweep2_kernel<B, DIR, ZC, NR, MINB, PK><<<grid, NR * 32, smem, s>>>(b);
-  return cudaGetLastError();
+  return launch_pdl(sweep2_kernel<B, DIR, ZC, NR, MINB, PK>, grid, dim3(NR * 32), smem, s, b);
 }
 
 int g_v2 = -1;

@@ -203,6 +203,7 @@ __device__ __forceinline__ void row_step(
 
 template <int B, int DIR, int G>
 __global__ void __launch_bounds__(kNWMax * 32, 2) sweep4_kernel(const SweepArgs a, const int th) {
+  pdl_wait();
   using SL = S4Layout<B, G>;
   constexpr int H2 = B / 2, NV = SL::NV, NVP = SL::NVP, NC = SL::NC, RB = SL::RB;
   extern __shared__ float4 smem4[];
@@ -538,8 +539,7 @@ cudaError_t launch4(const SweepArgs& a, cudaStream_t s) {
   SweepArgs b = a;
   b.rows.lo = (a.rows.lo / th) * th;
   dim3 grid((a.W + kTW - 1) / kTW, (b.rows.hi - b.rows.lo + th - 1) / th);
-  sweep4_kernel<B, DIR, G><<<grid, 32 * nw, lay.bytes, s>>>(b, th);
-  return cudaGetLastError();
+  return launch_pdl(sweep4_kernel<B, DIR, G>, grid, dim3(32 * nw), lay.bytes, s, b, th);
 }
 
 }  // namespace
