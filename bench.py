@@ -457,7 +457,7 @@ def run_ours(args, cfg):
 
 # dram__bytes_read.sum + dram__bytes_write.sum of the level-0 sweep launch from
 # the committed ncu --set full captures (profiles/), per config
-TRAFFIC = {"C2": 43131648 + 583424}   # r01_sweep4_c2_ncu.md (ncu --set full, L0 sweep)
+TRAFFIC = {"C2": 43133696 + 835584}   # r01_sweep4_c2_ncu.md (ncu --set full, L0 sweep)
 
 
 def sweep_kernel_name(level) -> str:
