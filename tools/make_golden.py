@@ -375,6 +375,9 @@ def main():
         full_case("C2", CONFIGS["C2"], CONFIGS["C2"].seed)
         full_case("C4", CONFIGS["C4"], CONFIGS["C4"].seed)
         return
+    if sys.argv[1:] == ["full_C3"]:   # full-size C3 (about 9 min, 8 GB)
+        full_case("C3", CONFIGS["C3"], CONFIGS["C3"].seed)
+        return
     scoring_cases()
     formats_cases()
     stage_cases()
