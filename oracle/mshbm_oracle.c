@@ -211,7 +211,7 @@ static int engine_init(Engine* e, const double* L, const double* R, int h, int w
 }
 
 /* Dense DSI row i: out[z*w + j] = rho(i, j, z) for z = 0..d (zncc.py:271-287).
- * vbuf: scratch of pw doubles. */
+ * vbuf: scratch of 2 * (pw + 2d + 8) doubles. */
 static void dsi_row(const Engine* e, int i, double* out, double* vbuf) {
     const int w = e->w, b = e->b, pw = e->pw, d = e->d;
     const double area = (double)(b * b);
@@ -237,15 +237,18 @@ static void dsi_row(const Engine* e, int i, double* out, double* vbuf) {
             const double* rr = e->rp + (size_t)(i + p) * pw + off;
             for (int c = c0; c < c1; ++c) vbuf[c] += lr[c] * rr[c];
         }
+        /* cross(j) = sum_t V(j + t), accumulated t-outer (vectorises over j) */
+        double* cr = vbuf + pw + 2 * d + 8;
+        for (int j = j0; j < j1; ++j) cr[j] = vbuf[j];
+        for (int t = 1; t < b; ++t)
+            for (int j = j0; j < j1; ++j) cr[j] += vbuf[j + t];
         for (int j = j0; j < j1; ++j) {
-            double cross = 0.0;
-            for (int t = 0; t < b; ++t) cross += vbuf[j + t];
             int q = j + off;
-            if (okl[j] && okr[q]) {
-                double cov = cross / area - mul[j] * mur[q];
-                double r = cov / (sl[j] * sr[q]);
-                o[j] = r < -1.0 ? -1.0 : (r > 1.0 ? 1.0 : r);
-            }
+            double cov = cr[j] / area - mul[j] * mur[q];
+            double den = sl[j] * sr[q];
+            double r = (okl[j] & okr[q]) ? cov / den : -1.0;
+            r = r < -1.0 ? -1.0 : r;
+            o[j] = r > 1.0 ? 1.0 : r;
         }
     }
 }
@@ -323,60 +326,75 @@ static int upsample_prior(const double* dc, const double* cc, int ch, int cw, in
     return ORC_OK;
 }
 
-/* selection of one row from its dense DSI row (matcher.py:263-320) */
+/* selection of one row from its dense DSI row (matcher.py:263-320).  z
+ * runs in the outer loop (the row is plane-major); bz/bc: scratch of w. */
 static void select_row(const Engine* e, const double* row, int i, const int* wsz,
-                       const double* dhat, int radius, double* dsel, double* csel) {
+                       const double* dhat, int radius, double* dsel, double* csel,
+                       int* bz, double* bc) {
     const int w = e->w, d = e->d;
+    const int* ws = wsz + (size_t)i * w;
+    const double* dh = dhat ? dhat + (size_t)i * w : NULL;
     for (int j = 0; j < w; ++j) {
-        size_t p = (size_t)i * w + j;
-        double bc = -2.0;
-        int bz = 0;
-        if (wsz[p] < 0) {                /* full search: first argmax */
-            bc = row[j];
-            for (int z = 1; z <= d; ++z)
-                if (row[(size_t)z * w + j] > bc) { bc = row[(size_t)z * w + j]; bz = z; }
-        } else {                          /* ascending window, strict > vs -2 */
-            long long ctr = (long long)dhat[p];
-            for (long long z = ctr - radius; z <= ctr + radius; ++z) {
-                if (z < 0 || z > d) continue;
-                double c = row[(size_t)z * w + j];
-                if (c > bc) { bc = c; bz = (int)z; }
+        bz[j] = 0;
+        bc[j] = ws[j] < 0 ? row[j] : -2.0;        /* full search: z = 0 is the first max */
+    }
+    for (int z = 0; z <= d; ++z) {
+        const double* rz = row + (size_t)z * w;
+        for (int j = 0; j < w; ++j) {
+            if (ws[j] < 0) {
+                if (z > 0 && rz[j] > bc[j]) { bc[j] = rz[j]; bz[j] = z; }
+            } else {                               /* ascending window, strict > vs -2 */
+                long long ctr = (long long)dh[j];
+                if (z >= ctr - radius && z <= ctr + radius && rz[j] > bc[j]) { bc[j] = rz[j]; bz[j] = z; }
             }
         }
-        dsel[p] = (double)bz;
-        csel[p] = bc;
+    }
+    for (int j = 0; j < w; ++j) {
+        dsel[(size_t)i * w + j] = (double)bz[j];
+        csel[(size_t)i * w + j] = bc[j];
     }
 }
 
 /* refinement of row i's low pixels (matcher.py:196-233); the ring holds
- * the DSI rows i-1, i, i+1 at slots (row % 3). */
+ * the DSI rows i-1, i, i+1 at slots (row % 3).  The clipped 3x3 sum of each
+ * pixel accumulates in the reference's order (di outer, dj inner); z runs
+ * in the outer loop.  bz/bs/acc: scratch of w. */
 static void refine_row(const Engine* e, const double* ring, size_t rowsz, int i, double alpha,
                        const double* dsel, const double* csel, double* dref, double* cref,
-                       double* sum) {
+                       int* bz, double* bs, double* acc) {
     const int h = e->h, w = e->w, d = e->d;
+    const double* cs = csel + (size_t)i * w;
+    int any = 0;
     for (int j = 0; j < w; ++j) {
-        size_t p = (size_t)i * w + j;
-        dref[p] = dsel[p];
-        cref[p] = csel[p];
-        if (!(csel[p] <= alpha)) continue;
-        for (int z = 0; z <= d; ++z) sum[z] = 0.0;
-        double members = 0.0;
+        dref[(size_t)i * w + j] = dsel[(size_t)i * w + j];
+        cref[(size_t)i * w + j] = cs[j];
+        any |= cs[j] <= alpha;
+    }
+    if (!any) return;
+    for (int z = 0; z <= d; ++z) {
+        for (int j = 0; j < w; ++j) acc[j] = 0.0;
         for (int di = -1; di <= 1; ++di) {
             int qi = i + di;
             if (qi < 0 || qi >= h) continue;
-            const double* row = ring + (size_t)(qi % 3) * rowsz;
-            for (int dj = -1; dj <= 1; ++dj) {
-                int qj = j + dj;
-                if (qj < 0 || qj >= w) continue;
-                for (int z = 0; z <= d; ++z) sum[z] += row[(size_t)z * w + qj];
-                members += 1.0;
+            const double* rz = ring + (size_t)(qi % 3) * rowsz + (size_t)z * w;
+            acc[0] += rz[0];                              /* j = 0: dj = 0, +1 */
+            if (w > 1) acc[0] += rz[1];
+            for (int j = 1; j < w - 1; ++j) {
+                double t = acc[j] + rz[j - 1];
+                t += rz[j];
+                acc[j] = t + rz[j + 1];
             }
+            if (w > 1) { acc[w - 1] += rz[w - 2]; acc[w - 1] += rz[w - 1]; }
         }
-        int bz = 0;
-        double bs = sum[0];
-        for (int z = 1; z <= d; ++z) if (sum[z] > bs) { bs = sum[z]; bz = z; }
-        dref[p] = (double)bz;
-        cref[p] = sum[bz] / members;
+        for (int j = 0; j < w; ++j)
+            if (z == 0 || acc[j] > bs[j]) { bs[j] = acc[j]; bz[j] = z; }
+    }
+    for (int j = 0; j < w; ++j) {
+        if (!(cs[j] <= alpha)) continue;
+        int rows_in = 1 + (i > 0) + (i < h - 1);
+        int cols_in = 1 + (j > 0) + (j < w - 1);
+        dref[(size_t)i * w + j] = (double)bz[j];
+        cref[(size_t)i * w + j] = bs[j] / (double)(rows_in * cols_in);
     }
 }
 
@@ -413,10 +431,12 @@ static int process_level(const Engine* e, const double* dhat, const double* chat
     {
         size_t rowsz = (size_t)(d + 1) * w;
         double* ring = (double*)malloc(sizeof(double) * rowsz * 3);
-        double* vbuf = (double*)malloc(sizeof(double) * (size_t)(e->pw + 2 * d + 8));
-        double* sum = (double*)malloc(sizeof(double) * (size_t)(d + 1));
+        double* vbuf = (double*)malloc(sizeof(double) * (size_t)(2 * (e->pw + 2 * d + 8)));
+        int* sbz = (int*)malloc(sizeof(int) * (size_t)w);
+        double* sbc = (double*)malloc(sizeof(double) * (size_t)w);
+        double* sacc = (double*)malloc(sizeof(double) * (size_t)w);
         int have[3] = {-1, -1, -1};
-        if (!ring || !vbuf || !sum) {
+        if (!ring || !vbuf || !sbz || !sbc || !sacc) {
             #pragma omp atomic write
             err = ORC_ENOMEM;
         }
@@ -431,14 +451,14 @@ static int process_level(const Engine* e, const double* dhat, const double* chat
                 int slot = i % 3;
                 if (have[slot] != i) { dsi_row(e, i, ring + slot * rowsz, vbuf); have[slot] = i; }
                 if (i >= r0 && i < r1)
-                    select_row(e, ring + slot * rowsz, i, wsz, dhat, radius, dsel, csel);
+                    select_row(e, ring + slot * rowsz, i, wsz, dhat, radius, dsel, csel, sbz, sbc);
                 if (i - 1 >= r0 && i - 1 < r1)
-                    refine_row(e, ring, rowsz, i - 1, alpha, dsel, csel, dref, c_out, sum);
+                    refine_row(e, ring, rowsz, i - 1, alpha, dsel, csel, dref, c_out, sbz, sbc, sacc);
             }
             if (hi == r1 - 1)
-                refine_row(e, ring, rowsz, r1 - 1, alpha, dsel, csel, dref, c_out, sum);
+                refine_row(e, ring, rowsz, r1 - 1, alpha, dsel, csel, dref, c_out, sbz, sbc, sacc);
         }
-        free(ring); free(vbuf); free(sum);
+        free(ring); free(vbuf); free(sbz); free(sbc); free(sacc);
     }
     if (err) { free(dsel); free(csel); free(dref); free(wsz); return err; }
     /* counters */
@@ -582,7 +602,7 @@ int mshbm_oracle_match_coarsest(const double* left, const double* right, int h, 
     #pragma omp parallel
     {
         double* row = (double*)malloc(sizeof(double) * (size_t)(d_max + 1) * w);
-        double* vbuf = (double*)malloc(sizeof(double) * (size_t)(e.pw + 2 * d_max + 8));
+        double* vbuf = (double*)malloc(sizeof(double) * (size_t)(2 * (e.pw + 2 * d_max + 8)));
         if (!row || !vbuf) {
             #pragma omp atomic write
             rc = ORC_ENOMEM;

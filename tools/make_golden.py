@@ -178,6 +178,23 @@ def full_case(name, cfg, seed):
          ref_seconds=np.array(dt))
 
 
+def crop_case(name, cfg, height, width):
+    """A large crop of a BASELINE config through the real reference, stored
+    like full_case (outputs only; the tests regenerate the images with
+    make_pair(cfg, height=, width=))."""
+    left, right, _ = make_pair(cfg, height=height, width=width)
+    rcfg = ref.MatchConfig(d_max=cfg.d_max, levels=cfg.levels, block=cfg.block)
+    t0 = time.perf_counter()
+    d, c, tr = pipeline_r(left, right, rcfg, cfg.radius)
+    dt = time.perf_counter() - t0
+    print(f"crop_{name}: {left.shape} {dt:.1f}s total_evals={tr.total_evals}")
+    save(f"crop_{name}_{width}x{height}.npz", disparity=d.astype(np.int16),
+         cost=c.astype(np.float32), counts=counts_array(tr), seed=np.array(cfg.seed),
+         shape=np.array([height, width]),
+         params=np.array([cfg.d_max, cfg.levels, cfg.block, cfg.radius, 0]),
+         ref_seconds=np.array(dt))
+
+
 def stage_cases():
     rng = np.random.default_rng(20261019)
     out = {}
@@ -374,6 +391,9 @@ def main():
     if sys.argv[1:] == ["full"]:   # full-size C2 and one C4 pair (minutes)
         full_case("C2", CONFIGS["C2"], CONFIGS["C2"].seed)
         full_case("C4", CONFIGS["C4"], CONFIGS["C4"].seed)
+        return
+    if sys.argv[1:] == ["crop_C5"]:   # 2048x1536 C5 crop (about 16 min, 35 GB)
+        crop_case("C5", CONFIGS["C5"], 1536, 2048)
         return
     if sys.argv[1:] == ["full_C3"]:   # full-size C3 (about 9 min, 8 GB)
         full_case("C3", CONFIGS["C3"], CONFIGS["C3"].seed)
