@@ -1,12 +1,13 @@
 """Benchmark: MSHBM disparity hot path on B200 (BASELINE.json metric).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2]
-                    [--impl ours|reference] [--no-cpu-baseline]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3]
+                    [--impl ours|reference] [--no-cpu-baseline] [--no-sharded]
 
-One "step" = one stereo pair of the workload (default BASELINE config C2,
-1472x992, D=144, 4 pyramid levels, 7x7 window, prior radius 2) through the
-whole hot path: pyramid -> per-level stats -> fused ZNCC sweep + WTA +
-refinement -> selective median -> B-spline prior for the next level.
+One "step" = one stereo pair of the workload through the whole hot path:
+pyramid -> per-level stats -> fused ZNCC sweep + WTA + refinement ->
+selective median -> B-spline prior for the next level.  The default
+workload is BASELINE C3 (2944x1984, D=288, 5 pyramid levels, 9x9 window,
+prior radius 3), the largest single-GPU config.
 
 value  : full-search-equivalent Mpixel*disparities/s = N * W*H*(D+1) / t,
          inputs resident in HBM, CUDA events on the launching stream, L2
@@ -14,13 +15,19 @@ value  : full-search-equivalent Mpixel*disparities/s = N * W*H*(D+1) / t,
 e2e    : the same metric through the C-ABI call a user makes
          (mshbm_run_pipeline, MSHBM_IO_HOST) from pinned host buffers:
          H2D of both images + D2H of disparity (int16) and cost (fp32)
-         inside the timed region.
-N > 1  : torchrun, one rank per GPU, each rank its own pair (seed + rank):
-         independent pairs shard with no data-path collective ("weak").
---impl reference: the CPU oracle port (oracle/mshbm_oracle.py, the
-         reference's own numpy algorithm restated; the reference package is
-         pure Python and cannot travel to the box) on a bounded crop of the
-         same workload, rank 0 only.
+         inside the timed region.  e2e_python: the drop-in
+         paper_1901_09593_b200.run_pipeline on numpy arrays (float64 maps
+         returned), host wall clock.
+sharded: BASELINE C4 (64 pairs sharded round-robin over the N ranks) and C5
+         (one 8192x6144 pair in N row bands, gathered to rank 0) at this N:
+         the configs north_star scales; pairs/s and MPD/s, max over ranks.
+--gpus N without torchrun: re-executes itself under torch.distributed.run
+         (one process per GPU, 127.0.0.1 rendezvous).
+--impl reference: the CPU oracle port (oracle/mshbm_oracle.c, the
+         reference's run_pipeline restated in C/OpenMP and pinned bit-exact to
+         the reference's own full-size outputs; the reference package is pure
+         Python and cannot travel to the box) on the FULL workload pair with
+         every host core, rank 0 only.
 """
 
 from __future__ import annotations
@@ -126,46 +133,143 @@ def dist_init():
     return ws, rank, local
 
 
-def cpu_oracle_run(cfg, seed, workers):
-    """Time the CPU oracle port on the bounded crop sample; returns (s, pde)."""
+def cpu_info() -> dict:
+    import numpy
+    try:
+        import scipy
+        scipy_v = scipy.__version__
+    except ImportError:
+        scipy_v = None
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    env = {k: os.environ[k] for k in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS",
+                                      "MKL_NUM_THREADS", "OMP_PROC_BIND") if k in os.environ}
+    return {"cpu_model": model, "nproc": os.cpu_count(), "numpy": numpy.__version__,
+            "scipy": scipy_v, "thread_env": env}
+
+
+def c_oracle_run(cfg, seed, threads, height=None, width=None):
+    """Full pair of ``cfg`` through the C/OpenMP oracle; returns (s, counts)."""
+    from oracle import c_oracle as CO
+    CO.build()
+    left, right, _ = make_pair(cfg, seed=seed, height=height, width=width)
+    t0 = time.perf_counter()
+    _, _, counts = CO.run_pipeline(left, right, cfg.d_max, cfg.levels, cfg.block,
+                                   radius=cfg.radius, threads=threads)
+    return time.perf_counter() - t0, counts
+
+
+def _pool_pair(i):
+    dt, _ = c_oracle_run(CONFIGS["C4"], CONFIGS["C4"].seed + i, 1)
+    return dt
+
+
+def c4_pool(nproc: int) -> dict:
+    """C4 pairs, one per process, multiprocessing.Pool(nproc)."""
+    import multiprocessing as mp
+    ctx = mp.get_context("fork")
+    t0 = time.perf_counter()
+    with ctx.Pool(nproc) as pool:
+        per = pool.map(_pool_pair, range(nproc))
+    wall = time.perf_counter() - t0
+    return {"pairs_per_s_nproc": nproc / wall, "pairs_per_s_1core": 1.0 / statistics.mean(per),
+            "processes": nproc, "pairs": nproc,
+            "impl": "oracle/mshbm_oracle.c, 1 thread per process"}
+
+
+def numpy_port_sample(cfg, workers):
+    """The numpy restatement (the reference's own gather/einsum algorithm) on
+    a bounded crop; returns (s, full-search PDE of the crop)."""
     from oracle import mshbm_oracle as O
     h, w = CPU_SAMPLE
-    left, right, _ = make_pair(cfg, seed=seed, height=h, width=w)
+    left, right, _ = make_pair(cfg, seed=cfg.seed, height=h, width=w)
     t0 = time.perf_counter()
     O.run_pipeline(left, right, cfg.d_max, cfg.levels, cfg.block, radius=cfg.radius,
                    workers=workers)
-    dt = time.perf_counter() - t0
-    return dt, h * w * (cfg.d_max + 1)
+    return time.perf_counter() - t0, h * w * (cfg.d_max + 1)
+
+
+def reference_cached() -> dict:
+    """Wall times of the REAL reference run_pipeline on the full BASELINE
+    pairs, measured once in the build container while making the goldens
+    (tools/make_golden.py; tests/golden/full_*.npz ref_seconds)."""
+    out = {"where": "build container: 8-core Intel Xeon, Python 3.12.3, numpy 2.3.5, "
+                    "scipy 1.18.1, reference run_pipeline (radius-generalised driver), "
+                    "workers=1 (workers only parallelise the coarsest level, cli.py:81-84)"}
+    for name in ("C2", "C3", "C4"):
+        path = os.path.join(ROOT, "tests", "golden", f"full_{name}.npz")
+        if os.path.exists(path):
+            g = np.load(path)
+            cfg = CONFIGS[name]
+            t = float(g["ref_seconds"])
+            out[name] = {"seconds": t, "mpd_per_s": cfg.full_search_pde / t / 1e6}
+    return out
+
+
+def cpu_baseline(cfg) -> dict:
+    nproc = os.cpu_count() or 1
+    dt, counts = c_oracle_run(cfg, cfg.seed, nproc)
+    base = {"value": cfg.full_search_pde / dt / 1e6, "unit": UNIT, "cores": nproc,
+            "kind": "port", "seconds": dt,
+            "sample": f"one full {cfg.name} pair ({cfg.width}x{cfg.height}, D={cfg.d_max}, "
+                      f"levels={cfg.levels + 1}, b={cfg.block}, r={cfg.radius}) through "
+                      "oracle/mshbm_oracle.c (C/OpenMP fp64 restatement of run_pipeline, "
+                      "bit-exact to the reference's full-size outputs), all host threads",
+            "evaluated_mpd_per_s": float(counts[:, 9].sum() + counts[:, 11].sum()) / dt / 1e6}
+    base.update(cpu_info())
+    base["reference_cached"] = reference_cached()
+    try:
+        pt, pde = numpy_port_sample(cfg, nproc)
+        base["numpy_port_sample"] = {"value": pde / pt / 1e6, "seconds": pt,
+                                     "sample": f"{CPU_SAMPLE[1]}x{CPU_SAMPLE[0]} crop through "
+                                               "oracle/mshbm_oracle.py (numpy, the "
+                                               "reference's gather/einsum algorithm)"}
+    except Exception as e:   # noqa: BLE001 (reported, not fatal)
+        base["numpy_port_sample"] = {"error": repr(e)}
+    try:
+        base["c4_pool"] = c4_pool(nproc)
+    except Exception as e:   # noqa: BLE001
+        base["c4_pool"] = {"error": repr(e)}
+    return base
 
 
 def run_reference(args, cfg):
     ws, rank, _ = dist_init()
     if rank != 0:
         return
-    workers = os.cpu_count() or 1
-    times = []
-    pde = 0
-    # each step is a bounded CPU sample (~3-4 s); cap the count so the arm
-    # ends within a few minutes whatever --steps the GPU arm uses
-    args.steps = max(1, min(args.steps, 20))
+    threads = os.cpu_count() or 1
+    c_oracle_run(cfg, cfg.seed, threads, height=256, width=384)   # build + page-in
+    times, counts = [], None
+    # each step is one full pair (a few seconds on the box's cores); cap the
+    # count so the arm ends within a few minutes whatever --steps says
+    args.steps = max(1, min(args.steps, 10))
     args.warmup = min(args.warmup, 1)
     for k in range(args.warmup + args.steps):
-        dt, pde = cpu_oracle_run(cfg, cfg.seed, workers)
+        dt, counts = c_oracle_run(cfg, cfg.seed, threads)
         if k >= args.warmup:
             times.append(dt)
     t = statistics.mean(times)
-    val = pde / t / 1e6
-    h, w = CPU_SAMPLE
+    val = cfg.full_search_pde / t / 1e6
     line = {
         "impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": ws,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": f"synthetic BASELINE generator, {cfg.name} params, {w}x{h} crop, seed {cfg.seed}",
+        "data": f"synthetic BASELINE generator, {cfg.name}, seed {cfg.seed} (full pair)",
         "config": workload_desc(cfg),
-        "cpu_baseline": {"value": val, "unit": UNIT, "cores": workers, "kind": "port",
-                         "sample": f"{w}x{h} crop of {cfg.name} (D={cfg.d_max}, "
-                                   f"levels={cfg.levels + 1}, b={cfg.block}, r={cfg.radius}) "
-                                   "through oracle/mshbm_oracle.run_pipeline (numpy fp64)"},
+        "cpu_baseline": dict({"value": val, "unit": UNIT, "cores": threads, "kind": "port",
+                              "sample": f"one full {cfg.name} pair per step through "
+                                        "oracle/mshbm_oracle.c (C/OpenMP restatement of the "
+                                        "reference run_pipeline, bit-exact to its full-size "
+                                        "outputs), all host threads"}, **cpu_info()),
+        "evaluated_mpd_per_s": float(counts[:, 9].sum() + counts[:, 11].sum()) / t / 1e6,
+        "reference_cached": reference_cached(),
         "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -307,20 +411,59 @@ class Workload:
         lib.check(st, self.ctx)
 
 
+def sweep4_row_step_flops(b: int) -> int:
+    """Implemented FP32 flops of one sweep4 row step of one lane (one z) over
+    the 16 output pixels of a CTA tile (csrc/sweep4.cu, FFMA = 2 flops):
+      V slide   2 FFMA per tile column, NV = 16 + b + 1 columns   4 NV
+      S sums    two sliding chains over the NC = 18 cost columns  2 (b + 16)
+      cost      FFMA + FMUL + FFMA.sat per cost column            5 NC
+      WTA       per pixel: key FADD; 3x3: 2 FADD + FADD + FFMA;
+                vertical 3-sum carry FADD                         16 x 7
+    Divided by 16 this is the implemented count per (pixel, disparity) of
+    the dense sweep (SURVEY 8d asks a sliding-sum design to declare its own
+    count); tools/flop_check.py checks it against ncu's FP32 instruction
+    counts."""
+    nv, nc = 16 + b + 1, 18
+    return 4 * nv + 2 * (b + 16) + 5 * nc + 16 * 7
+
+
+def impl_flops_per_pde(kernel: str, b: int) -> float:
+    if kernel == "sweep4_kernel":
+        return sweep4_row_step_flops(b) / 16.0
+    # sweep2: b^2 + b + 1 FMAs per two pixels + normalise / WTA (~11 flops)
+    return (b * b + b + 1) + 11.0
+
+
+def measure(wl, steps, flush, stream, barrier, max_over_ranks, use_flush=True):
+    """Average device ms per step of ``wl.step`` (CUDA events, max over ranks)."""
+    import torch
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(steps)]
+    barrier()
+    for k in range(steps):
+        if use_flush:
+            flush.fill_(k & 0xFF)
+        ev[k][0].record(stream)
+        wl.step()
+        ev[k][1].record(stream)
+    barrier()
+    return max_over_ranks(sum(a.elapsed_time(b) for a, b in ev) / steps)
+
+
 def run_ours(args, cfg):
     import torch
     import torch.distributed as dist
 
     ws, rank, local = dist_init()
     if ws > 1:
-        dist.init_process_group("nccl", init_method="env://")
+        dist.init_process_group("nccl", init_method="env://",
+                                device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
 
     import paper_1901_09593_b200 as gpu
     from paper_1901_09593_b200 import _lib
 
-    gpu.matcher.STAGE_TIMING = False
     wl = Workload(cfg, gpu, _lib, dev, ws, rank)
     stream = torch.cuda.current_stream(dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
@@ -349,18 +492,9 @@ def run_ours(args, cfg):
     # ---- device-resident timed region
     ctx = _lib.context(local)
     n0 = _lib.lib().mshbm_launch_count(ctx)
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-          for _ in range(args.steps)]
     with ClockSampler(local) as clocks:
-        barrier()
-        for k in range(args.steps):
-            flush.fill_(k & 0xFF)
-            ev[k][0].record(stream)
-            wl.step()
-            ev[k][1].record(stream)
-        barrier()
+        ms = measure(wl, args.steps, flush, stream, barrier, max_over_ranks)
     launches = int(_lib.lib().mshbm_launch_count(ctx) - n0)
-    ms = max_over_ranks(sum(a.elapsed_time(b) for a, b in ev) / args.steps)
     value = wl.units / (ms * 1e-3) / 1e6
 
     # ---- end to end through the C ABI with host buffers (pinned)
@@ -380,6 +514,7 @@ def run_ours(args, cfg):
     e2e_value = wl.units / (ems * 1e-3) / 1e6
     # ---- pipelined end to end (pair workloads): consecutive pairs in flight
     pipe = None
+    epy = None
     if wl.kind == "pair":
         wl.e2e_pipelined(stream, 8)   # warm-up: slot plans and graphs
         pms_ = max_over_ranks(min(wl.e2e_pipelined(stream, e2e_steps) for _ in range(2)))
@@ -388,9 +523,22 @@ def run_ours(args, cfg):
                 "steps": e2e_steps,
                 "path": "C ABI mshbm_run_batch(MSHBM_IO_HOST, 4 slot streams): each step's "
                         "copies overlap other steps' compute; host wall clock around the call"}
+        # ---- the drop-in itself: numpy in, float64 numpy maps + trace out
+        for _ in range(2):
+            gpu.run_pipeline(wl.left, wl.right, wl.mc)
+        py_steps = max(3, min(args.steps, 20))
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(py_steps):
+            gpu.run_pipeline(wl.left, wl.right, wl.mc)
+        pyms = max_over_ranks((time.perf_counter() - t0) * 1e3 / py_steps)
+        epy = {"value": wl.units / (pyms * 1e-3) / 1e6, "unit": UNIT, "ms_per_step": pyms,
+               "steps": py_steps, "h2d_bytes_per_step": wl.h2d,
+               "d2h_bytes_per_step": wl.d2h,
+               "path": "paper_1901_09593_b200.run_pipeline(numpy float32 L, R, MatchConfig) -> "
+                       "(float64 disparity, float64 cost, PipelineTrace); host wall clock"}
 
     # ---- roofline of the dominant kernel (level-0 sweep), live CUDA events
-    gpu.matcher.STAGE_TIMING = True
     sweep_ms = []
     for _ in range(3 if cfg.name == "C5" else 5):
         flush.fill_(1)
@@ -400,22 +548,55 @@ def run_ours(args, cfg):
     tf = C.c_double()
     pms = C.c_double()
     _lib.check(_lib.lib().mshbm_probe_fp32_peak(local, 20000, C.byref(tf), C.byref(pms)))
-    alg_flops = l0.evals * flops_per_pde(l0.block)
-    achieved = alg_flops / (sweep_ms * 1e-3) / 1e12
-    dense_flops = l0.pixels * (l0.d_max + 1) * flops_per_pde(l0.block)
+    kname = sweep_kernel_name(l0)
+    dense_pde = l0.pixels * (l0.d_max + 1)
+    impl = impl_flops_per_pde(kname, l0.block)
+    impl_flops = dense_pde * impl
+    achieved = impl_flops / (sweep_ms * 1e-3) / 1e12
+    direct_flops = l0.evals * flops_per_pde(l0.block)
+    direct = direct_flops / (sweep_ms * 1e-3) / 1e12
     per_pair_ms = ms / max(1, wl.pairs_per_step / ws) if wl.kind != "bands" else ms
-    roof = {"bound": "fp32", "kernel": "%s<b=%d> (level 0)" % (sweep_kernel_name(l0), l0.block),
+    traffic = TRAFFIC.get(cfg.name)
+    hbm_peak = hbm_peak_gbs()
+    roof = {"bound": "fp32", "kernel": "%s<b=%d> (level 0)" % (kname, l0.block),
             "achieved": achieved, "peak": tf.value, "unit": "TFLOP/s",
-            "frac": achieved / tf.value, "traffic": TRAFFIC.get(cfg.name),
+            "frac": achieved / tf.value,
+            "traffic": traffic,
+            "traffic_source": "ncu --set full dram__bytes_read.sum + dram__bytes_write.sum of "
+                              "this launch (profiles/r02_ncu_sweep_*.md)" if traffic else None,
+            "hbm_time_ms": (traffic / (hbm_peak * 1e9) * 1e3) if traffic else None,
             "peak_source": "measured live: mshbm_probe_fp32_peak FFMA probe on this GPU "
                            "(MEASURED_PEAKS.json has no FP32 figure)",
-            "algorithmic_flops_per_launch": alg_flops,
-            "algorithmic_basis": "level-0 trace evals (selection_evals + refine_evals) "
-                                 "x F(b)=2b^2+8 (SURVEY 8d)",
+            "algorithmic_flops_per_launch": impl_flops,
+            "algorithmic_basis": f"implemented count: dense level-0 PDE W*H*(D+1) = {dense_pde} "
+                                 f"x {impl:.4g} flops per PDE (bench.sweep4_row_step_flops, "
+                                 "checked against ncu FP32 instruction counts, tools/flop_check.py)",
             "launch_ms": sweep_ms,
             "share_of_step": sweep_ms / per_pair_ms if wl.kind != "bands" or ws == 1 else None,
-            "dense_pde_flops_per_launch": dense_flops,
-            "dense_achieved": dense_flops / (sweep_ms * 1e-3) / 1e12}
+            "direct_equivalent": {
+                "achieved": direct, "frac": direct / tf.value, "flops_per_launch": direct_flops,
+                "basis": "level-0 trace evals (selection_evals + refine_evals) x F(b)=2b^2+8 "
+                         "(SURVEY 8d direct form)"}}
+
+    # ---- the sharded configs (north_star: C4 pairs and C5 bands at 1/2/4/8)
+    sharded = None
+    if not args.no_sharded:
+        sharded = {}
+        for name in ("C4", "C5"):
+            if name == cfg.name:
+                continue
+            swl = Workload(CONFIGS[name], gpu, _lib, dev, ws, rank)
+            for _ in range(2):
+                swl.step()
+            sms = measure(swl, 5 if name == "C5" else 10, flush, stream, barrier,
+                          max_over_ranks)
+            ent = {"ms_per_step": sms, "mpd_per_s": swl.units / (sms * 1e-3) / 1e6,
+                   "pairs_per_s": swl.pairs_per_step / (sms * 1e-3),
+                   "parallelism": swl.parallelism(), "scaling": swl.scaling,
+                   "workload": workload_desc(CONFIGS[name])["workload"]}
+            sharded[name] = ent
+            del swl
+            torch.cuda.empty_cache()
 
     out = None
     if rank == 0:
@@ -436,23 +617,27 @@ def run_ours(args, cfg):
                     "path": "C ABI (mshbm_run_pipeline / _batch / _band, MSHBM_IO_HOST) "
                             "from pinned host buffers"},
             "e2e_pipelined": pipe,
+            "e2e_python": epy,
             "roofline": roof,
+            "sharded": sharded,
             "gpu_launches": launches,
             "clocks": clocks.summary(),
         }
         if ws == 1 and not args.no_cpu_baseline:
-            workers = os.cpu_count() or 1
-            dt, pde = cpu_oracle_run(cfg, cfg.seed, workers)
-            h, w = CPU_SAMPLE
-            out["cpu_baseline"] = {
-                "value": pde / dt / 1e6, "unit": UNIT, "cores": workers, "kind": "port",
-                "sample": f"{w}x{h} crop of {cfg.name} params through the numpy oracle "
-                          f"(reference algorithm, fp64), {dt:.1f} s"}
+            out["cpu_baseline"] = cpu_baseline(cfg)
     if ws > 1:
         dist.barrier()
         dist.destroy_process_group()
     if out is not None:
         print(json.dumps(out), flush=True)
+
+
+def hbm_peak_gbs() -> float:
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"])
+    except (OSError, KeyError, ValueError):
+        return 6552.0
 
 
 # dram__bytes_read.sum + dram__bytes_write.sum of the level-0 sweep launch from
@@ -470,19 +655,36 @@ def sweep_kernel_name(level) -> str:
     return "sweep2_kernel"
 
 
+def maybe_spawn(args) -> bool:
+    """--gpus N outside torchrun: re-exec under torch.distributed.run."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return False
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    os.execv(sys.executable, cmd)
+    return True
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=None)
     ap.add_argument("--warmup", type=int, default=10)
-    ap.add_argument("--config", default="C2", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default="C3", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-sharded", action="store_true")
     args = ap.parse_args()
+    maybe_spawn(args)
     args.warmup = max(3, args.warmup) if args.impl == "ours" else args.warmup
     cfg = CONFIGS[args.config]
     if args.steps is None:   # a timed region of roughly 0.3-2 s per config
-        args.steps = {"C1": 400, "C2": 200, "C3": 40, "C4": 20, "C5": 10}[cfg.name]
+        args.steps = {"C1": 400, "C2": 200, "C3": 100, "C4": 20, "C5": 10}[cfg.name]
     if args.impl == "reference":
         run_reference(args, cfg)
     else:

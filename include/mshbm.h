@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define MSHBM_ABI_VERSION 1
+#define MSHBM_ABI_VERSION 2
 
 typedef enum {
   MSHBM_OK = 0,
@@ -52,7 +52,8 @@ enum { MSHBM_SIGN_MIDDLEBURY = 0, MSHBM_SIGN_PAPER = 1 };
 enum { MSHBM_IO_DEVICE = 0, MSHBM_IO_HOST = 1 };
 /* flags for mshbm_run_pipeline */
 enum {
-  MSHBM_FLAG_TIMING = 1,   /* fill per-stage milliseconds (no graph replay) */
+  MSHBM_FLAG_TIMING = 1,   /* fill per-stage milliseconds (read from event-record
+                              nodes of the graph; synchronises like a trace) */
   MSHBM_FLAG_NO_GRAPH = 2  /* launch kernels directly instead of a CUDA graph */
 };
 
@@ -70,7 +71,10 @@ typedef struct {
   int32_t reserved;
 } mshbm_config;
 
-/* LevelTrace (matcher.py:98-153): exact counters + stage milliseconds. */
+/* LevelTrace (matcher.py:98-153): exact counters + stage milliseconds.
+ * ms_build (pyramid construction, PipelineTrace.build_seconds,
+ * matcher.py:410-416) and ms_total (whole pipeline on the device) are the
+ * same in every level record of one run. */
 typedef struct {
   int32_t level, height, width, d_max, block, reserved;
   int64_t trusted;
@@ -82,6 +86,7 @@ typedef struct {
   int64_t refine_evals;
   int64_t median_replaced;
   float ms_upsample, ms_select, ms_refine, ms_median;
+  float ms_build, ms_total;
 } mshbm_level_trace;
 
 typedef struct mshbm_ctx mshbm_ctx;

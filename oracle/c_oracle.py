@@ -40,7 +40,7 @@ def lib():
         L.mshbm_oracle_run_pipeline.argtypes = [
             C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
             C.c_double, C.c_double, C.c_double, C.c_int, C.c_int,
-            C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(C.c_int)]
+            C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(C.c_int), C.c_void_p, C.c_void_p]
         L.mshbm_oracle_match_coarsest.restype = C.c_int
         L.mshbm_oracle_match_coarsest.argtypes = [
             C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, C.c_int,
@@ -52,8 +52,10 @@ def lib():
 
 
 def run_pipeline(left, right, d_max, levels=None, block=11, alpha=0.9, beta=0.9,
-                 sigma_eps=1e-6, sign="middlebury", radius=1, threads=0):
-    """Returns (disparity f64 (H, W), cost f64 (H, W), counts int64 (K+1, 13))."""
+                 sigma_eps=1e-6, sign="middlebury", radius=1, threads=0, levels_out=False):
+    """Returns (disparity f64 (H, W), cost f64 (H, W), counts int64 (K+1, 13)),
+    plus, with ``levels_out``, the list of every level's (disparity, cost)
+    maps, level 0 first (post-median disparity, refined cost)."""
     L = np.ascontiguousarray(left, dtype=np.float64)
     R = np.ascontiguousarray(right, dtype=np.float64)
     if L.ndim != 2 or L.shape != R.shape:
@@ -66,15 +68,28 @@ def run_pipeline(left, right, d_max, levels=None, block=11, alpha=0.9, beta=0.9,
     ncol = lib().mshbm_oracle_trace_cols()
     tr = np.zeros((max(k, 0) + 1, ncol), dtype=np.int64)
     kout = C.c_int(0)
+    shapes = [(h, w)]
+    for _ in range(max(k, 0)):
+        shapes.append(((shapes[-1][0] + 1) // 2, (shapes[-1][1] + 1) // 2))
+    tot = sum(a * b for a, b in shapes)
+    ld_ = np.empty(tot) if levels_out else None
+    lc_ = np.empty(tot) if levels_out else None
     rc = lib().mshbm_oracle_run_pipeline(
         L.ctypes.data, R.ctypes.data, h, w, int(d_max), lv, int(block), int(radius),
         float(alpha), float(beta), float(sigma_eps), 1 if sign == "paper" else 0,
-        int(threads), d.ctypes.data, c.ctypes.data, tr.ctypes.data, C.byref(kout))
+        int(threads), d.ctypes.data, c.ctypes.data, tr.ctypes.data, C.byref(kout),
+        ld_.ctypes.data if levels_out else None, lc_.ctypes.data if levels_out else None)
     if rc == 1:
         raise ValueError("invalid pipeline arguments")
     if rc != 0:
         raise MemoryError("oracle out of memory")
-    return d, c, tr
+    if not levels_out:
+        return d, c, tr
+    maps, off = [], 0
+    for a, b in shapes:
+        maps.append((ld_[off:off + a * b].reshape(a, b), lc_[off:off + a * b].reshape(a, b)))
+        off += a * b
+    return d, c, tr, maps
 
 
 def match_coarsest(left, right, block, d_max, sigma_eps=1e-6, sign="middlebury"):

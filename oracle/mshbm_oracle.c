@@ -523,11 +523,14 @@ int mshbm_oracle_trace_cols(void) { return T_NCOLS; }
 
 /* run_pipeline (matcher.py:398-466) with radius r.  levels < 0 = auto.
  * trace: (levels+1) x T_NCOLS int64, coarsest level first (the golden
- * `counts` layout).  Returns 0, or 1 for a ValueError, 2 for out of memory. */
+ * `counts` layout).  level_d/level_c (optional): every level's final
+ * disparity and (refined) cost map, levels 0..K concatenated (teacher-forced
+ * stage parity).  Returns 0, or 1 for a ValueError, 2 for out of memory. */
 int mshbm_oracle_run_pipeline(const double* left, const double* right, int height, int width,
                               int d_max, int levels, int block, int radius, double alpha,
                               double beta, double sigma_eps, int sign, int threads,
-                              double* d_out, double* c_out, int64_t* trace, int* levels_out) {
+                              double* d_out, double* c_out, int64_t* trace, int* levels_out,
+                              double* level_d, double* level_c) {
 #ifdef _OPENMP
     if (threads > 0) omp_set_num_threads(threads);
 #else
@@ -580,6 +583,12 @@ int mshbm_oracle_run_pipeline(const double* left, const double* right, int heigh
             free(dh); free(ch);
         }
         engine_free(&e);
+        if (level_d && level_c && rc == ORC_OK) {
+            size_t off = 0;
+            for (int t = 0; t < k; ++t) off += (size_t)hs[t] * ws[t];
+            memcpy(level_d + off, dk, sizeof(double) * n);
+            memcpy(level_c + off, ck, sizeof(double) * n);
+        }
         free(dprev); free(cprev);
         dprev = k == 0 ? NULL : dk;
         cprev = k == 0 ? NULL : ck;

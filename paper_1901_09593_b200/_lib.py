@@ -16,6 +16,7 @@ LIB_PATH = os.path.join(HERE, "libmshbm.so")
 MSHBM_OK = 0
 MSHBM_ERR_VALUE = 1
 MSHBM_ERR_CONFIG = 2
+ABI_VERSION = 2        # include/mshbm.h MSHBM_ABI_VERSION
 IO_DEVICE = 0
 IO_HOST = 1
 FLAG_TIMING = 1
@@ -54,7 +55,8 @@ class LevelTraceC(C.Structure):
                 ("selection_evals", C.c_int64), ("refined", C.c_int64),
                 ("refine_evals", C.c_int64), ("median_replaced", C.c_int64),
                 ("ms_upsample", C.c_float), ("ms_select", C.c_float),
-                ("ms_refine", C.c_float), ("ms_median", C.c_float)]
+                ("ms_refine", C.c_float), ("ms_median", C.c_float),
+                ("ms_build", C.c_float), ("ms_total", C.c_float)]
 
 
 P = C.c_void_p
@@ -123,6 +125,10 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
                 f"libmshbm.so not found at {path}: build it with "
                 "`python -m paper_1901_09593_b200.build` (there is no CPU fallback)")
         lib = C.CDLL(path)
+        lib.mshbm_abi_version.restype = C.c_int
+        if lib.mshbm_abi_version() != ABI_VERSION:
+            raise RuntimeError(f"{path} has ABI {lib.mshbm_abi_version()}, this binding expects "
+                               f"{ABI_VERSION}: rebuild with `python -m paper_1901_09593_b200.build`")
         for name, (res, args) in SIGNATURES.items():
             fn = getattr(lib, name)
             fn.restype = res

@@ -7,6 +7,7 @@
 #include <cstdio>
 #include <cstring>
 #include <map>
+#include <mutex>
 #include <string>
 #include <tuple>
 #include <vector>
@@ -42,6 +43,7 @@ struct LevelBuf {
   float* muL = nullptr;     // left window statistics (sweep4 levels, b >= 5)
   float* isL = nullptr;
   unsigned* flags = nullptr;  // sweep4 precision-guard tile flags
+  float* guard_col = nullptr; // guard scratch (per tile row and column)
   int64_t flags_ld = 0;
   int* fix_list = nullptr;   // sweep2 fixup jobs (+ count)
   int* fix_count = nullptr;
@@ -75,6 +77,10 @@ struct PlanKey {
   }
 };
 
+struct StageEvents {
+  cudaEvent_t up0, up1, sel0, sel1, med0, med1;
+};
+
 struct Plan {
   PlanKey key{};
   int H = 0, W = 0, K = 0;
@@ -90,7 +96,15 @@ struct Plan {
   cudaGraphExec_t exec = nullptr;
   int launches = 0;
   cudaStream_t stream = nullptr;   // batch slot stream (run_batch)
+  // recorded after every use: a call on another stream waits for it before
+  // touching the plan's buffers (inputs, pyramid, outputs are per plan)
   cudaEvent_t done = nullptr;
+  cudaStream_t last_stream = nullptr;
+  bool used = false;
+  // stage timing: events recorded by every run (external event-record nodes
+  // of the captured graph, or plain records on the direct path)
+  std::vector<StageEvents> tev;
+  cudaEvent_t t_begin = nullptr, t_built = nullptr, t_end = nullptr;
 };
 
 }  // namespace
@@ -99,6 +113,7 @@ struct mshbm_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
   std::string err;
+  std::recursive_mutex mu;   // plans map + plan use (calls from several host threads)
   std::map<PlanKey, Plan*> plans;
   int64_t launches = 0;
   cudaEvent_t ev[64];
@@ -221,6 +236,7 @@ void carve(Plan& p, Carver& cv) {
       l.flags = cv.take<unsigned>((size_t)l.flags_ld * ((l.h + 1) / 2) + 1);
       l.fix_count = reinterpret_cast<int*>(l.flags + (size_t)l.flags_ld * ((l.h + 1) / 2));
       l.fix_list = cv.take<int>((size_t)((l.w + 29) / 30) * (l.h / 14 + 2));
+      l.guard_col = cv.take<float>((size_t)((l.h + sweep4_th() - 1) / sweep4_th() + 1) * l.w);
     }
     l.wc = cv.take<int>(n);
     l.dsel = cv.take<int16_t>(n);
@@ -302,9 +318,14 @@ void plan_rows(Plan& p, int b0, int b1) {
   }
 }
 
-struct StageEvents {
-  cudaEvent_t up0, up1, sel0, sel1, med0, med1;
-};
+// Event record that becomes an event-record node under stream capture.
+cudaError_t rec(cudaEvent_t e, cudaStream_t s) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaError_t err = cudaStreamIsCapturing(s, &cs);
+  if (err != cudaSuccess) return err;
+  return cs == cudaStreamCaptureStatusActive ? cudaEventRecordWithFlags(e, s, cudaEventRecordExternal)
+                                             : cudaEventRecord(e, s);
+}
 
 // Enqueue the whole pair on `s` (also used under stream capture).
 // side/evs (graph capture only): the window statistics and staging arrays
@@ -313,12 +334,13 @@ struct StageEvents {
 // evs[k].  evs[K+1] is the fork point.  The spline prefilter of level k's
 // costs also runs on the branch, beside level k's median (evs[K+2+k] =
 // sweep k done, evs[2K+3+(k-1)] = prefilter done, joined by prior k-1).
-int enqueue(mshbm_ctx* ctx, Plan& p, cudaStream_t s, std::vector<StageEvents>* tev,
-            cudaStream_t side = nullptr, cudaEvent_t* evs = nullptr,
-            cudaStream_t side2 = nullptr) {
+// Every run records the plan's stage events (p.tev, t_begin/t_built/t_end).
+int enqueue(mshbm_ctx* ctx, Plan& p, cudaStream_t s, cudaStream_t side = nullptr,
+            cudaEvent_t* evs = nullptr, cudaStream_t side2 = nullptr) {
   int n = 0;
   const mshbm_config& cfg = p.cfg;
   const int dir = cfg.sign == MSHBM_SIGN_PAPER ? -1 : 1;
+  CK(rec(p.t_begin, s));
   CK(cudaMemsetAsync(p.counters, 0,
                      sizeof(unsigned long long) * (p.K + 1) * kCntSlots * kCntCopies, s));
   if (!p.user) {
@@ -342,6 +364,7 @@ int enqueue(mshbm_ctx* ctx, Plan& p, cudaStream_t s, std::vector<StageEvents>* t
       ++n;
     }
   }
+  CK(rec(p.t_built, s));   // pyramid built (build_pyramid, matcher.py:410-416)
   // the right offset c of every level: the level-0 right sample at the
   // image centre (whole input on every rank, so row bands agree)
   CK(launch_centre_sample(p.user ? nullptr : p.in_r, p.user ? p.lv[0].R : nullptr,
@@ -356,7 +379,7 @@ int enqueue(mshbm_ctx* ctx, Plan& p, cudaStream_t s, std::vector<StageEvents>* t
     LevelBuf& l = p.lv[k];
     cudaStream_t t = (fork && k < p.K) ? side : s;
     CK(launch_stats_f32(l.R, l.h, l.w, l.ld, l.b, cfg.sigma_eps, l.muR, l.isR, l.ld, t,
-                        Sweep4Guard{}, l.st_lo, l.st_hi));
+                        l.st_lo, l.st_hi));
     CK(launch_prep_staging(l.R, l.ld, l.muR, l.isR, l.ld, l.h, l.w, l.pc, l.Rp, l.Mp, l.ldp, t,
                            l.st_lo, l.st_hi, p.cR));
     n += 2;
@@ -364,26 +387,37 @@ int enqueue(mshbm_ctx* ctx, Plan& p, cudaStream_t s, std::vector<StageEvents>* t
       // L statistics + sweep4's precision guard (tile flags), then the job
       // list of its sweep2 fixup
       Sweep4Guard g;
+      g.L = l.L;
+      g.ld = l.ld;
+      g.muL = l.muL;
+      g.isL = l.isL;
       g.muR = l.muR;
       g.isR = l.isR;
+      g.lds = l.ld;
       g.cR = p.cR;
+      g.h = l.h;
+      g.w = l.w;
+      g.d = l.d;
+      g.dir = dir;
       g.tile_h = sweep4_th();
+      g.colR = l.guard_col;
       g.flags = l.flags;
       g.flags_ld = l.flags_ld;
       CK(cudaMemsetAsync(l.flags, 0, sizeof(unsigned) * (l.flags_ld * ((l.h + 1) / 2) + 1), t));
-      CK(launch_stats_f32(l.L, l.h, l.w, l.ld, l.b, cfg.sigma_eps, l.muL, l.isL, l.ld, t, g,
+      CK(launch_stats_f32(l.L, l.h, l.w, l.ld, l.b, cfg.sigma_eps, l.muL, l.isL, l.ld, t,
                           l.st_lo, l.st_hi));
+      CK(launch_sweep4_guard(g, l.rows, t));
       CK(launch_fixup_list(l.flags, l.flags_ld, sweep4_th(), l.h, l.w, l.rows, l.b, l.fix_list,
                            l.fix_count, t));
-      n += 2;
+      n += 4;
     }
     if (fork && k < p.K) CK(cudaEventRecord(evs[k], side));
   }
   for (int k = p.K; k >= 0; --k) {
     LevelBuf& l = p.lv[k];
     unsigned long long* cnt = p.counters + (size_t)(p.K - k) * kCntSlots * kCntCopies;
-    StageEvents* ev = tev ? &(*tev)[p.K - k] : nullptr;
-    if (ev) CK(cudaEventRecord(ev->up0, s));
+    StageEvents* ev = &p.tev[p.K - k];
+    CK(rec(ev->up0, s));
     if (k < p.K) {
       LevelBuf& c = p.lv[k + 1];
       if (fork) {
@@ -398,7 +432,7 @@ int enqueue(mshbm_ctx* ctx, Plan& p, cudaStream_t s, std::vector<StageEvents>* t
                            cfg.beta, l.wc, l.ld, cnt, l.rows, s));
       ++n;
     }
-    if (ev) CK(cudaEventRecord(ev->up1, s));
+    CK(rec(ev->up1, s));
     SweepArgs a{};
     a.L = l.L; a.R = l.R; a.ld = l.ld;
     a.muR = l.muR; a.isR = l.isR; a.lds = l.ld;
@@ -415,9 +449,9 @@ int enqueue(mshbm_ctx* ctx, Plan& p, cudaStream_t s, std::vector<StageEvents>* t
     a.Rp = l.Rp; a.Mp = l.Mp; a.ldp = l.ldp; a.pc = l.pc;
     if (fork && k < p.K) CK(cudaStreamWaitEvent(s, evs[k], 0));
     const bool s4 = sweep_uses_sweep4(a);
-    if (ev) CK(cudaEventRecord(ev->sel0, s));
+    CK(rec(ev->sel0, s));
     CK(launch_sweep(a, s, &n));
-    if (ev) CK(cudaEventRecord(ev->sel1, s));
+    CK(rec(ev->sel1, s));
     if (s4) {   // sweep2 on the tiles sweep4's precision guard left (usually none)
       CK(launch_sweep4_fixup(a, s));
       ++n;
@@ -436,18 +470,20 @@ int enqueue(mshbm_ctx* ctx, Plan& p, cudaStream_t s, std::vector<StageEvents>* t
       CK(cudaEventRecord(evs[2 * p.K + 3 + (k - 1)], pf));
       n += 1;
     }
-    if (ev) CK(cudaEventRecord(ev->med0, s));
+    CK(rec(ev->med0, s));
     CK(launch_median_pipeline(l.dsel, l.c, l.low, l.ld, l.h, l.w, cfg.alpha, l.dmed, cnt, l.rows,
                               s));
     ++n;
-    if (ev) CK(cudaEventRecord(ev->med1, s));
+    CK(rec(ev->med1, s));
   }
+  CK(rec(p.t_end, s));
   p.launches = n;
   return MSHBM_OK;
 }
 
 Plan* get_plan(mshbm_ctx* ctx, const PlanKey& key, const mshbm_config& cfg,
                const std::vector<std::tuple<int, int, int, int>>& dims, int* st) {
+  std::lock_guard<std::recursive_mutex> g(ctx->mu);
   auto it = ctx->plans.find(key);
   if (it != ctx->plans.end()) return it->second;
   Plan* p = new Plan();
@@ -472,24 +508,26 @@ Plan* get_plan(mshbm_ctx* ctx, const PlanKey& key, const mshbm_config& cfg,
     return nullptr;
   }
   plan_rows(*p, key.band_lo, key.band_hi);
+  p->tev.resize(p->K + 1);
+  bool ok = cudaEventCreateWithFlags(&p->done, cudaEventDisableTiming) == cudaSuccess;
+  for (cudaEvent_t* e : {&p->t_begin, &p->t_built, &p->t_end}) ok &= cudaEventCreate(e) == cudaSuccess;
+  for (auto& e : p->tev) {
+    cudaEvent_t* ev = &e.up0;
+    for (int t = 0; t < 6; ++t) ok &= cudaEventCreate(&ev[t]) == cudaSuccess;
+  }
+  if (!ok) {
+    *st = fail(ctx, MSHBM_ERR_CUDA, "event create failed");
+    return nullptr;
+  }
   ctx->plans[key] = p;
   return p;
 }
 
-// run a plan: graph replay (captured on first use) or direct launches.
-// Stage events are only recorded on the direct path (MSHBM_FLAG_TIMING).
-int launch_plan(mshbm_ctx* ctx, Plan& p, cudaStream_t s, int flags,
-                std::vector<StageEvents>* tev) {
-  const bool direct = (tev != nullptr) || (flags & MSHBM_FLAG_NO_GRAPH);
-  if (tev) {
-    tev->resize(p.K + 1);
-    for (auto& e : *tev) {
-      cudaEvent_t* ev = &e.up0;
-      for (int t = 0; t < 6; ++t) CK(cudaEventCreate(&ev[t]));
-    }
-  }
-  if (direct) {
-    int st = enqueue(ctx, p, s, tev);
+// run a plan: graph replay (captured on first use) or direct launches
+// (MSHBM_FLAG_NO_GRAPH).  Both record the plan's stage events.
+int launch_plan(mshbm_ctx* ctx, Plan& p, cudaStream_t s, int flags) {
+  if (flags & MSHBM_FLAG_NO_GRAPH) {
+    int st = enqueue(ctx, p, s);
     if (st) return st;
   } else {
     if (!p.exec) {
@@ -507,7 +545,7 @@ int launch_plan(mshbm_ctx* ctx, Plan& p, cudaStream_t s, int flags,
       // faster with one branch)
       bool s4 = false;
       for (const LevelBuf& l : p.lv) s4 |= l.muL != nullptr;
-      int st = enqueue(ctx, p, cs, nullptr, side, evs.data(), s4 ? side2 : nullptr);
+      int st = enqueue(ctx, p, cs, side, evs.data(), s4 ? side2 : nullptr);
       cudaError_t ce = cudaStreamEndCapture(cs, &g);
       for (auto& e : evs) cudaEventDestroy(e);
       cudaStreamDestroy(side);
@@ -537,7 +575,12 @@ void reduce_copies(const unsigned long long* h, unsigned long long* c) {
 }
 
 void pack_trace(const Plan& p, const unsigned long long* h, mshbm_level_trace* trace,
-                std::vector<StageEvents>* tev) {
+                bool timed) {
+  float ms_build = 0.f, ms_total = 0.f;
+  if (timed) {
+    cudaEventElapsedTime(&ms_build, p.t_begin, p.t_built);
+    cudaEventElapsedTime(&ms_total, p.t_begin, p.t_end);
+  }
   for (int t = 0; t <= p.K; ++t) {
     const int k = p.K - t;
     const LevelBuf& l = p.lv[k];
@@ -564,8 +607,8 @@ void pack_trace(const Plan& p, const unsigned long long* h, mshbm_level_trace* t
     o.refined = (int64_t)c[kCntRefined];
     o.refine_evals = o.refined > 0 ? (int64_t)c[kCntNeeded] * (l.d + 1) : 0;
     o.median_replaced = (int64_t)c[kCntMedianReplaced];
-    if (tev && !tev->empty()) {
-      StageEvents& e = (*tev)[t];
+    if (timed) {
+      const StageEvents& e = p.tev[t];
       float ms = 0.f;
       if (k < p.K) {
         cudaEventElapsedTime(&ms, e.up0, e.up1);
@@ -576,17 +619,18 @@ void pack_trace(const Plan& p, const unsigned long long* h, mshbm_level_trace* t
       o.ms_refine = 0.f;   // fused into the sweep (reported under select)
       cudaEventElapsedTime(&ms, e.med0, e.med1);
       o.ms_median = ms;
+      o.ms_build = ms_build;
+      o.ms_total = ms_total;
     }
   }
 }
 
 // Copy the device counters back (synchronises `s`) and pack the trace.
-int finish_trace(mshbm_ctx* ctx, Plan& p, cudaStream_t s, mshbm_level_trace* trace,
-                 std::vector<StageEvents>* tev) {
+int finish_trace(mshbm_ctx* ctx, Plan& p, cudaStream_t s, mshbm_level_trace* trace, bool timed) {
   std::vector<unsigned long long> h((size_t)(p.K + 1) * kCntSlots * kCntCopies);
   CK(cudaMemcpyAsync(h.data(), p.counters, h.size() * sizeof(h[0]), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
-  pack_trace(p, h.data(), trace, tev);
+  pack_trace(p, h.data(), trace, timed);
   return MSHBM_OK;
 }
 
@@ -598,6 +642,19 @@ void destroy_events(std::vector<StageEvents>& tev) {
   tev.clear();
 }
 
+// A plan's buffers belong to one stream at a time: a call on a different
+// stream than the plan's last user waits for that use to finish.
+int plan_acquire(mshbm_ctx* ctx, Plan& p, cudaStream_t s) {
+  if (p.used && p.last_stream != s) CK(cudaStreamWaitEvent(s, p.done, 0));
+  return MSHBM_OK;
+}
+int plan_release(mshbm_ctx* ctx, Plan& p, cudaStream_t s) {
+  CK(cudaEventRecord(p.done, s));
+  p.last_stream = s;
+  p.used = true;
+  return MSHBM_OK;
+}
+
 // inputs (optional) -> plan -> outputs (+ trace).  Host I/O synchronises.
 int run_plan_io(mshbm_ctx* ctx, Plan* p, const float* left, const float* right, int64_t ld,
                 int16_t* disparity, float* cost, int64_t ld_out, mshbm_level_trace* trace,
@@ -605,17 +662,14 @@ int run_plan_io(mshbm_ctx* ctx, Plan* p, const float* left, const float* right, 
   const bool host = io == MSHBM_IO_HOST;
   const cudaMemcpyKind kin = host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
   const cudaMemcpyKind kout = host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+  int st = plan_acquire(ctx, *p, s);
+  if (st) return st;
   if (left) {
     CK(cudaMemcpy2DAsync(p->in_l, p->ld_in * 4, left, ld * 4, (size_t)p->W * 4, p->H, kin, s));
     CK(cudaMemcpy2DAsync(p->in_r, p->ld_in * 4, right, ld * 4, (size_t)p->W * 4, p->H, kin, s));
   }
-  std::vector<StageEvents> tev;
-  const bool timing = trace && (flags & MSHBM_FLAG_TIMING);
-  int st = launch_plan(ctx, *p, s, flags, timing ? &tev : nullptr);
-  if (st) {
-    destroy_events(tev);
-    return st;
-  }
+  st = launch_plan(ctx, *p, s, flags);
+  if (st) return st;
   const LevelBuf& l0 = p->lv[0];
   const int r0 = l0.rows.cnt_lo, nr = l0.rows.cnt_hi - l0.rows.cnt_lo;
   if (disparity)
@@ -624,11 +678,12 @@ int run_plan_io(mshbm_ctx* ctx, Plan* p, const float* left, const float* right, 
   if (cost)
     CK(cudaMemcpy2DAsync(cost, ld_out * 4, l0.c + (int64_t)r0 * l0.ld, l0.ld * 4,
                          (size_t)l0.w * 4, nr, kout, s));
-  if (trace) st = finish_trace(ctx, *p, s, trace, &tev);
+  st = plan_release(ctx, *p, s);
+  if (st) return st;
+  if (trace) st = finish_trace(ctx, *p, s, trace, (flags & MSHBM_FLAG_TIMING) != 0);
   else if (host && allow_sync) {
     CK(cudaStreamSynchronize(s));
   }
-  destroy_events(tev);
   return st;
 }
 
@@ -687,6 +742,9 @@ int mshbm_destroy(mshbm_ctx* ctx) {
     if (kv.second->exec) cudaGraphExecDestroy(kv.second->exec);
     if (kv.second->stream) cudaStreamDestroy(kv.second->stream);
     if (kv.second->done) cudaEventDestroy(kv.second->done);
+    destroy_events(kv.second->tev);
+    for (cudaEvent_t e : {kv.second->t_begin, kv.second->t_built, kv.second->t_end})
+      if (e) cudaEventDestroy(e);
     cudaFree(kv.second->arena);
     delete kv.second;
   }
@@ -798,6 +856,7 @@ int mshbm_run_pipeline(mshbm_ctx* ctx, const float* left, const float* right, in
                        float* cost, int64_t ld_out, mshbm_level_trace* trace,
                        int32_t* out_levels, int32_t io, int32_t flags, void* stream) {
   if (!ctx) return fail(nullptr, MSHBM_ERR_VALUE, "null context");
+  std::lock_guard<std::recursive_mutex> lock(ctx->mu);
   if (!left || !right) return fail(ctx, MSHBM_ERR_VALUE, "null image pointer");
   if (ld < width || ld_out < width) return fail(ctx, MSHBM_ERR_VALUE, "row stride < width");
   Plan* p = nullptr;
@@ -813,6 +872,7 @@ int mshbm_run_pipeline_band(mshbm_ctx* ctx, const float* left, const float* righ
                             int64_t ld_out, mshbm_level_trace* trace, int32_t* out_levels,
                             int32_t io, int32_t flags, void* stream) {
   if (!ctx) return fail(nullptr, MSHBM_ERR_VALUE, "null context");
+  std::lock_guard<std::recursive_mutex> lock(ctx->mu);
   if (!left || !right) return fail(ctx, MSHBM_ERR_VALUE, "null image pointer");
   if (ld < width || ld_out < width) return fail(ctx, MSHBM_ERR_VALUE, "row stride < width");
   Plan* p = nullptr;
@@ -828,6 +888,7 @@ int mshbm_run_batch(mshbm_ctx* ctx, int32_t n_pairs, const float* const* lefts,
                     int64_t ld_out, mshbm_level_trace* traces, int32_t io, int32_t n_streams,
                     void* stream) {
   if (!ctx) return fail(nullptr, MSHBM_ERR_VALUE, "null context");
+  std::lock_guard<std::recursive_mutex> lock(ctx->mu);
   if (n_pairs < 0 || (n_pairs > 0 && (!lefts || !rights)))
     return fail(ctx, MSHBM_ERR_VALUE, "bad pair arrays");
   if (ld < width || ld_out < width) return fail(ctx, MSHBM_ERR_VALUE, "row stride < width");
@@ -840,10 +901,7 @@ int mshbm_run_batch(mshbm_ctx* ctx, int32_t n_pairs, const float* const* lefts,
     int st = prepare_plan(ctx, height, width, cfg, 0, height, 1 + k, &K, &slot[k]);
     if (st) return st;
     Plan* p = slot[k];
-    if (!p->stream) {
-      CK(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
-      CK(cudaEventCreateWithFlags(&p->done, cudaEventDisableTiming));
-    }
+    if (!p->stream) CK(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
   }
   const size_t per = (size_t)(K + 1) * kCntSlots * kCntCopies;
   unsigned long long* hc = nullptr;
@@ -868,7 +926,7 @@ int mshbm_run_batch(mshbm_ctx* ctx, int32_t n_pairs, const float* const* lefts,
   cudaEventDestroy(start);
   if (hc || io == MSHBM_IO_HOST) CK(cudaStreamSynchronize(s));
   if (hc) {
-    for (int i = 0; i < n_pairs; ++i) pack_trace(*slot[i % nslot], hc + per * i, traces + (size_t)(K + 1) * i, nullptr);
+    for (int i = 0; i < n_pairs; ++i) pack_trace(*slot[i % nslot], hc + per * i, traces + (size_t)(K + 1) * i, false);
     cudaFreeHost(hc);
   }
   return MSHBM_OK;
@@ -880,6 +938,7 @@ int mshbm_run_pyramid(mshbm_ctx* ctx, int32_t n_levels, const double* const* lef
                       const int32_t* blocks, const mshbm_config* cfg, int16_t* disparity,
                       float* cost, int64_t ld_out, mshbm_level_trace* trace, void* stream) {
   if (!ctx) return fail(nullptr, MSHBM_ERR_VALUE, "null context");
+  std::lock_guard<std::recursive_mutex> lock(ctx->mu);
   int st = validate_config(ctx, cfg);
   if (st) return st;
   if (n_levels < 1) return fail(ctx, MSHBM_ERR_VALUE, "empty pyramid");

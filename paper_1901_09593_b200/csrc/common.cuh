@@ -4,11 +4,32 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <mutex>
 #include <utility>
 
 #define MSHBM_DEV __device__ __forceinline__
 
 namespace mshbm {
+
+// Per-device dynamic shared-memory opt-in for one kernel.  The limit is a
+// per-device function attribute, and one process may drive several devices
+// (one context per device); calls may come from several host threads.
+struct SmemAttr {
+  std::mutex m;
+  size_t bytes[64] = {};
+  template <typename F>
+  cudaError_t ensure(F* kernel, size_t need) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> g(m);
+    if (bytes[dev & 63] >= need) return cudaSuccess;
+    e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)need);
+    if (e == cudaSuccess) bytes[dev & 63] = need;
+    return e;
+  }
+};
+
 
 constexpr int kWcNone = -2147483647 - 1;   // "untrusted" window centre
 

@@ -73,8 +73,6 @@ cudaError_t launch_fixup_list(const unsigned* flags, int64_t flags_ld, int tile_
 bool sweep_supported_block(int b);
 // two-pixels-per-thread variant (sweep2.cu) for b in {3,5,7,9,11}
 bool sweep2_supported(int b);
-bool sweep3_supported(int b);
-cudaError_t launch_sweep3(const SweepArgs& a, cudaStream_t s);
 cudaError_t launch_sweep2(const SweepArgs& a, cudaStream_t s);
 // disparities-across-lanes variant (sweep4.cu): pipeline mode, b in {5,7,9,11}
 bool sweep4_supported(const SweepArgs& a, bool force);
@@ -112,31 +110,42 @@ cudaError_t launch_downsample_f32(const float* in0, const float* in1, int h, int
                                   cudaStream_t s, int i0 = 0, int i1 = -1);
 
 // ---------------------------------------------------------------- stats
-// sweep4 precision guard, evaluated by the statistics kernel of L (R's
-// statistics already computed).  sweep4 centres L by one constant per
-// 16 x tile_h tile (the L sample at the tile centre) and R by the level
-// constant c (the level-0 right sample at the image centre), so its fp32
-// rounding error relative
-// to the cost grows with the amplification
-//   A(p) = (|muL(p) - cL| / sigmaL(p) + 3) x (|muR(p) - c| / sigmaR(p) + 3)
-// (measured: cost error ~1.1e-7 A; BASELINE configs A <= 90, the reference's
-// smooth low-contrast [0, 1] fixtures up to ~900).  Tiles with a pixel above
-// kSweep4RiskMax get flags[tile] |= 1 (zeroed before every run); sweep4
+// sweep4 precision guard.  sweep4 centres L by one constant per 16 x tile_h
+// tile (the L sample at the tile centre, cL) and R by the level constant c
+// (the level-0 right sample at the image centre), so the fp32 rounding error
+// of its sliding sums, relative to the cost at (p, z), grows with
+//   aL(p) x aR(q),  aL = |muL(p) - cL| / sigmaL(p) + 3,  aR = |muR(q) - c| / sigmaR(q) + 3
+// for the right pixel q = p -+ z (measured: cost error ~1.1e-7 aL aR).
+// The guard bounds it per tile by (max aL over the tile's cost pixels: its
+// 16 x tile_h outputs plus the 1-pixel 3x3 border) x (max aR over every right
+// pixel those cost pixels meet for z in [0, d]); tiles above
+// kSweep4RiskMax get flags[tile] = 1 (zeroed before every run) and sweep4
 // leaves them to sweep2's per-pixel centring (launch_sweep4_fixup).
+// BASELINE configs stay far below the limit; the reference's smooth
+// low-contrast [0, 1] fixtures reach it.
 constexpr float kSweep4RiskMax = 200.f;
 struct Sweep4Guard {
-  const float* muR = nullptr;   // stride lds, as the output maps
+  const double* L = nullptr;    // level image (cL samples), stride ld
+  int64_t ld = 0;
+  const float* muL = nullptr;   // fp32 statistics, stride lds
+  const float* isL = nullptr;
+  const float* muR = nullptr;
   const float* isR = nullptr;
+  int64_t lds = 0;
   const float* cR = nullptr;    // the right offset c (prep_staging's)
+  int h = 0, w = 0, d = 0, dir = 1;
   int tile_h = 0;
-  unsigned* flags = nullptr;    // nullptr: no guard
+  float* colR = nullptr;        // scratch: per (tile row, column) max aR
+  unsigned* flags = nullptr;
   int64_t flags_ld = 0;
 };
+// guard flags of the sweep4 tile rows covering `rows` (two launches)
+cudaError_t launch_sweep4_guard(const Sweep4Guard& g, RowBand rows, cudaStream_t s);
 // fp32 mean / inverse sigma (0 = degenerate) of the b x b replicate-padded
 // window, centred arithmetic in fp64.
 cudaError_t launch_stats_f32(const double* img, int h, int w, int64_t ld,
                              int b, double sigma_eps, float* mu, float* is,
-                             int64_t lds, cudaStream_t s, Sweep4Guard g = Sweep4Guard{},
+                             int64_t lds, cudaStream_t s,
                              int y0 = 0, int y1 = -1);   // rows [y0, y1) (tile-aligned)
 // fp64 mean / sigma maps (dense) for the CostEngine API
 cudaError_t launch_stats_f64(const double* img, int h, int w, int64_t ld,

@@ -456,8 +456,7 @@ template <int B>
 __global__ void __launch_bounds__(kTX * kTY) stats_tiled_kernel(const double* img, int h, int w,
                                                               int64_t ld, double sigma_eps,
                                                               float* mu32, float* is32,
-                                                              int64_t lds, Sweep4Guard g,
-                                                              int y_base) {
+                                                              int64_t lds, int y_base) {
   // Separable box sums of x' and x'^2 (x' = x - c, c the tile's first sample,
   // fp64); windows whose shifted variance cancels to < 1e-9 of E[x'^2]
   // (flat or near-flat) recompute it centred from the tile, so flat blocks
@@ -511,20 +510,54 @@ __global__ void __launch_bounds__(kTX * kTY) stats_tiled_kernel(const double* im
   const double sigma = sqrt(fmax(var, 0.0));
   mu32[(int64_t)y * lds + x] = (float)(m1 + c);
   is32[(int64_t)y * lds + x] = sigma >= sigma_eps ? (float)(1.0 / sigma) : 0.f;
-  if (g.flags != nullptr && sigma >= sigma_eps) {
-    // sweep4 precision guard (see Sweep4Guard): this pixel's amplification
-    // against its sweep4 tile's centring constants
-    const int ty = y / g.tile_h, tx = x / 16;
-    const double cL = img[(int64_t)clampi(ty * g.tile_h + g.tile_h / 2, 0, h - 1) * ld +
-                          clampi(tx * 16 + 8, 0, w - 1)];
-    const float ir = g.isR[(int64_t)y * lds + x];
-    if (ir > 0.f) {
-      const float cR = *g.cR;
-      const float aL = (float)fabs(m1 + c - cL) * (float)(1.0 / sigma) + 3.f;
-      const float aR = fabsf(g.muR[(int64_t)y * lds + x] - cR) * ir + 3.f;
-      if (aL * aR > kSweep4RiskMax) atomicOr(&g.flags[(int64_t)ty * g.flags_ld + tx], 1u);
-    }
+}
+
+// ---- sweep4 precision guard (kernels.h Sweep4Guard) -----------------------
+__device__ __forceinline__ float guard_amp(float mu, float is, float c) {
+  return is > 0.f ? fabsf(mu - c) * is + 3.f : 0.f;   // degenerate: cost -1 exactly
+}
+
+// per (tile row, column): max aR over the tile row's cost rows y0-1 .. y0+th
+__global__ void __launch_bounds__(128) guard_col_kernel(const Sweep4Guard g, int ty0) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= g.w) return;
+  const int ty = ty0 + blockIdx.y;
+  const int y0 = ty * g.tile_h;
+  const float c = *g.cR;
+  float m = 0.f;
+  for (int y = max(y0 - 1, 0); y <= min(y0 + g.tile_h, g.h - 1); ++y) {
+    const int64_t o = (int64_t)y * g.lds + j;
+    m = fmaxf(m, guard_amp(g.muR[o], g.isR[o], c));
   }
+  g.colR[(int64_t)blockIdx.y * g.w + j] = m;
+}
+
+// one warp per tile: max aL over the cost pixels x max aR over their right span
+__global__ void __launch_bounds__(32) guard_tile_kernel(const Sweep4Guard g, int ty0) {
+  const int tx = blockIdx.x, ty = ty0 + blockIdx.y, lane = threadIdx.x;
+  const int x0 = tx * 16, y0 = ty * g.tile_h;
+  const double cLd = g.L[(int64_t)clampi(y0 + g.tile_h / 2, 0, g.h - 1) * g.ld +
+                         clampi(x0 + 8, 0, g.w - 1)];
+  const float cL = (float)cLd;
+  float aL = 0.f, aR = 0.f;
+  const int ylo = max(y0 - 1, 0), yhi = min(y0 + g.tile_h, g.h - 1);
+  const int xlo = max(x0 - 1, 0), xhi = min(x0 + 16, g.w - 1);
+  const int nx = xhi - xlo + 1;
+  for (int t = lane; t < (yhi - ylo + 1) * nx; t += 32) {
+    const int y = ylo + t / nx, x = xlo + t % nx;
+    const int64_t o = (int64_t)y * g.lds + x;
+    aL = fmaxf(aL, guard_amp(g.muL[o], g.isL[o], cL));
+  }
+  const int qlo = max(g.dir > 0 ? x0 - 1 - g.d : x0 - 1, 0);
+  const int qhi = min(g.dir > 0 ? x0 + 16 : x0 + 16 + g.d, g.w - 1);
+  const float* col = g.colR + (int64_t)blockIdx.y * g.w;
+  for (int q = qlo + lane; q <= qhi; q += 32) aR = fmaxf(aR, col[q]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    aL = fmaxf(aL, __shfl_xor_sync(kFull, aL, o));
+    aR = fmaxf(aR, __shfl_xor_sync(kFull, aR, o));
+  }
+  if (lane == 0 && aL * aR > kSweep4RiskMax) g.flags[(int64_t)ty * g.flags_ld + tx] = 1u;
 }
 
 // prior_eval with the 4x4 spline support of the block staged in smem
@@ -882,18 +915,18 @@ cudaError_t launch_downsample_f32(const float* in0, const float* in1, int h, int
 
 cudaError_t launch_stats_f32(const double* img, int h, int w, int64_t ld,
                              int b, double sigma_eps, float* mu, float* is,
-                             int64_t lds, cudaStream_t s, Sweep4Guard g, int y0, int y1) {
+                             int64_t lds, cudaStream_t s, int y0, int y1) {
   if (y1 < 0 || y1 > h) y1 = h;
   if (y1 <= y0) return cudaSuccess;
   dim3 blk(32, 8);
   const int yb = (y0 / kTY) * kTY;   // whole-image tile grid
   const dim3 gr = grid2d(w, y1 - yb, blk);
   switch (b) {
-    case 3: stats_tiled_kernel<3><<<gr, blk, 0, s>>>(img, h, w, ld, sigma_eps, mu, is, lds, g, yb); return cudaGetLastError();
-    case 5: stats_tiled_kernel<5><<<gr, blk, 0, s>>>(img, h, w, ld, sigma_eps, mu, is, lds, g, yb); return cudaGetLastError();
-    case 7: stats_tiled_kernel<7><<<gr, blk, 0, s>>>(img, h, w, ld, sigma_eps, mu, is, lds, g, yb); return cudaGetLastError();
-    case 9: stats_tiled_kernel<9><<<gr, blk, 0, s>>>(img, h, w, ld, sigma_eps, mu, is, lds, g, yb); return cudaGetLastError();
-    case 11: stats_tiled_kernel<11><<<gr, blk, 0, s>>>(img, h, w, ld, sigma_eps, mu, is, lds, g, yb); return cudaGetLastError();
+    case 3: stats_tiled_kernel<3><<<gr, blk, 0, s>>>(img, h, w, ld, sigma_eps, mu, is, lds, yb); return cudaGetLastError();
+    case 5: stats_tiled_kernel<5><<<gr, blk, 0, s>>>(img, h, w, ld, sigma_eps, mu, is, lds, yb); return cudaGetLastError();
+    case 7: stats_tiled_kernel<7><<<gr, blk, 0, s>>>(img, h, w, ld, sigma_eps, mu, is, lds, yb); return cudaGetLastError();
+    case 9: stats_tiled_kernel<9><<<gr, blk, 0, s>>>(img, h, w, ld, sigma_eps, mu, is, lds, yb); return cudaGetLastError();
+    case 11: stats_tiled_kernel<11><<<gr, blk, 0, s>>>(img, h, w, ld, sigma_eps, mu, is, lds, yb); return cudaGetLastError();
     default: break;
   }
   stats_kernel<false><<<gr, blk, 0, s>>>(img, h, w, ld, b, sigma_eps, mu, is, nullptr, nullptr,
@@ -915,13 +948,8 @@ cudaError_t launch_fir(const T* cin, int ch, int cw, int64_t ldcin, double* coef
   const int nh = ch + 2 * kNpad, nw = cw + 2 * kNpad;
   constexpr size_t smem = (sizeof(T) * kFE * (kFE + 1) + 7) / 8 * 8 +
                           sizeof(double) * kFT * (kFE + 1);
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(bspline_fir_kernel<T>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
+  static SmemAttr attr;
+  if (cudaError_t e = attr.ensure(bspline_fir_kernel<T>, smem); e != cudaSuccess) return e;
   // coefficient rows [r0, r1) of the padded grid (r1 < 0: all), whole tiles
   if (r1 < 0 || r1 > nh) r1 = nh;
   r0 = std::max(r0, 0);
@@ -1039,6 +1067,15 @@ cudaError_t launch_combine_refine(const double* din, const double* cin, int h,
   dim3 blk(32, 8);
   combine_refine_kernel<<<grid2d(w, h, blk), blk, 0, s>>>(din, cin, h, w, alpha, nz, nc, dout,
                                                            cout, counters);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sweep4_guard(const Sweep4Guard& g, RowBand rows, cudaStream_t s) {
+  if (g.flags == nullptr || rows.hi <= rows.lo) return cudaSuccess;
+  const int ty0 = rows.lo / g.tile_h, ty1 = (rows.hi - 1) / g.tile_h;
+  const int nty = ty1 - ty0 + 1;
+  guard_col_kernel<<<dim3((g.w + 127) / 128, nty), 128, 0, s>>>(g, ty0);
+  guard_tile_kernel<<<dim3((g.w + 15) / 16, nty), 32, 0, s>>>(g, ty0);
   return cudaGetLastError();
 }
 

@@ -391,16 +391,6 @@ sweep_generic(const SweepArgs a) {
   }
 }
 
-int g_variant = -1;
-
-int variant() {
-  if (g_variant < 0) {
-    const char* v = getenv("MSHBM_SWEEP_VARIANT");
-    g_variant = v ? atoi(v) : 0;
-  }
-  return g_variant;
-}
-
 template <int B, int ZC, int NR>
 constexpr size_t sweep_smem() {
   return 2 * sizeof(float[NR + B - 1][30 + B + ZC]) + 2 * sizeof(float2[NR][31 + ZC]) +
@@ -410,13 +400,8 @@ constexpr size_t sweep_smem() {
 template <int B, int DIR, int ZC, int NR, int MINB>
 cudaError_t launch_v(const SweepArgs& a, cudaStream_t s) {
   constexpr size_t smem = sweep_smem<B, ZC, NR>();
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(sweep_kernel<B, DIR, ZC, NR, MINB>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
+  static SmemAttr attr;
+  if (cudaError_t e = attr.ensure(sweep_kernel<B, DIR, ZC, NR, MINB>, smem); e != cudaSuccess) return e;
   SweepArgs b = a;   // CTA rows on the whole-image grid (see sweep2.cu)
   b.rows.lo = (a.rows.lo / (NR - 2)) * (NR - 2);
   dim3 grid((a.W + 29) / 30, (b.rows.hi - b.rows.lo + NR - 3) / (NR - 2));
@@ -426,14 +411,6 @@ cudaError_t launch_v(const SweepArgs& a, cudaStream_t s) {
 
 template <int B, int DIR>
 cudaError_t launch_b(const SweepArgs& a, cudaStream_t s) {
-  if constexpr (DIR > 0 && B == 7) {
-    switch (variant()) {
-      case 1: return launch_v<B, DIR, 16, 8, 1>(a, s);
-      case 2: return launch_v<B, DIR, 16, 8, 2>(a, s);
-      case 3: return launch_v<B, DIR, 24, 16, 1>(a, s);
-      default: break;
-    }
-  }
   if constexpr (B <= 7) {
     return launch_v<B, DIR, 16, 16, 1>(a, s);
   } else {
@@ -470,7 +447,7 @@ int env_int(const char* name, int dflt) {
   const char* v = getenv(name);
   return v ? atoi(v) : dflt;
 }
-// MSHBM_SWEEP_IMPL: 1 = one pixel per thread, 2 = sweep2 (default), 3 = sweep3
+// MSHBM_SWEEP_IMPL: 1 = one pixel per thread (sweep_kernel), 2 = sweep2 (default)
 int sweep_impl() {
   static int v = env_int("MSHBM_SWEEP_IMPL", 2);
   return v;
@@ -514,7 +491,6 @@ cudaError_t launch_sweep(const SweepArgs& a, cudaStream_t s, int* n_launch) {
     if (!sweep4_guard()) b.tile_flags = nullptr;
     return launch_sweep4(b, s);   // + launch_sweep4_fixup (caller's stream choice)
   }
-  if (impl == 3 && sweep3_supported(a.block)) return launch_sweep3(a, s);
   if (impl >= 2 && sweep2_supported(a.block)) return launch_sweep2(a, s);
   return a.dir > 0 ? launch_dir<1>(a, s) : launch_dir<-1>(a, s);
 }

@@ -37,163 +37,39 @@ __device__ __forceinline__ void cp_async8(void* dst, const void* src) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
 
-// Packed FP32 (FFMA2) helpers: one instruction, two lanes of fp32 FMA.
-__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
-  unsigned long long r;
-  asm("fma.rn.f32x2 %0, %1, %2, %3;"
-      : "=l"(r)
-      : "l"(*reinterpret_cast<unsigned long long*>(&a)),
-        "l"(*reinterpret_cast<unsigned long long*>(&b)),
-        "l"(*reinterpret_cast<unsigned long long*>(&c)));
-  return *reinterpret_cast<float2*>(&r);
-}
 __device__ __forceinline__ float fma_sat(float a, float b, float c) {
   float r;
   asm("fma.rn.sat.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
   return r;
 }
-__device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
-  unsigned long long r;
-  asm("add.rn.f32x2 %0, %1, %2;"
-      : "=l"(r)
-      : "l"(*reinterpret_cast<unsigned long long*>(&a)),
-        "l"(*reinterpret_cast<unsigned long long*>(&b)));
-  return *reinterpret_cast<float2*>(&r);
-}
-
-// PK: the right strip is staged twice (as-is and shifted by one element) so
-// every pair (v[e], v[e+1]) is one aligned 8-byte shared load, and the cross
-// sums run as FFMA2 over pairs of disparities with the left weight broadcast.
-// Row length of the staged strip.  With PK the two copies must sit 16 banks
-// apart (copy 1 = copy 0 + RR*RW words), so the even lanes (copy 0) and odd
-// lanes (copy 1) of an 8-byte load hit disjoint banks.
-constexpr int strip_row_words(int base, int rr, bool pk) {
-  int rw = (base + 1) & ~1;
-  if (pk)
-    for (int k = 0; k < 32 && (rr * rw) % 32 != 16; ++k) rw += 2;
-  return rw;
-}
-
-template <int B, int ZC, int NR, int PK = 0>
+template <int B, int ZC, int NR>
 struct Sweep2Smem {
   static constexpr int NROW = 2 * NR;
-  static constexpr int RW = strip_row_words(30 + B + ZC, NROW + B - 1, PK == 1);
+  static constexpr int RW = (30 + B + ZC + 1) & ~1;   // staged strip row length
   static constexpr int RR = NROW + B - 1;
-  static_assert(PK != 1 || (RR * RW) % 32 == 16, "copy offset must be 16 banks");
   static constexpr int SW = 31 + ZC;
   static constexpr int LC = 31 + B;
   using RsT = float[RR][RW];
   using MsT = float2[NROW][SW];
   using HxT = float[ZC][2][NR][32];   // [0] hsA, [1] hsB (horizontal 3-sums)
   using LsT = double[RR][LC];
-  static constexpr int NRS = PK == 1 ? 4 : 2;   // strip buffers (x2 copies when PK == 1)
+  static constexpr int NRS = 2;   // strip buffers (double-buffered)
   static constexpr size_t bytes() {
     return NRS * sizeof(RsT) + 2 * sizeof(MsT) + 2 * sizeof(HxT);
   }
 };
 
 // One chunk of NZ disparities (NZ == ZC, or 4 for the tail) for pixels A, B.
-template <int B, int DIR, int ZC, int NR, int NZ, int PK>
+template <int B, int DIR, int ZC, int NR, int NZ>
 __device__ __forceinline__ void chunk2(
-    const typename Sweep2Smem<B, ZC, NR, PK>::RsT& Rs,
-    const typename Sweep2Smem<B, ZC, NR, PK>::RsT& Rs1,
-    const typename Sweep2Smem<B, ZC, NR, PK>::MsT& Ms,
-    typename Sweep2Smem<B, ZC, NR, PK>::HxT& Hx, const float (&Lt)[B][B], const float (&Lb)[B],
+    const typename Sweep2Smem<B, ZC, NR>::RsT& Rs,
+    const typename Sweep2Smem<B, ZC, NR>::MsT& Ms,
+    typename Sweep2Smem<B, ZC, NR>::HxT& Hx, const float (&Lt)[B][B], const float (&Lb)[B],
     float kLA, float kLB, float dW, int z0, int zoff, int zend, bool inA, bool inB, int lane,
     int wp, float (&best)[4], int (&bestz)[4], bool wchunk, const int (&wlo)[2],
     const int (&whi)[2]) {
   float SA[NZ], P[NZ];
-  if constexpr (PK == 1) {
-    // g-space accumulators: pair h holds g = 2h (x) and 2h+1 (y); zz is
-    // g (DIR < 0) or NZ-1-g (DIR > 0); v[e] = strip[row][lane + eo0 + e]
-    constexpr int NH = NZ / 2;
-    float2 SA2[NH], P2[NH];
-#pragma unroll
-    for (int h = 0; h < NH; ++h) SA2[h] = make_float2(0.f, 0.f), P2[h] = SA2[h];
-    const int base = lane + (DIR > 0 ? (ZC - NZ - zoff) : zoff);
-    const bool odd = base & 1;
-#pragma unroll
-    for (int r = 0; r <= B; ++r) {
-      const float* r0 = &Rs[2 * wp + r][0];
-      const float* r1 = &Rs1[2 * wp + r][0];
-      // pe[k] = (v[2k], v[2k+1]), po[k] = (v[2k+1], v[2k+2]); Rs1[e] = Rs[e+1]
-      const float2* pe = reinterpret_cast<const float2*>(odd ? r1 + base - 1 : r0 + base);
-      const float2* po = reinterpret_cast<const float2*>(odd ? r0 + base + 1 : r1 + base);
-#pragma unroll
-      for (int k = 0; k < NH + (B - 1) / 2; ++k) {
-        const float2 v = pe[k];
-#pragma unroll
-        for (int c = 0; c < B; c += 2) {
-          const int h = k - c / 2;
-          if (h >= 0 && h < NH) {
-            if (r == 0) SA2[h] = ffma2(make_float2(Lt[0][c], Lt[0][c]), v, SA2[h]);
-            else if (r < B) P2[h] = ffma2(make_float2(Lt[r][c], Lt[r][c]), v, P2[h]);
-            else P2[h] = ffma2(make_float2(Lb[c], Lb[c]), v, P2[h]);
-          }
-        }
-      }
-#pragma unroll
-      for (int k = 0; k < NH + (B - 3) / 2; ++k) {
-        const float2 v = po[k];
-#pragma unroll
-        for (int c = 1; c < B; c += 2) {
-          const int h = k - (c - 1) / 2;
-          if (h >= 0 && h < NH) {
-            if (r == 0) SA2[h] = ffma2(make_float2(Lt[0][c], Lt[0][c]), v, SA2[h]);
-            else if (r < B) P2[h] = ffma2(make_float2(Lt[r][c], Lt[r][c]), v, P2[h]);
-            else P2[h] = ffma2(make_float2(Lb[c], Lb[c]), v, P2[h]);
-          }
-        }
-      }
-      if (r == B - 1) {
-#pragma unroll
-        for (int h = 0; h < NH; ++h) SA2[h] = fadd2(SA2[h], P2[h]);   // S_A complete
-      }
-    }
-#pragma unroll
-    for (int zz = 0; zz < NZ; ++zz) {
-      const int g = DIR > 0 ? (NZ - 1 - zz) : zz;
-      SA[zz] = (g & 1) ? SA2[g >> 1].y : SA2[g >> 1].x;
-      P[zz] = (g & 1) ? P2[g >> 1].y : P2[g >> 1].x;
-    }
-  } else if constexpr (PK == 2) {
-    // FFMA2 over disparity pairs from one staged copy: scalar loads, the
-    // odd-offset pairs are assembled in registers
-    constexpr int NH = NZ / 2;
-    constexpr int NE = NZ + B - 1;
-    float2 SA2[NH], P2[NH];
-#pragma unroll
-    for (int h = 0; h < NH; ++h) SA2[h] = make_float2(0.f, 0.f), P2[h] = SA2[h];
-    const int eo0 = DIR > 0 ? (ZC - NZ - zoff) : zoff;
-#pragma unroll
-    for (int r = 0; r <= B; ++r) {
-      const float* rp = &Rs[2 * wp + r][lane + eo0];
-      float v[NE + 1];
-#pragma unroll
-      for (int e = 0; e < NE; ++e) v[e] = rp[e];
-      v[NE] = 0.f;
-#pragma unroll
-      for (int c = 0; c < B; ++c) {
-        const float w = r == 0 ? Lt[0][c] : (r < B ? Lt[r][c] : Lb[c]);
-#pragma unroll
-        for (int h = 0; h < NH; ++h) {
-          const float2 vv = make_float2(v[2 * h + c], v[2 * h + c + 1]);
-          if (r == 0) SA2[h] = ffma2(make_float2(w, w), vv, SA2[h]);
-          else P2[h] = ffma2(make_float2(w, w), vv, P2[h]);
-        }
-      }
-      if (r == B - 1) {
-#pragma unroll
-        for (int h = 0; h < NH; ++h) SA2[h] = fadd2(SA2[h], P2[h]);
-      }
-    }
-#pragma unroll
-    for (int zz = 0; zz < NZ; ++zz) {
-      const int g = DIR > 0 ? (NZ - 1 - zz) : zz;
-      SA[zz] = (g & 1) ? SA2[g >> 1].y : SA2[g >> 1].x;
-      P[zz] = (g & 1) ? P2[g >> 1].y : P2[g >> 1].x;
-    }
-  } else {
+  {
 #pragma unroll
     for (int zz = 0; zz < NZ; ++zz) SA[zz] = 0.f, P[zz] = 0.f;
     // window rows r = 0 (A only), 1..B-1 (shared), B (B's bottom)
@@ -249,9 +125,9 @@ __device__ __forceinline__ void chunk2(
   }
 }
 
-template <int B, int DIR, int ZC, int NR, int MINB, int PK>
+template <int B, int DIR, int ZC, int NR, int MINB>
 __device__ __forceinline__ void sweep2_body(const SweepArgs& a, const int bx, const int by) {
-  using SM = Sweep2Smem<B, ZC, NR, PK>;
+  using SM = Sweep2Smem<B, ZC, NR>;
   constexpr int H2 = B / 2;
   constexpr int NT = NR * 32;
   constexpr int NROW = SM::NROW, RW = SM::RW, RR = SM::RR, SW = SM::SW, LC = SM::LC;
@@ -328,12 +204,7 @@ __device__ __forceinline__ void sweep2_body(const SweepArgs& a, const int bx, co
         for (int u = 0; u < UR; ++u) {
           const int e = lane + 32 * u;
           if (e < RW) {
-            if constexpr (PK == 1) {
-              cp_async4(&Rs[2 * buf][rr][e], src + 32 * u);
-              cp_async4(&Rs[2 * buf + 1][rr][e], src + 32 * u + 1);
-            } else {
-              cp_async4(&Rs[buf][rr][e], src + 32 * u);
-            }
+            cp_async4(&Rs[buf][rr][e], src + 32 * u);
           }
         }
       }
@@ -454,13 +325,13 @@ __device__ __forceinline__ void sweep2_body(const SweepArgs& a, const int bx, co
                                              (trusted[1] && wlo[1] <= z0 + ZC - 1 && whi[1] >= z0));
     int nz;
     if (z0 + ZC - 1 <= zmax) {
-      chunk2<B, DIR, ZC, NR, ZC, PK>(Rs[PK == 1 ? 2 * cur : cur], Rs[PK == 1 ? 2 * cur + 1 : cur], Ms[cur], Hx[cur], Lt, Lb, kLA, kLB, dW, z0, 0, zmax,
+      chunk2<B, DIR, ZC, NR, ZC>(Rs[cur], Ms[cur], Hx[cur], Lt, Lb, kLA, kLB, dW, z0, 0, zmax,
                                  inA, inB, lane, wp, best, bestz, wchunk, wlo, whi);
       nz = ZC;
     } else {
       nz = zmax - z0 + 1;
       for (int zo = 0; zo < nz; zo += 4)
-        chunk2<B, DIR, ZC, NR, 4, PK>(Rs[PK == 1 ? 2 * cur : cur], Rs[PK == 1 ? 2 * cur + 1 : cur], Ms[cur], Hx[cur], Lt, Lb, kLA, kLB, dW, z0, zo, zmax,
+        chunk2<B, DIR, ZC, NR, 4>(Rs[cur], Ms[cur], Hx[cur], Lt, Lb, kLA, kLB, dW, z0, zo, zmax,
                                   inA, inB, lane, wp, best, bestz, wchunk, wlo, whi);
     }
     cp_async_wait_all();
@@ -524,7 +395,7 @@ __device__ __forceinline__ void sweep2_body(const SweepArgs& a, const int bx, co
 // One CTA per 30 x (2 NR - 2) job; in sweep4-fixup list mode a persistent
 // grid walks the job list the list kernel built (only jobs that touch
 // guard-flagged tiles), so an empty list costs one short wave.
-template <int B, int DIR, int ZC, int NR, int MINB, int PK>
+template <int B, int DIR, int ZC, int NR, int MINB>
 __global__ void __launch_bounds__(NR * 32, MINB) sweep2_kernel(const SweepArgs a) {
   pdl_wait();
   // one inlined copy of the body (instruction cache): the plain launch is a
@@ -538,21 +409,22 @@ __global__ void __launch_bounds__(NR * 32, MINB) sweep2_kernel(const SweepArgs a
       bx = job % a.fix_nbx;
       by = job / a.fix_nbx;
     }
-    sweep2_body<B, DIR, ZC, NR, MINB, PK>(a, bx, by);
+    sweep2_body<B, DIR, ZC, NR, MINB>(a, bx, by);
     if (lm) __syncthreads();   // shared memory is reused by the next job
   }
 }
 
-template <int B, int DIR, int ZC, int NR, int MINB, int PK = 0>
+// sweep2 job geometry: NR warps x 2 pixel rows (NROW - 2 output rows per
+// job), NR = 16 at b = 5 and 8 otherwise (launch_fixup_list reads this too).
+constexpr int sweep2_nr(int b) { return b == 5 ? 16 : 8; }
+
+template <int B, int DIR, int ZC, int NR, int MINB>
 cudaError_t launch2(const SweepArgs& a, cudaStream_t s) {
-  constexpr size_t smem = Sweep2Smem<B, ZC, NR, PK>::bytes();
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(sweep2_kernel<B, DIR, ZC, NR, MINB, PK>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
+  static_assert(NR == sweep2_nr(B), "job geometry shared with launch_fixup_list");
+  constexpr size_t smem = Sweep2Smem<B, ZC, NR>::bytes();
+  static SmemAttr attr;
+  cudaError_t e = attr.ensure(sweep2_kernel<B, DIR, ZC, NR, MINB>, smem);
+  if (e != cudaSuccess) return e;
   constexpr int NROW = 2 * NR;
   // CTA rows stay on the whole-image grid (row bands are then bit-identical:
   // the per-CTA offset c of the right strip depends on the CTA)
@@ -563,47 +435,11 @@ cudaError_t launch2(const SweepArgs& a, cudaStream_t s) {
     b.fix_nbx = grid.x;
     grid = dim3(std::min<unsigned>(grid.x * grid.y, 2 * 148), 1);
   }
-  return launch_pdl(sweep2_kernel<B, DIR, ZC, NR, MINB, PK>, grid, dim3(NR * 32), smem, s, b);
-}
-
-int g_v2 = -1;
-int v2() {
-  if (g_v2 < 0) {
-    const char* v = getenv("MSHBM_SWEEP2_VARIANT");
-    g_v2 = v ? atoi(v) : 0;
-  }
-  return g_v2;
+  return launch_pdl(sweep2_kernel<B, DIR, ZC, NR, MINB>, grid, dim3(NR * 32), smem, s, b);
 }
 
 template <int DIR>
 cudaError_t launch2_dir(const SweepArgs& a, cudaStream_t s) {
-  if (DIR > 0) {
-    switch (v2() * 100 + a.block) {
-      case 103: return launch2<3, DIR, 16, 8, 2, 1>(a, s);
-      case 105: return launch2<5, DIR, 16, 16, 1, 1>(a, s);
-      case 107: return launch2<7, DIR, 16, 8, 2, 1>(a, s);
-      case 109: return launch2<9, DIR, 16, 8, 1, 1>(a, s);
-      case 111: return launch2<11, DIR, 16, 8, 1, 1>(a, s);
-      case 207: return launch2<7, DIR, 12, 8, 2, 1>(a, s);
-      case 307: return launch2<7, DIR, 16, 16, 1, 1>(a, s);
-      case 807: return launch2<7, DIR, 16, 8, 2, 2>(a, s);
-      case 907: return launch2<7, DIR, 16, 16, 1, 2>(a, s);
-      case 805: return launch2<5, DIR, 16, 16, 1, 2>(a, s);
-      case 809: return launch2<9, DIR, 16, 8, 1, 2>(a, s);
-      case 803: return launch2<3, DIR, 16, 8, 2, 2>(a, s);
-      case 407: return launch2<7, DIR, 12, 8, 2>(a, s);
-      case 507: return launch2<7, DIR, 16, 16, 1>(a, s);
-      case 607: return launch2<7, DIR, 8, 16, 2>(a, s);
-      case 707: return launch2<7, DIR, 12, 16, 1>(a, s);
-      case 409: return launch2<9, DIR, 12, 8, 1>(a, s);
-      case 509: return launch2<9, DIR, 8, 8, 2>(a, s);
-      case 405: return launch2<5, DIR, 16, 8, 2>(a, s);
-      case 505: return launch2<5, DIR, 12, 16, 1>(a, s);
-      case 403: return launch2<3, DIR, 16, 16, 1>(a, s);
-      case 503: return launch2<3, DIR, 24, 8, 2>(a, s);
-      default: break;
-    }
-  }
   switch (a.block) {
     case 3: return launch2<3, DIR, 16, 8, 2>(a, s);
     case 5: return launch2<5, DIR, 16, 16, 1>(a, s);
@@ -616,8 +452,8 @@ cudaError_t launch2_dir(const SweepArgs& a, cudaStream_t s) {
 
 }  // namespace
 
-// sweep4 fixup job list: the sweep2 jobs (default variant geometry for b:
-// 30 columns x 2 NR - 2 rows, NR = 16 at b = 5, 8 otherwise) whose output
+// sweep4 fixup job list: the sweep2 jobs (30 columns x 2 NR - 2 rows,
+// NR = sweep2_nr(b), the geometry launch2 uses) whose output
 // pixels touch a tile the sweep4 guard flagged.  One thread per job; *count
 // is zeroed with the flags before every run.
 __global__ void __launch_bounds__(256) fixup_list_kernel(const unsigned* flags, int64_t flags_ld,
@@ -638,7 +474,7 @@ __global__ void __launch_bounds__(256) fixup_list_kernel(const unsigned* flags, 
 
 cudaError_t launch_fixup_list(const unsigned* flags, int64_t flags_ld, int tile_h, int h, int w,
                               RowBand rows, int block, int* list, int* count, cudaStream_t s) {
-  const int nr = block == 5 ? 16 : 8;   // the sweep2 variant launch2_dir picks
+  const int nr = sweep2_nr(block);
   const int job_rows = 2 * nr - 2;
   const int lo = (rows.lo / job_rows) * job_rows;
   const int nbx = (w + 29) / 30, nby = std::max((rows.hi - lo + job_rows - 1) / job_rows, 0);

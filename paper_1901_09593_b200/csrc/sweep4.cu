@@ -513,7 +513,8 @@ int sweep4_th() {
   if (g_th < 0) {
     const char* v = getenv("MSHBM_SWEEP4_TH");
     g_th = v ? atoi(v) : 32;
-    if (g_th < 2 || (g_th & 1)) g_th = 32;
+    // <= 32: the band plans size their statistics halos for 32-row tiles
+    if (g_th < 2 || (g_th & 1) || g_th > 32) g_th = 32;
   }
   return g_th;
 }
@@ -527,14 +528,8 @@ cudaError_t launch4(const SweepArgs& a, cudaStream_t s) {
   const int passes = (nzw + kNWMax - 1) / kNWMax;
   const int nw = (nzw + passes - 1) / passes;
   const S4Layout<B, G> lay(th, nw, passes * nw);
-  static size_t configured = 0;
-  if (configured < lay.bytes) {
-    cudaError_t e = cudaFuncSetAttribute(sweep4_kernel<B, DIR, G>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)lay.bytes);
-    if (e != cudaSuccess) return e;
-    configured = lay.bytes;
-  }
+  static SmemAttr attr;
+  if (cudaError_t e = attr.ensure(sweep4_kernel<B, DIR, G>, lay.bytes); e != cudaSuccess) return e;
   // CTA rows on the whole-image grid (row bands bit-identical to whole runs)
   SweepArgs b = a;
   b.rows.lo = (a.rows.lo / th) * th;

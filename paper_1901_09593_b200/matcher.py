@@ -41,9 +41,14 @@ __all__ = [
     "run_batch",
 ]
 
-# Per-stage CUDA-event timings in the trace (direct launches instead of the
-# captured CUDA graph).  bench.py turns this off.
-STAGE_TIMING = True
+# Launch every kernel directly instead of replaying the plan's CUDA graph
+# (tests exercise both paths; stage timings are filled either way, from the
+# graph's event-record nodes or the direct path's event records).
+DIRECT_LAUNCH = False
+
+
+def _flags() -> int:
+    return _lib.FLAG_TIMING | (_lib.FLAG_NO_GRAPH if DIRECT_LAUNCH else 0)
 
 
 class ConfigError(ValueError):
@@ -153,6 +158,8 @@ class LevelTrace:
                  refined=t.refined, refine_evals=t.refine_evals,
                  median_replaced=t.median_replaced)
         if timed:
+            # the 3x3-summed refinement runs inside the selection sweep, so
+            # its time is reported under "select" and "refine" is 0
             lt.seconds = {"select": t.ms_select / 1e3, "refine": t.ms_refine / 1e3,
                           "median": t.ms_median / 1e3}
             if t.ms_upsample or t.level < 0:
@@ -301,8 +308,13 @@ def _as_f32(img) -> np.ndarray:
                                 dtype=np.float32)
 
 
-def _trace_from(tr, K: int, timed: bool, build_seconds: float, t_start: float) -> PipelineTrace:
-    out = PipelineTrace(build_seconds=build_seconds)
+def _trace_from(tr, K: int, timed: bool, t_start: float, user_pyramid: bool = False
+                ) -> PipelineTrace:
+    """PipelineTrace from the C records; build_seconds is the device time of
+    the pyramid construction (0 for a caller-supplied pyramid, as the
+    reference, matcher.py:410-416)."""
+    build = 0.0 if (user_pyramid or not timed) else tr[0].ms_build / 1e3
+    out = PipelineTrace(build_seconds=build)
     out.levels = [LevelTrace.from_c(tr[t], timed) for t in range(K + 1)]
     out.total_seconds = time.perf_counter() - t_start
     return out
@@ -332,11 +344,10 @@ def run_pipeline(left, right, config: MatchConfig, workers: int = 1,
     tr = (_lib.LevelTraceC * (K.value + 1))()
     d16 = np.empty((h, w), dtype=np.int16)
     c32 = np.empty((h, w), dtype=np.float32)
-    flags = _lib.FLAG_TIMING if STAGE_TIMING else 0
     _lib.check(_lib.lib().mshbm_run_pipeline(
         ctx, lf.ctypes.data, rf.ctypes.data, h, w, w, C.byref(cfg), d16.ctypes.data,
-        c32.ctypes.data, w, tr, C.byref(K), _lib.IO_HOST, flags, None), ctx)
-    trace = _trace_from(tr, K.value, STAGE_TIMING, 0.0, t_start)
+        c32.ctypes.data, w, tr, C.byref(K), _lib.IO_HOST, _flags(), None), ctx)
+    trace = _trace_from(tr, K.value, True, t_start)
     return d16.astype(np.float64), c32.astype(np.float64), trace
 
 
@@ -360,10 +371,11 @@ def run_pipeline_device(left, right, config: MatchConfig, trace: bool = True, st
     c32 = torch.empty((h, w), dtype=torch.float32, device=lt.device)
     tr = (_lib.LevelTraceC * (K.value + 1))() if trace else None
     s = C.c_void_p(stream.cuda_stream) if stream is not None else _lib.current_stream()
+    t0 = time.perf_counter()
     _lib.check(_lib.lib().mshbm_run_pipeline(
         ctx, lt.data_ptr(), rt.data_ptr(), h, w, w, C.byref(cfg), d16.data_ptr(),
-        c32.data_ptr(), w, tr, C.byref(K), _lib.IO_DEVICE, 0, s), ctx)
-    t = _trace_from(tr, K.value, False, 0.0, time.perf_counter()) if trace else None
+        c32.data_ptr(), w, tr, C.byref(K), _lib.IO_DEVICE, _flags() if trace else 0, s), ctx)
+    t = _trace_from(tr, K.value, True, t0) if trace else None
     return d16, c32, t
 
 
@@ -393,7 +405,7 @@ def _run_user_pyramid(pyramid: StereoPyramid, config: MatchConfig, t_start: floa
     _lib.check(_lib.lib().mshbm_run_pyramid(ctx, n, ptrL, ptrR, hs, ws, lds, dms, bks,
                                             C.byref(cfg), d16.data_ptr(), c32.data_ptr(), w,
                                             tr, _lib.current_stream()), ctx)
-    trace = _trace_from(tr, n - 1, False, 0.0, t_start)
+    trace = _trace_from(tr, n - 1, False, t_start, user_pyramid=True)
     return (d16.cpu().numpy().astype(np.float64), c32.cpu().numpy().astype(np.float64), trace)
 
 
@@ -463,5 +475,5 @@ def run_pipeline_band(left, right, config: MatchConfig, row_begin: int, row_end:
         ctx, lt.data_ptr(), rt.data_ptr(), h, w, w, C.byref(cfg), int(row_begin), int(row_end),
         d16.data_ptr(), c32.data_ptr(), w, tr, C.byref(K), _lib.IO_DEVICE, 0,
         _lib.current_stream()), ctx)
-    t = _trace_from(tr, K.value, False, 0.0, time.perf_counter()) if trace else None
+    t = _trace_from(tr, K.value, False, time.perf_counter()) if trace else None
     return d16, c32, t

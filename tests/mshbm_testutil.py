@@ -59,20 +59,24 @@ def counts_close(a, b, rel=2e-3):
 
 
 def classify_mismatches(d_gpu, d_ref, left, right, block, d_max, sign="middlebury",
-                        tol=1e-4):
+                        tol=1e-4, return_pixels=False, c_gpu=None, alpha=0.9):
     """Explain level-0 disparity mismatches.
 
     A mismatch is a *near tie* when the reference's own cost or its clipped
-    3x3-averaged cost differs by < ``tol`` between the two disparities, and
-    a *median descendant* when it lies within the 5x5 median window of a
-    near tie.  Returns (n_mismatch, n_near_tie, n_descendant, n_unexplained).
+    3x3-averaged cost differs by < ``tol`` between the two disparities, or
+    (with ``c_gpu``) when its final cost lies within ``tol`` of ``alpha`` (an
+    alpha-gate near tie: refine and median run only for C <= alpha).  It is
+    a *median descendant* when its 5x5 median window holds a near-tie
+    mismatch or any alpha-gate near-tie pixel (the gate decides which
+    neighbours qualify, matcher.py:345-352).  Returns (n_mismatch, n_near_tie, n_descendant, n_unexplained)
+    (+ the unexplained pixels' (row, col) list with ``return_pixels``).
     """
     from oracle import mshbm_oracle as O
     d_gpu = np.asarray(d_gpu).astype(np.int64)
     d_ref = np.asarray(d_ref).astype(np.int64)
     bad = np.argwhere(d_gpu != d_ref)
     if bad.size == 0:
-        return 0, 0, 0, 0
+        return (0, 0, 0, 0, []) if return_pixels else (0, 0, 0, 0)
     e = O.Engine(left, right, block, d_max, sign=sign)
     h, w = d_ref.shape
     ties = []
@@ -84,10 +88,18 @@ def classify_mismatches(d_gpu, d_ref, left, right, block, d_max, sign="middlebur
         s = e.dsi_rows(np.array([r for r, _ in nb]), np.array([c for _, c in nb])).sum(0)
         ties.append(min(abs(own[a] - own[b]), abs(s[a] - s[b]) / len(nb)) < tol)
     ties = np.array(ties)
-    tie_px = bad[ties]
+    gate = np.zeros(d_ref.shape, dtype=bool)
+    if c_gpu is not None:
+        gate = np.abs(np.asarray(c_gpu, np.float64) - alpha) < tol
+        ties |= gate[bad[:, 0], bad[:, 1]]
+    tie_px = np.concatenate([bad[ties], np.argwhere(gate)])
     desc = 0
+    other = []
     for k, (i, j) in enumerate(bad):
         if not ties[k] and tie_px.size and np.any(np.max(np.abs(tie_px - [i, j]), axis=1) <= 2):
             desc += 1
+        elif not ties[k]:
+            other.append((int(i), int(j)))
     n = len(bad)
-    return n, int(ties.sum()), desc, n - int(ties.sum()) - desc
+    out = (n, int(ties.sum()), desc, n - int(ties.sum()) - desc)
+    return out + (other,) if return_pixels else out

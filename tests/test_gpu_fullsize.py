@@ -1,12 +1,36 @@
-"""GPU parity at the full BASELINE sizes against the real reference.
+"""GPU parity at the full BASELINE sizes.
 
-`tests/golden/full_C2.npz` and `full_C4.npz` hold the reference's
-`run_pipeline` outputs (radius-generalised driver, `tools/make_golden.py full`)
-for the full 1472x992 C2 pair and the first 1280x720 C4 pair; the images are
-regenerated here from the seeded BASELINE generator.  C1's golden is full size
-already (test_gpu_parity); C3 and C5 are covered at parity size and by the
-sweep4-vs-sweep2 and row-band properties.  Gates as everywhere:
-disparities exact except near ties (<= 0.05 % of the image), costs within 1e-4.
+Goldens (outputs only; the images are regenerated from the seeded BASELINE
+generator, `synthetic.make_pair`):
+
+* `full_C2.npz`, `full_C3.npz`, `full_C4.npz` -- the real reference's
+  `run_pipeline` (radius-generalised driver, `tools/make_golden.py`) on the
+  full 1472x992 C2 pair, the full 2944x1984 C3 pair and the first 1280x720
+  C4 pair (65 s, 413 s and 25 s of reference CPU time).
+* `crop_C5_2048x1536.npz` -- the real reference on a 2048x1536 canvas of
+  C5 (D=512, 6 levels, b=7, r=2); large enough that level 0 runs sweep4.
+* `oracle_C5.npz` -- full 8192x6144 C5 from the C/OpenMP oracle
+  (`oracle/mshbm_oracle.c`; the reference itself would need ~0.5 TB).  The
+  oracle reproduces every reference golden above exactly
+  (`tests/test_oracle_c.py`).  Costs are stored on every 8th row.
+
+Mismatches that are neither near ties nor 5x5-median descendants of one
+are attributed by teacher forcing: the GPU stage API (upsample_prior ->
+select -> refine -> median, `match_level_with_prior`) reruns level 0 from
+the C oracle's level-1 maps (the reference's prior).  A pixel that then
+agrees with the golden owes its mismatch to a level-1 difference (a coarse
+near tie, propagated through the prior), not to level-0 arithmetic; any
+pixel left after that fails the test.
+
+Each golden runs through both product paths: direct kernel launches
+(`matcher.DIRECT_LAUNCH`) and the plan's CUDA-graph replay, the default of
+the drop-in `run_pipeline` and the path `bench.py` times
+(`run_pipeline_device`).  Gates: disparities
+exact except near ties (<= 0.05 % of the image, every mismatch classified:
+a near tie of the winner-take-all or of the alpha gate, or a descendant of
+one through the 5x5 median or the level-1 prior),
+costs within 1e-4 where disparities agree, trace counters exact when no
+pixel flipped.
 """
 import os
 
@@ -17,6 +41,7 @@ from mshbm_testutil import classify_mismatches, counts_close, counts_of, parity_
 
 pytestmark = pytest.mark.gpu
 GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+CASES = ["full_C2", "full_C4", "full_C3", "crop_C5_2048x1536", "oracle_C5"]
 
 
 @pytest.fixture(scope="module")
@@ -28,23 +53,75 @@ def gpu():
     return g
 
 
-@pytest.mark.parametrize("name", ["C2", "C4"])
-def test_full_size_config_matches_reference(gpu, name):
+def _load(name):
+    path = os.path.join(GOLDEN, f"{name}.npz")
+    if not os.path.exists(path):
+        pytest.skip(f"{name}.npz not generated")
+    return np.load(path)
+
+
+def _inputs(name, g):
     from paper_1901_09593_b200.synthetic import CONFIGS, make_pair
-    g = np.load(os.path.join(GOLDEN, f"full_{name}.npz"))
-    cfg = CONFIGS[name]
-    left, right, _ = make_pair(cfg, seed=int(g["seed"]))
+    cfg = CONFIGS[name.split("_")[1]]
+    if "shape" in g:
+        h, w = (int(v) for v in g["shape"])
+        left, right, _ = make_pair(cfg, seed=int(g["seed"]), height=h, width=w)
+    else:
+        left, right, _ = make_pair(cfg, seed=int(g["seed"]))
+    return cfg, left, right
+
+
+def _prior_descendants(gpu, cfg, left, right, pixels, ref_d):
+    """How many of ``pixels`` (unexplained level-0 mismatches) the GPU gets
+    right when level 0 reruns from the reference's level-1 maps (C oracle,
+    pinned to the reference)."""
+    from oracle import c_oracle as CO
+    _, _, _, maps = CO.run_pipeline(left, right, cfg.d_max, cfg.levels, cfg.block,
+                                    radius=cfg.radius, levels_out=True)
+    eng = gpu.CostEngine(left.astype(np.float64), right.astype(np.float64), cfg.block,
+                         cfg.d_max)
+    d_hat, c_hat = gpu.upsample_prior(maps[1][0], maps[1][1], left.shape)
+    tf_d, _ = gpu.match_level_with_prior(eng, d_hat, c_hat, 0.9, 0.9, cfg.radius)
+    return sum(1 for i, j in pixels if tf_d[i, j] == ref_d[i, j])
+
+
+@pytest.mark.parametrize("path", ["direct", "graph"])
+@pytest.mark.parametrize("name", CASES)
+def test_full_size_config_matches_reference(gpu, name, path):
+    import torch
+    g = _load(name)
+    cfg, left, right = _inputs(name, g)
     mc = gpu.MatchConfig(d_max=cfg.d_max, levels=cfg.levels, block=cfg.block, radius=cfg.radius)
-    d, c, trace = gpu.run_pipeline(left, right, mc)
-    frac, cerr, med = parity_report(d, c, g["disparity"], g["cost"], 1e-4)
-    n, ties, desc, unexplained = classify_mismatches(d, g["disparity"], left, right, cfg.block,
-                                                     cfg.d_max)
-    msg = (f"{name}: discrepant {frac:.4%}, {n} mismatches ({ties} near ties, {desc} median "
-           f"descendants, {unexplained} other), max cost err {cerr:.2e}, median {med:.1e}")
+    if path == "direct":
+        gpu.matcher.DIRECT_LAUNCH = True
+        try:
+            d, c, trace = gpu.run_pipeline(left, right, mc)
+        finally:
+            gpu.matcher.DIRECT_LAUNCH = False
+        assert trace.build_seconds > 0 and trace.levels[-1].seconds["select"] > 0
+    else:
+        dd, cc, trace = gpu.run_pipeline_device(torch.from_numpy(left).cuda(),
+                                                torch.from_numpy(right).cuda(), mc, trace=True)
+        d = dd.cpu().numpy().astype(np.float64)
+        c = cc.cpu().numpy().astype(np.float64)
+    ref_d = g["disparity"].astype(np.float64)
+    rows = g["cost_rows"] if "cost_rows" in g else slice(None)
+    frac_d = float(np.mean(d != ref_d))
+    frac, cerr, med = parity_report(d[rows], c[rows], ref_d[rows], g["cost"], 1e-4)
+    n, ties, desc, unexplained, other = classify_mismatches(
+        d, ref_d, left, right, cfg.block, cfg.d_max, return_pixels=True, c_gpu=c)
+    prior_desc = _prior_descendants(gpu, cfg, left, right, other, ref_d) if unexplained else 0
+    msg = (f"{name}/{path}: {n} disparity mismatches ({frac_d:.5%}: {ties} near ties, {desc} "
+           f"median descendants, {prior_desc} level-1 prior descendants, "
+           f"{unexplained - prior_desc} other), cost-discrepant {frac:.5%} of the "
+           f"checked pixels, max cost err {cerr:.2e}, median {med:.1e}")
     print(msg)
-    assert frac <= 5e-4, msg
+    assert frac_d <= 5e-4 and frac <= 5e-4, msg
     assert cerr <= 1e-4, msg
     assert med <= 1e-6, msg
-    # other mismatches descend from a coarse-level near tie through the prior
-    assert unexplained <= max(2, 2e-5 * d.size), msg
-    assert counts_close(counts_of(trace), g["counts"]), (counts_of(trace), g["counts"])
+    assert unexplained - prior_desc == 0, msg
+    got = counts_of(trace)
+    if n == 0 and frac == 0.0:
+        np.testing.assert_array_equal(got, g["counts"], err_msg=msg)
+    else:
+        assert counts_close(got, g["counts"]), (got, g["counts"])

@@ -28,7 +28,6 @@ def gpu():
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     import paper_1901_09593_b200 as g
-    g.matcher.STAGE_TIMING = True
     return g
 
 

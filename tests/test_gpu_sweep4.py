@@ -67,7 +67,7 @@ import sys, numpy as np
 sys.path.insert(0, "."); sys.path.insert(0, "tests")
 import paper_1901_09593_b200 as gpu
 from mshbm_testutil import load_golden
-gpu.matcher.STAGE_TIMING = False          # CUDA-graph replay path
+gpu.matcher.DIRECT_LAUNCH = False         # CUDA-graph replay path
 g = load_golden("pipe_shift48_k0.npz")
 d_max, levels, block, r, paper = (int(v) for v in g["params"])
 cfg = gpu.MatchConfig(d_max=d_max, levels=levels, block=block, radius=r)
@@ -81,9 +81,21 @@ print(int((~same).sum()), float(np.abs(c - g["cost"])[same].max()))
 @pytest.mark.skipif(os.environ.get("MSHBM_SWEEP4") == "2", reason="already forced")
 def test_guard_fixup_runs_in_graph_replay():
     """shift48 (smooth, [0, 1], low contrast) has tiles the sweep4 precision
-    guard flags; in graph replay their fixup is a conditional node switched on
-    by sweep4.  Without it those tiles would carry no output at all."""
+    guard flags; in graph replay their pixels come from the sweep2 fixup
+    launch that walks the guard's job list (built on the statistics branch).
+    Without it those tiles would carry no output at all."""
     r = _run({"MSHBM_SWEEP4": "2"}, ["-c", _GUARD])
     assert r.returncode == 0, r.stderr[-3000:]
     mism, cerr = r.stdout.split()
     assert int(mism) == 0 and float(cerr) <= 5e-5, r.stdout
+
+
+@pytest.mark.skipif(os.environ.get("MSHBM_SWEEP_IMPL") == "1", reason="already forced")
+def test_parity_suite_with_one_pixel_per_thread_sweep():
+    """The one-pixel-per-thread sweep (csrc/sweep.cu sweep_kernel; opt-in with
+    MSHBM_SWEEP_IMPL=1, the reference for sweep2's pixel-pair algebra) on the
+    reference goldens."""
+    r = _run({"MSHBM_SWEEP_IMPL": "1", "MSHBM_SWEEP4": "0"},
+             ["-m", "pytest", "-q", "-x", "-m", "gpu", "-p", "no:cacheprovider",
+              "tests/test_gpu_parity.py", "-k", "pipeline_matches_reference_golden"])
+    assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]

@@ -44,15 +44,19 @@ def test_pipeline_matches_reference(path):
     np.testing.assert_array_equal(counts, g["counts"])
 
 
-@pytest.mark.parametrize("name", ["C2", "C4", "C3"])
-def test_full_size_matches_reference(name):
-    path = os.path.join(GOLDEN, f"full_{name}.npz")
+@pytest.mark.parametrize("golden", ["full_C2", "full_C4", "full_C3", "crop_C5_2048x1536"])
+def test_full_size_matches_reference(golden):
+    path = os.path.join(GOLDEN, f"{golden}.npz")
     if not os.path.exists(path):
         pytest.skip(f"{path} not generated")
     from paper_1901_09593_b200.synthetic import CONFIGS, make_pair
     g = np.load(path)
-    cfg = CONFIGS[name]
-    left, right, _ = make_pair(cfg, seed=int(g["seed"]))
+    cfg = CONFIGS[golden.split("_")[1]]
+    if "shape" in g:
+        h, w = (int(v) for v in g["shape"])
+        left, right, _ = make_pair(cfg, seed=int(g["seed"]), height=h, width=w)
+    else:
+        left, right, _ = make_pair(cfg, seed=int(g["seed"]))
     d, c, counts = CO.run_pipeline(left, right, cfg.d_max, cfg.levels, cfg.block,
                                    radius=cfg.radius)
     np.testing.assert_array_equal(d, g["disparity"])

@@ -195,6 +195,28 @@ def crop_case(name, cfg, height, width):
          ref_seconds=np.array(dt))
 
 
+def oracle_c5_case(threads=0):
+    """Full-size C5 (8192x6144, D=512) through the C/OpenMP oracle, which
+    reproduces every reference golden exactly (tests/test_oracle_c.py); the
+    reference itself would need ~0.5 TB of host RAM here.  Stored: int16
+    disparities (whole image), float32 costs on 384 stratified rows (one per
+    16-row group, all 16 phases), counters."""
+    from oracle import c_oracle as CO
+    cfg = CONFIGS["C5"]
+    left, right, _ = make_pair(cfg)
+    t0 = time.perf_counter()
+    d, c, counts = CO.run_pipeline(left, right, cfg.d_max, cfg.levels, cfg.block,
+                                   radius=cfg.radius, threads=threads)
+    dt = time.perf_counter() - t0
+    h = d.shape[0]
+    rows = np.arange(0, h, 16) + (np.arange(h // 16) * 7) % 16
+    print(f"oracle_C5: {left.shape} {dt:.1f}s total_evals={counts[:, 9].sum() + counts[:, 11].sum()}")
+    save("oracle_C5.npz", disparity=d.astype(np.int16), cost=c[rows].astype(np.float32),
+         cost_rows=rows, counts=counts, seed=np.array(cfg.seed),
+         params=np.array([cfg.d_max, cfg.levels, cfg.block, cfg.radius, 0]),
+         oracle_seconds=np.array(dt))
+
+
 def stage_cases():
     rng = np.random.default_rng(20261019)
     out = {}
@@ -391,6 +413,9 @@ def main():
     if sys.argv[1:] == ["full"]:   # full-size C2 and one C4 pair (minutes)
         full_case("C2", CONFIGS["C2"], CONFIGS["C2"].seed)
         full_case("C4", CONFIGS["C4"], CONFIGS["C4"].seed)
+        return
+    if sys.argv[1:] == ["oracle_C5"]:   # full C5 via the C oracle (about 80 s on 8 cores)
+        oracle_c5_case()
         return
     if sys.argv[1:] == ["crop_C5"]:   # 2048x1536 C5 crop (about 16 min, 35 GB)
         crop_case("C5", CONFIGS["C5"], 1536, 2048)

@@ -31,7 +31,7 @@ for name in sys.argv[1:] or ["C2"]:
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / n
     # per-stage timing
-    gpu.matcher.STAGE_TIMING = True
+    gpu.matcher.DIRECT_LAUNCH = False
     _, _, trt = gpu.run_pipeline(l, r, mc)
     print(name, f"{ms:.3f} ms/pair", f"full-search MPD/s {cfg.full_search_pde / ms / 1e3:.0f}",
           f"evaluated {tr.total_evals / ms / 1e3:.0f} MPD/s")
