@@ -119,6 +119,12 @@ int mshbm_resolve_levels(const mshbm_config* cfg, int32_t height, int32_t width,
 int mshbm_downsample(mshbm_ctx* ctx, const double* in, int32_t h, int32_t w,
                      int64_t ld_in, double* out, int64_t ld_out, void* stream);
 
+/* binomial_smooth (pyramid.py:65-68): the (1,4,6,4,1)/16 filter along axis 0
+ * then axis 1 with replicate borders, full resolution (no decimation),
+ * float64 device arrays. */
+int mshbm_binomial_smooth(mshbm_ctx* ctx, const double* in, int32_t h, int32_t w,
+                          int64_t ld_in, double* out, int64_t ld_out, void* stream);
+
 /* ---- whole pipeline (matcher.py:398-466 run_pipeline) ------------------ */
 /* left/right: float32 HxW (row stride ld), host or device per `io`.
  * disparity: int16 HxW (stride ld_out), cost: float32 HxW (stride ld_out).

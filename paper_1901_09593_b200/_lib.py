@@ -77,6 +77,7 @@ SIGNATURES = {
     "mshbm_auto_levels": (C.c_int, [I64, I64, I64, I64, C.POINTER(I32)]),
     "mshbm_resolve_levels": (C.c_int, [C.POINTER(Config), I32, I32, C.POINTER(I32)]),
     "mshbm_downsample": (C.c_int, [P, P, I32, I32, I64, P, I64, P]),
+    "mshbm_binomial_smooth": (C.c_int, [P, P, I32, I32, I64, P, I64, P]),
     "mshbm_run_pipeline": (C.c_int, [P, P, P, I32, I32, I64, C.POINTER(Config), P, P, I64,
                                      P, C.POINTER(I32), I32, I32, P]),
     "mshbm_run_pipeline_band": (C.c_int, [P, P, P, I32, I32, I64, C.POINTER(Config), I32, I32, P,

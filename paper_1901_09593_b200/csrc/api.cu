@@ -820,6 +820,16 @@ int mshbm_downsample(mshbm_ctx* ctx, const double* in, int32_t h, int32_t w, int
   return MSHBM_OK;
 }
 
+int mshbm_binomial_smooth(mshbm_ctx* ctx, const double* in, int32_t h, int32_t w,
+                          int64_t ld_in, double* out, int64_t ld_out, void* stream) {
+  if (!ctx) return fail(nullptr, MSHBM_ERR_VALUE, "null context");
+  if (h < 1 || w < 1) return fail(ctx, MSHBM_ERR_VALUE, "cannot smooth an empty image");
+  CK(cudaSetDevice(ctx->device));
+  CK(launch_binomial_smooth(in, h, w, ld_in, out, ld_out, pick(ctx, stream)));
+  ctx->launches += 1;
+  return MSHBM_OK;
+}
+
 static int prepare_plan(mshbm_ctx* ctx, int32_t height, int32_t width, const mshbm_config* cfg,
                         int32_t band_lo, int32_t band_hi, int32_t slot, int32_t* out_levels,
                         Plan** out) {

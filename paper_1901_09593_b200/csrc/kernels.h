@@ -102,6 +102,8 @@ cudaError_t launch_f32_to_f64(const float* a, const float* b, int h, int w,
 cudaError_t launch_downsample(const double* in0, const double* in1, int h,
                               int w, int64_t ld_in, double* out0, double* out1,
                               int64_t ld_out, cudaStream_t s, int i0 = 0, int i1 = -1);
+cudaError_t launch_binomial_smooth(const double* in, int h, int w, int64_t ld_in, double* out,
+                                   int64_t ld_out, cudaStream_t s);
 // level 1 from the fp32 input, writing the exact fp64 level-0 copy as well
 // (rows 2 i0 .. 2 i1 of it)
 cudaError_t launch_downsample_f32(const float* in0, const float* in1, int h, int w,

@@ -39,7 +39,8 @@ __global__ void f32_to_f64_kernel(const float* a, const float* b, int h, int w,
 template <typename T, bool COPY>
 __global__ void downsample_kernel(const T* in0, const T* in1, int h, int w, int64_t ldi,
                                   double* out0, double* out1, int64_t ldo, int oh, int ow,
-                                  double* cp0, double* cp1, int64_t ldc, int i0, int i1) {
+                                  double* cp0, double* cp1, int64_t ldc, int i0, int i1,
+                                  int step) {
   pdl_wait();
   // output rows [i0, i1) only (row bands compute the rows their levels need)
   const int J = blockIdx.x * blockDim.x + threadIdx.x;
@@ -50,11 +51,11 @@ __global__ void downsample_kernel(const T* in0, const T* in1, int h, int w, int6
   const double k[5] = {1.0 / 16.0, 4.0 / 16.0, 6.0 / 16.0, 4.0 / 16.0, 1.0 / 16.0};
   int rows[5];
 #pragma unroll
-  for (int a = 0; a < 5; ++a) rows[a] = clampi(2 * I + a - 2, 0, h - 1);
+  for (int a = 0; a < 5; ++a) rows[a] = clampi(step * I + a - 2, 0, h - 1);
   double acc = 0.0;
 #pragma unroll
   for (int b = 0; b < 5; ++b) {
-    const int col = clampi(2 * J + b - 2, 0, w - 1);
+    const int col = clampi(step * J + b - 2, 0, w - 1);
     double v = 0.0;
 #pragma unroll
     for (int a = 0; a < 5; ++a) v += k[a] * (double)in[(int64_t)rows[a] * ldi + col];
@@ -898,7 +899,17 @@ cudaError_t launch_downsample(const double* in0, const double* in1, int h,
   dim3 blk(32, 8);
   return launch_pdl(downsample_kernel<double, false>, grid2d(ow, i1 - i0, blk, in1 ? 2 : 1), blk,
                     0, s, in0, in1, h, w, ld_in, out0, out1, ld_out, oh, ow, (double*)nullptr,
-                    (double*)nullptr, (int64_t)0, i0, i1);
+                    (double*)nullptr, (int64_t)0, i0, i1, 2);
+}
+
+// binomial_smooth (pyramid.py:65-68): the same separable 5-tap filter at
+// full resolution (step 1, no decimation); stage API only
+cudaError_t launch_binomial_smooth(const double* in, int h, int w, int64_t ld_in, double* out,
+                                   int64_t ld_out, cudaStream_t s) {
+  dim3 blk(32, 8);
+  return launch_pdl(downsample_kernel<double, false>, grid2d(w, h, blk, 1), blk, 0, s, in,
+                    (const double*)nullptr, h, w, ld_in, out, (double*)nullptr, ld_out, h, w,
+                    (double*)nullptr, (double*)nullptr, (int64_t)0, 0, h, 1);
 }
 
 cudaError_t launch_downsample_f32(const float* in0, const float* in1, int h, int w,
@@ -910,7 +921,7 @@ cudaError_t launch_downsample_f32(const float* in0, const float* in1, int h, int
   if (i1 <= i0) return cudaSuccess;
   dim3 blk(32, 8);
   return launch_pdl(downsample_kernel<float, true>, grid2d(ow, i1 - i0, blk, 2), blk, 0, s, in0,
-                    in1, h, w, ld_in, out0, out1, ld_out, oh, ow, copy0, copy1, ld_copy, i0, i1);
+                    in1, h, w, ld_in, out0, out1, ld_out, oh, ow, copy0, copy1, ld_copy, i0, i1, 2);
 }
 
 cudaError_t launch_stats_f32(const double* img, int h, int w, int64_t ld,

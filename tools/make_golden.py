@@ -29,6 +29,7 @@ sys.path.insert(0, ROOT)
 
 import pyrstereo as ref  # noqa: E402
 from pyrstereo import matcher as ref_matcher  # noqa: E402
+from pyrstereo import pyramid as ref_pyramid  # noqa: E402
 from paper_1901_09593_b200.synthetic import CONFIGS, make_pair  # noqa: E402
 
 COUNT_KEYS = ("trusted", "trusted_evals", "trusted_window_max",
@@ -291,6 +292,58 @@ def stage_cases():
     save("stages.npz", **out)
 
 
+def stage_api_cases():
+    """Stage APIs off run_pipeline's path:
+    CostEngine.plane / full_volume (zncc.py:202-249), dsi_entry,
+    dsi_slice, averaged_dsi (zncc.py:304-350), the EvalCounter tally of each
+    call, match_level_with_prior (matcher.py:362-369) and binomial_smooth
+    (pyramid.py:65-68)."""
+    out = {}
+    rng = np.random.default_rng(20261020)
+    # plane / full_volume on random textures (both sign conventions), incl.
+    # a flat (degenerate) patch so the -1 floor of sigma < eps is pinned
+    for i, (h, w, b, d, sign) in enumerate([(8, 10, 3, 5, "middlebury"),
+                                            (16, 16, 5, 8, "middlebury"),
+                                            (13, 21, 3, 7, "paper"),
+                                            (24, 31, 7, 12, "middlebury")]):
+        left, right = rng.random((h, w)), rng.random((h, w))
+        left[2:6, 2:6] = 0.5
+        e = ref.CostEngine(left, right, block=b, d_max=d, sign=sign)
+        vol = e.full_volume()
+        out[f"vol_l_{i}"], out[f"vol_r_{i}"] = left, right
+        out[f"vol_p_{i}"] = np.array([b, d, 1 if sign == "paper" else 0])
+        out[f"vol_{i}"] = vol
+        out[f"vol_count_{i}"] = np.array(e.counter.count)
+    # dsi_entry / dsi_slice / averaged_dsi on a shifted pair
+    left, right = ref.shifted_pair(9, 12, 2, rng, cutoff=0.2)
+    e = ref.CostEngine(left, right, block=3, d_max=4)
+    pts = [(4, 6, 2), (0, 0, 0), (8, 11, 4), (3, 1, 3), (5, 9, 1)]
+    out["pt_l"], out["pt_r"] = left, right
+    out["pt_ijz"] = np.array(pts)
+    out["pt_entry"] = np.array([ref.dsi_entry(e, i, j, z) for i, j, z in pts])
+    out["pt_slice"] = np.array([e.dsi_slice(i, j).costs for i, j, _ in pts])
+    far = [(-5, -5), (-6, 0), (0, -9)]
+    out["pt_avg"] = np.array([ref.averaged_dsi(e, i, j).costs for i, j, _ in pts])
+    out["pt_avg_far"] = ref.averaged_dsi(e, 0, 0, neighborhood=far).costs
+    out["pt_count"] = np.array(e.counter.count)
+    # match_level_with_prior (r = 1, the reference's own) on a shifted pair
+    srng = np.random.default_rng(8)
+    left, right = ref.shifted_pair(32, 48, 6, srng, cutoff=0.1)
+    e = ref.CostEngine(left, right, block=5, d_max=14)
+    d_hat = np.clip(np.round(6 + srng.normal(0, 2, size=(32, 48))), -3, 17)
+    d_hat[5, 7] = np.nan
+    c_hat = srng.uniform(0.6, 1.0, size=(32, 48))
+    md, mc = ref.match_level_with_prior(e, d_hat, c_hat, 0.9, 0.9)
+    out.update(ml_l=left, ml_r=right, ml_dhat=d_hat, ml_chat=c_hat, ml_d=md, ml_c=mc,
+               ml_count=np.array(e.counter.count))
+    # binomial_smooth (full resolution, no decimation)
+    for i, shp in enumerate([(5, 7), (2, 2), (33, 18)]):
+        img = rng.random(shp) * 255.0
+        out[f"bs_in_{i}"] = img
+        out[f"bs_out_{i}"] = ref_pyramid.binomial_smooth(img)
+    save("stage_api.npz", **out)
+
+
 def scoring_cases():
     """baseline.py / evaluation.py / synthetic.py vectors."""
     out = {}
@@ -409,6 +462,9 @@ def main():
         return
     if sys.argv[1:] == ["formats"]:
         formats_cases()
+        return
+    if sys.argv[1:] == ["stage_api"]:
+        stage_api_cases()
         return
     if sys.argv[1:] == ["full"]:   # full-size C2 and one C4 pair (minutes)
         full_case("C2", CONFIGS["C2"], CONFIGS["C2"].seed)
