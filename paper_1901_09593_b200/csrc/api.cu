@@ -435,6 +435,7 @@ int enqueue(mshbm_ctx* ctx, Plan& p, cudaStream_t s, cudaStream_t side = nullptr
     CK(rec(ev->up1, s));
     SweepArgs a{};
     a.L = l.L; a.R = l.R; a.ld = l.ld;
+    if (k == 0 && !p.user) a.L32 = p.in_l, a.ld32 = p.ld_in;
     a.muR = l.muR; a.isR = l.isR; a.lds = l.ld;
     a.muL = l.muL; a.isL = l.isL;
     a.tile_flags = l.flags; a.flags_ld = l.flags_ld;

@@ -32,6 +32,13 @@ struct SmemAttr {
 
 
 constexpr int kWcNone = -2147483647 - 1;   // "untrusted" window centre
+// sweep4 levels: the trusted-window selection (sweep4.cu prior_select_kernel)
+// runs before the dense sweep and marks its trusted pixels as done (final
+// outputs written) or low (the sweep computes their 3x3 refinement).  Real
+// window centres are >= -radius, so these never collide, and c -+ radius
+// cannot overflow.
+constexpr int kWcLow = -(1 << 30);
+constexpr int kWcDone = -(1 << 30) - 1;
 
 MSHBM_DEV int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
 

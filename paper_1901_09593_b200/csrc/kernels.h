@@ -23,6 +23,8 @@ struct SweepArgs {
   const double* L;      // level images, float64, row stride ld
   const double* R;
   int64_t ld;
+  const float* L32;     // level 0 of a built pyramid: the fp32 input (exact), stride ld32
+  int64_t ld32;
   const float* muR;     // box mean of R (fp32)
   const float* isR;     // 1/sigma_R, 0 where degenerate (fp32)
   int64_t lds;

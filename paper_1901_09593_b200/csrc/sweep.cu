@@ -489,6 +489,7 @@ cudaError_t launch_sweep(const SweepArgs& a, cudaStream_t s, int* n_launch) {
     SweepArgs b = a;
     b.tile_h = sweep4_th();
     if (!sweep4_guard()) b.tile_flags = nullptr;
+    if (n_launch && a.wc != nullptr) ++*n_launch;   // + prior_select_kernel
     return launch_sweep4(b, s);   // + launch_sweep4_fixup (caller's stream choice)
   }
   if (impl >= 2 && sweep2_supported(a.block)) return launch_sweep2(a, s);

@@ -93,16 +93,15 @@ struct S4Layout {
   static constexpr int NC = kTW + 2;            // cost columns (1-pixel halo for 3x3 sums)
   static constexpr int RB = B + 2 * G;          // R ring rows (b + G live + G in flight)
   int th, rwp, mwp, nzw;
-  size_t o_bar, o_lt, o_pp, o_wn, o_rr, o_mr, o_sk, o_rk, o_hs, bytes;
+  size_t o_bar, o_lt, o_pp, o_rr, o_mr, o_sk, o_rk, o_hs, bytes;
   __host__ __device__ S4Layout(int th_, int nw, int nzw_) : th(th_), nzw(nzw_) {
     // ring rows start 16-byte aligned in global memory: up to 3 (R) / 1 (Mp)
     // extra leading elements, and the copy is rounded up to 16 bytes
     rwp = (NV + 32 * nw - 1 + 3 + 3 + 3) & ~3;
     mwp = (NC + 32 * nw - 1 + 1 + 1 + 1) & ~1;
     size_t o = 0;
-    o_bar = o; o += 16;
+    o_bar = o; o += 16;   // the tile's row masks (sel, ref) + the ring's mbarrier
     o_pp = o; o += sizeof(float4) * (th + 2) * (NC / 2);
-    o_wn = o; o += sizeof(int2) * th * kTW;
     o_mr = o; o += sizeof(float2) * 2 * G * mwp;
     o = (o + 15) & ~(size_t)15;
     o_lt = o; o += sizeof(float) * (th + B + 1) * NVP;
@@ -118,13 +117,14 @@ struct S4Layout {
 
 // One row step: cost row k (image row y0 - 1 + k).  Xin = 3-sums of row
 // k - 1, Xout <- 3-sums of row k, Y = 3-sums of rows k-2 + k-1 on entry and
-// rows k-1 + k on exit.  Lane 0 stores the warp's winner key per pixel:
-// selection for output row k - 1 into sk, refinement for row k - 2 into rk.
+// rows k-1 + k on exit.  SEL: full-range winner of output row k - 1 (lane 0
+// stores the warp's key per pixel into sk); REF: 3x3-summed winner of
+// output row k - 2 (into rk).  Rows whose pixels need neither skip the
+// reductions (the tile's row masks, see sweep4_kernel).
 template <int B>
 __device__ __forceinline__ void row_step(
-    const int k, const int th, float (&V)[S4Layout<B>::NV], const float (&Xin)[kTW],
-    float (&Xout)[kTW], float (&Y)[kTW], const float4* __restrict__ Pp,
-    const int4* __restrict__ Wn, const float2* __restrict__ mrow, const int z,
+    const int k, const bool SEL, const bool REF, float (&V)[S4Layout<B>::NV], float (&X)[kTW],
+    float (&Y)[kTW], const float4* __restrict__ Pp, const float2* __restrict__ mrow,
     const float half, const unsigned laneK, const bool lane0, unsigned* __restrict__ sk,
     unsigned* __restrict__ rk) {
   using SL = S4Layout<B>;
@@ -162,48 +162,46 @@ __device__ __forceinline__ void row_step(
     cp[2 * u2] = fma_sat(fmaf(-pp.x, m0.x, cp[2 * u2]) * pp.y, m0.y, half);
     cp[2 * u2 + 1] = fma_sat(fmaf(-pp.z, m1.x, cp[2 * u2 + 1]) * pp.w, m1.y, half);
   }
-  // per output pixel p, in one pass so the cost row dies as it is consumed:
-  // selection winner-take-all for output row k - 1 (keys of lanes outside the
-  // pixel's window [lo, lo + span] are 0), the 3x3 sums (horizontal 3-sum of
-  // this row + the two rows above in Y) and their winner for row k - 2
-  auto wta = [&](auto sel_t, auto ref_t) {
-    constexpr bool SEL = decltype(sel_t)::value, REF = decltype(ref_t)::value;
-    const int4* wrow = Wn + (k - 1) * (kTW / 2);
+  // selection (untrusted pixels: the full range [0, d], no window mask):
+  // key = (bits(c' + 1) - 0x3F800000 + 1) << 5 | (31 - lane), REDUX.MAX = the
+  // warp's first maximum
+  if (SEL) {
     unsigned* srow = sk + (k - 1) * kTW;
-    unsigned* rrow = rk + (k - 2) * kTW;
 #pragma unroll
     for (int p = 0; p < kTW; ++p) {
-      if constexpr (SEL) {
-        const int4 win = wrow[p / 2];   // (lo, span) of pixels p & ~1 and p | 1
-        const int lo = (p & 1) ? win.z : win.x, span = (p & 1) ? win.w : win.y;
-        const unsigned key = (unsigned)(z - lo) <= (unsigned)span
-                                 ? (__float_as_uint(cp[p + 1] + 1.0f) << 5) + laneK
-                                 : 0u;
-        const unsigned r = __reduce_max_sync(kFull, key);
-        if (lane0) srow[p] = r;
-      }
-      const float h = (cp[p] + cp[p + 1]) + cp[p + 2];
-      if constexpr (REF) {
-        const float n = Y[p] + h;
-        const unsigned key = (__float_as_uint(fmaf(n, 0.0625f, 1.0f)) << 5) + laneK;
-        const unsigned r = __reduce_max_sync(kFull, key);
-        if (lane0) rrow[p] = r;
-      }
-      Y[p] = Xin[p] + h;
-      Xout[p] = h;
+      const unsigned key = (__float_as_uint(cp[p + 1] + 1.0f) << 5) + laneK;
+      const unsigned r = __reduce_max_sync(kFull, key);
+      if (lane0) srow[p] = r;
     }
-  };
-  using T1 = std::true_type;
-  using F1 = std::false_type;
-  if (k >= 2 && k <= th) wta(T1{}, T1{});
-  else if (k == 1) wta(T1{}, F1{});
-  else if (k == 0) wta(F1{}, F1{});
-  else wta(F1{}, T1{});
+  }
+  // 3x3 sums (horizontal 3-sum of this row + the two rows above in Y) and,
+  // for REF rows, their winner; the cost row dies as it is consumed
+  unsigned* rrow = rk + (k - 2) * kTW;
+  if (REF) {
+#pragma unroll
+    for (int p = 0; p < kTW; ++p) {
+      const float h = (cp[p] + cp[p + 1]) + cp[p + 2];
+      const float n = Y[p] + h;
+      const unsigned key = (__float_as_uint(fmaf(n, 0.0625f, 1.0f)) << 5) + laneK;
+      const unsigned r = __reduce_max_sync(kFull, key);
+      if (lane0) rrow[p] = r;
+      Y[p] = X[p] + h;
+      X[p] = h;
+    }
+  } else {
+#pragma unroll
+    for (int p = 0; p < kTW; ++p) {
+      const float h = (cp[p] + cp[p + 1]) + cp[p + 2];
+      Y[p] = X[p] + h;
+      X[p] = h;
+    }
+  }
 }
 
 template <int B, int DIR, int G>
-__global__ void __launch_bounds__(kNWMax * 32, 2) sweep4_kernel(const SweepArgs a, const int th) {
+__global__ void __launch_bounds__(kNWMax * 32, 2) sweep4_kernel(const SweepArgs a, const int th_) {
   pdl_wait();
+  const int th = th_;
   using SL = S4Layout<B, G>;
   constexpr int H2 = B / 2, NV = SL::NV, NVP = SL::NVP, NC = SL::NC, RB = SL::RB;
   extern __shared__ float4 smem4[];
@@ -217,11 +215,11 @@ __global__ void __launch_bounds__(kNWMax * 32, 2) sweep4_kernel(const SweepArgs 
   const int nz = tail ? d : d + 1;                          // disparities on lanes
   const int nslot = ((nz + 32 * nw - 1) / (32 * nw)) * nw;  // passes x warps
   const SL lay(th, nw, nslot);
-  unsigned long long* bar = reinterpret_cast<unsigned long long*>(smem + lay.o_bar);
+  unsigned long long* bars = reinterpret_cast<unsigned long long*>(smem + lay.o_bar) + 1;
   unsigned* sK = reinterpret_cast<unsigned*>(smem + lay.o_sk);
   unsigned* rK = reinterpret_cast<unsigned*>(smem + lay.o_rk);
   float4* Pp = reinterpret_cast<float4*>(smem + lay.o_pp);
-  int2* Wn = reinterpret_cast<int2*>(smem + lay.o_wn);
+  unsigned* masks = reinterpret_cast<unsigned*>(smem + lay.o_bar);
   float2* Mr = reinterpret_cast<float2*>(smem + lay.o_mr);
   float* Lt = reinterpret_cast<float*>(smem + lay.o_lt);
   float* Rr = reinterpret_cast<float*>(smem + lay.o_rr);
@@ -240,8 +238,27 @@ __global__ void __launch_bounds__(kNWMax * 32, 2) sweep4_kernel(const SweepArgs 
   // sweep2 fixup launch (launch_sweep4_fixup), which may run concurrently.
   if (a.tile_flags != nullptr && a.tile_flags[(int64_t)(y0 / th) * a.flags_ld + blockIdx.x] != 0)
     return;   // uniform: the whole CTA leaves
-  // ---- prologue: winner slots, left tile L' = L - cL, window bounds
-  if (tid == 0) mbar_init(bar, 1);
+  // ---- which output rows need what.  Pixel states (wc): kWcDone = trusted,
+  // not low, finished by prior_select_kernel; kWcLow = trusted and low: only
+  // the 3x3-summed refinement; kWcNone (or no prior) = untrusted: full-range
+  // selection + refinement.  masks[0] bit o: row o holds an untrusted pixel
+  // (SEL), masks[1] bit o: a pixel needing refinement (REF).  Rows outside
+  // the stage's rows need nothing.
+  if (tid < 2) masks[tid] = 0u;
+  __syncthreads();
+  for (int t = tid; t < th * kTW; t += nt) {
+    const int o = t / kTW, p = t - o * kTW;
+    const int y = y0 + o, x = x0 + p;
+    if (y < a.rows.lo || y >= a.rows.hi || y >= H || x >= W) continue;
+    const int c = a.wc != nullptr ? a.wc[(int64_t)y * a.ldw + x] : kWcNone;
+    if (c == kWcNone) atomicOr(&masks[0], 1u << o);
+    if (c == kWcNone || c == kWcLow) atomicOr(&masks[1], 1u << o);
+  }
+  __syncthreads();
+  const unsigned selm = masks[0], refm = masks[1];
+  if ((selm | refm) == 0u) return;   // uniform: every pixel finished (or none here)
+  // ---- prologue: winner slots, left tile L' = L - cL
+  if (tid == 0) mbar_init(bars, 1);
   for (int t = tid; t < nslot * th * kTW; t += nt) sK[t] = 0u, rK[t] = 0u;
   // centring constant: the L sample at the tile centre (the guard in the L
   // statistics kernel uses the same one)
@@ -251,20 +268,12 @@ __global__ void __launch_bounds__(kNWMax * 32, 2) sweep4_kernel(const SweepArgs 
     const int y = clampi(y0 - 1 - H2 + rr, 0, H - 1), x = clampi(x0 - 1 - H2 + c, 0, W - 1);
     Lt[rr * NVP + c] = (float)(a.L[(int64_t)y * a.ld + x] - cL);
   }
-  for (int t = tid; t < th * kTW; t += nt) {
-    const int o = t / kTW, p = t - o * kTW;
-    const int y = y0 + o, x = x0 + p;
-    int2 win = make_int2(0, d);   // (lo, span): untrusted = the full range
-    if (a.wc != nullptr && y < H && x < W) {
-      const int c = a.wc[(int64_t)y * a.ldw + x];
-      if (c != kWcNone) {
-        const int lo = max(c - a.radius, 0);
-        win = make_int2(lo, min(c + a.radius, d) - lo);
-      }
-    }
-    Wn[t] = win;
-  }
   __syncthreads();
+  // cost row k (output row k - 1) is needed by SEL of row k - 1 and REF of
+  // rows k - 2, k - 1, k; rows nobody needs skip the cost and reductions
+  const unsigned long long needc = ((unsigned long long)selm << 1) |
+                                   ((unsigned long long)refm << 2) |
+                                   ((unsigned long long)refm << 1) | (unsigned long long)refm;
   // per cost pixel: the sum of L' over its window (fp64 sums of the fp32
   // values, so the centring cancels the rounding of L'), separable through
   // per-row horizontal sums, and kL = 1/(b^2 sigma_L)
@@ -293,6 +302,7 @@ __global__ void __launch_bounds__(kNWMax * 32, 2) sweep4_kernel(const SweepArgs 
     pf[0] = (float)s;
     pf[1] = kL;
   }
+  __syncthreads();   // Pp, Lt, the mbarriers
 
   const float* __restrict__ Rp = a.Rp + a.pc;
   const float2* __restrict__ Mp = a.Mp + a.pc;
@@ -321,24 +331,24 @@ __global__ void __launch_bounds__(kNWMax * 32, 2) sweep4_kernel(const SweepArgs 
     const int lb = (DIR > 0 ? (span - (z - zp)) : (z - zp)) + rmis;
     const int mb = (DIR > 0 ? (span - (z - zp)) : (z - zp)) + mmis;
 
-    auto stage_r = [&](int rr) {
+    auto stage_r = [&](int rr, unsigned long long* bar) {
       const int y = clampi(y0 - 1 - H2 + rr, 0, H - 1);
       bulk_g2s(Rr + (rr % RB) * lay.rwp, Rp + ((int64_t)y * a.ldp + rc0), rbytes, bar);
     };
-    auto stage_m = [&](int k) {
+    auto stage_m = [&](int k, unsigned long long* bar) {
       const int y = clampi(y0 - 1 + k, 0, H - 1);
       bulk_g2s(Mr + (k % (2 * G)) * lay.mwp, Mp + ((int64_t)y * a.ldp + mc0), mbytes, bar);
     };
-    __syncthreads();   // previous pass done with the rings (and the prologue)
+    if (pass > 0) __syncthreads();   // previous pass done with the rings
 
     if (tid == 0) {
       fence_proxy_async();
       const int nr0 = min(B + G, th + B + 1), nm0 = min(G, th + 2);
-      mbar_expect_tx(bar, nr0 * rbytes + nm0 * mbytes);
-      for (int rr = 0; rr < nr0; ++rr) stage_r(rr);
-      for (int k = 0; k < nm0; ++k) stage_m(k);
+      mbar_expect_tx(bars, nr0 * rbytes + nm0 * mbytes);
+      for (int rr = 0; rr < nr0; ++rr) stage_r(rr, bars);
+      for (int k = 0; k < nm0; ++k) stage_m(k, bars);
     }
-    mbar_wait(bar, phase);
+    mbar_wait(bars, phase & 1u);
     phase ^= 1u;
 
     float V[NV];
@@ -366,18 +376,23 @@ __global__ void __launch_bounds__(kNWMax * 32, 2) sweep4_kernel(const SweepArgs 
     const bool lane0 = lane == 0;
     unsigned* sk = sK + (pass * nw + wp) * th * kTW;
     unsigned* rk = rK + (pass * nw + wp) * th * kTW;
-    float X1[kTW], X2[kTW], Y[kTW];
+    float X[kTW], Y[kTW];
 #pragma unroll
-    for (int p = 0; p < kTW; ++p) X1[p] = 0.f, X2[p] = 0.f, Y[p] = 0.f;
+    for (int p = 0; p < kTW; ++p) X[p] = 0.f, Y[p] = 0.f;
 
-    // Rows are consumed in pairs of steps: one mbarrier wait and one CTA
-    // barrier per pair; the ring holds the pair's b + 2 R rows and 2 Mp rows
-    // plus the next pair's, prefetched by one thread with bulk copies.
-    auto step = [&](int k, float (&Xin)[kTW], float (&Xout)[kTW]) {
+    // Rows are consumed in groups of G steps: one mbarrier wait and one CTA
+    // barrier per group; the ring holds the group's b + G R rows and G Mp
+    // rows plus the next group's, prefetched by one thread with bulk copies.
+    // One copy of the step body (instruction cache): the SEL / REF
+    // reductions are warp-uniform branches on the tile's row masks.
+    auto step = [&](int k) {
       if (active) {
-        const float2* mrow = Mr + (k % (2 * G)) * lay.mwp + mb;
-        row_step<B>(k, th, V, Xin, Xout, Y, Pp, reinterpret_cast<const int4*>(Wn), mrow, z, half,
-                    laneK, lane0, sk, rk);
+        if ((needc >> k) & 1ull) {
+          const float2* mrow = Mr + (k % (2 * G)) * lay.mwp + mb;
+          const bool sl = k >= 1 && ((selm >> (k - 1)) & 1u);
+          const bool rf = k >= 2 && ((refm >> (k - 2)) & 1u);
+          row_step<B>(k, sl, rf, V, X, Y, Pp, mrow, half, laneK, lane0, sk, rk);
+        }
         // slide V down one row: + row k + B, - row k
         if (k <= th) {
           const float4* lin = reinterpret_cast<const float4*>(Lt + (k + B) * NVP);
@@ -400,7 +415,7 @@ __global__ void __launch_bounds__(kNWMax * 32, 2) sweep4_kernel(const SweepArgs 
 #pragma unroll 1
     for (int k = 0; k < th + 2; k += G) {
       if (k > 0) {
-        mbar_wait(bar, phase);
+        mbar_wait(bars, phase & 1u);
         phase ^= 1u;
         __syncthreads();   // every warp done with the previous group (its slots are reused)
       }
@@ -408,16 +423,13 @@ __global__ void __launch_bounds__(kNWMax * 32, 2) sweep4_kernel(const SweepArgs 
         fence_proxy_async();
         const int r0 = k + B + G, r1 = min(k + B + 2 * G, th + B + 1);
         const int m0 = k + G, m1 = min(k + 2 * G, th + 2);
-        mbar_expect_tx(bar, max(r1 - r0, 0) * rbytes + (m1 - m0) * mbytes);
-        for (int rr = r0; rr < r1; ++rr) stage_r(rr);
-        for (int km = m0; km < m1; ++km) stage_m(km);
+        mbar_expect_tx(bars, max(r1 - r0, 0) * rbytes + (m1 - m0) * mbytes);
+        for (int rr = r0; rr < r1; ++rr) stage_r(rr, bars);
+        for (int km = m0; km < m1; ++km) stage_m(km, bars);
       }
-#pragma unroll
-      for (int g = 0; g < G; g += 2) {
-        if (k + g < th + 2) {
-          step(k + g, X1, X2);
-          step(k + g + 1, X2, X1);
-        }
+#pragma unroll 1
+      for (int g = 0; g < G; ++g) {
+        if (k + g < th + 2) step(k + g);
       }
     }
   }
@@ -459,7 +471,10 @@ __global__ void __launch_bounds__(kNWMax * 32, 2) sweep4_kernel(const SweepArgs 
   for (int t = tid; t < th * kTW; t += nt) {
     const int o = t / kTW, p = t - o * kTW;
     const int i = y0 + o, j = x0 + p;
-    if (i >= H || j >= W) continue;
+    if (i >= H || j >= W || i < a.rows.lo || i >= a.rows.hi) continue;
+    const int wcp = a.wc != nullptr ? a.wc[(int64_t)i * a.ldw + j] : kWcNone;
+    if (wcp != kWcNone && wcp != kWcLow) continue;   // finished by prior_select_kernel
+    const bool sel = wcp == kWcNone;   // untrusted: full-range selection first
     unsigned bs = 0u, br = 0u;
     int zs = -1, nbz = 0;
     for (int w = 0; w < nslot; ++w) {
@@ -467,22 +482,16 @@ __global__ void __launch_bounds__(kNWMax * 32, 2) sweep4_kernel(const SweepArgs 
       if ((ks >> 5) > (bs >> 5)) bs = ks, zs = 32 * w + 31 - (int)(ks & 31u);
       if ((kr >> 5) > (br >> 5)) br = kr, nbz = 32 * w + 31 - (int)(kr & 31u);
     }
-    bool trusted = false;
-    int lo = 0, hi = d;
-    if (a.wc != nullptr) {
-      const int c = a.wc[(int64_t)i * a.ldw + j];
-      if (c != kWcNone) trusted = true, lo = max(c - a.radius, 0), hi = min(c + a.radius, d);
-    }
     if (zs < 0) {
-      // no candidate on an active warp: the window lies where every right
-      // centre is outside the image, all -1 (value 1), smallest legal z
+      // no candidate on an active warp: every right centre is outside the
+      // image, all -1 (value 1), smallest z
       bs = 1u << 5;
-      zs = trusted ? lo : 0;
+      zs = 0;
     }
     if (tail) {   // z = d last: it wins only if strictly better
       const float* ct = Ct + o * NC + p;
       const unsigned vd = __float_as_uint(ct[NC + 1] + 1.0f) - 0x3F800000u + 1u;
-      if (hi == d && vd > (bs >> 5)) bs = vd << 5, zs = d;
+      if (vd > (bs >> 5)) bs = vd << 5, zs = d;
       const float nsum = (((ct[0] + ct[1]) + ct[2]) + ((ct[NC] + ct[NC + 1]) + ct[NC + 2])) +
                          ((ct[2 * NC] + ct[2 * NC + 1]) + ct[2 * NC + 2]);
       const unsigned vn = __float_as_uint(fmaf(nsum, 0.0625f, 1.0f)) - 0x3F800000u + 1u;
@@ -493,12 +502,115 @@ __global__ void __launch_bounds__(kNWMax * 32, 2) sweep4_kernel(const SweepArgs 
     const float nsum = (n1 - 1.0f) * 16.0f;
     const int members = ((i > 0) + 1 + (i < H - 1)) * ((j > 0) + 1 + (j < W - 1));
     const float nbc = 2.f * nsum / (float)members - 1.f;
-    const bool low = (double)cs <= a.alpha;
+    // trusted low pixels were counted by prior_select_kernel
+    const bool low = !sel || (double)cs <= a.alpha;
     const int64_t off = (int64_t)i * a.ldo + j;
     a.dout[off] = (int16_t)(low ? nbz : zs);
     a.cout[off] = low ? nbc : cs;
     a.low[off] = (uint8_t)low;
-    nlow += (low && i >= a.rows.cnt_lo && i < a.rows.cnt_hi) ? 1u : 0u;
+    nlow += (sel && low && i >= a.rows.cnt_lo && i < a.rows.cnt_hi) ? 1u : 0u;
+  }
+  const int slot[1] = {kCntRefined};
+  const unsigned long long val[1] = {nlow};
+  const bool mx[1] = {false};
+  block_accumulate<1>(a.counters, slot, val, mx);
+}
+
+// Trusted-window selection of a sweep4 level (matcher.py:263-320, prior
+// window +-r), before the dense sweep.  For every trusted pixel the <= 2r+1
+// candidates [c - r, c + r] & [0, d] are scored directly, centred per pixel
+// (L' = L - muL rounded once; S = sum L' R' - (sum L') (muR(q) - c), the
+// fp64 sum of L' cancelling its rounding), ascending z with a strict >, so
+// ties keep the smallest z.  Non-low pixels get their final outputs here and
+// are marked kWcDone (the sweep skips them); low pixels are marked kWcLow
+// and counted (the sweep computes only their 3x3-summed refinement,
+// matcher.py:196-233); untrusted pixels keep kWcNone.  Tiles the precision
+// guard flagged are left whole to the sweep2 fixup.  One thread per pixel,
+// the right span of one window row in registers.
+template <int B, int DIR, int MAXW, bool F32>
+__global__ void __launch_bounds__(256, 4) prior_select_kernel(const SweepArgs a, const int th) {
+  pdl_wait();
+  constexpr int H2 = B / 2, NRV = B + MAXW - 1;
+  constexpr int TR = 8 + B - 1, TC = 32 + B - 1;   // left tile (replicate-clamped)
+  using LT = typename std::conditional<F32, float, double>::type;
+  __shared__ LT Ls[TR][TC];
+  const int x0 = blockIdx.x * 32, y0 = a.rows.lo + blockIdx.y * 8;
+  const int j = x0 + threadIdx.x, i = y0 + threadIdx.y;
+  const int H = a.H, W = a.W;
+  for (int t = threadIdx.x + 32 * threadIdx.y; t < TR * TC; t += 256) {
+    const int rr = t / TC, cc = t - rr * TC;
+    const int y = clampi(y0 - H2 + rr, 0, H - 1), x = clampi(x0 - H2 + cc, 0, W - 1);
+    if constexpr (F32) Ls[rr][cc] = a.L32[(int64_t)y * a.ld32 + x];
+    else Ls[rr][cc] = a.L[(int64_t)y * a.ld + x];
+  }
+  __syncthreads();
+  int* wc = const_cast<int*>(a.wc);
+  unsigned nlow = 0;
+  int c = kWcNone;
+  if (i < a.rows.hi && i < H && j < W) c = wc[(int64_t)i * a.ldw + j];
+  if (c > kWcLow &&
+      !(a.tile_flags != nullptr && a.tile_flags[(int64_t)(i / th) * a.flags_ld + (j >> 4)] != 0)) {
+    const int lo = max(c - a.radius, 0), hi = min(c + a.radius, a.d);
+    const int nw = hi - lo + 1;   // >= 1: trusted windows meet [0, d] (prior)
+    const float is = a.isL[(int64_t)i * a.lds + j];
+    const float kL = is > 0.f ? is * (1.0f / (float)(B * B)) : __int_as_float(0x7fc00000);
+    const float muf = a.muL[(int64_t)i * a.lds + j];
+    float S[MAXW];
+#pragma unroll
+    for (int zi = 0; zi < MAXW; ++zi) S[zi] = 0.f;
+    double sumL = 0.0;
+    // first staged right column of this pixel's window rows: z = lo + zi
+    // reads column j - H2 + cc - z (middlebury) or j - H2 + cc + z (paper)
+    const int base = DIR > 0 ? (j - H2 - (lo + MAXW - 1)) : (j - H2 + lo);
+    const float* __restrict__ Rp = a.Rp + a.pc + base;
+#pragma unroll 1
+    for (int r = 0; r < B; ++r) {
+      const int y = clampi(i - H2 + r, 0, H - 1);
+      const float* __restrict__ rrow = Rp + (int64_t)y * a.ldp;
+      const LT* lrow = &Ls[threadIdx.y + r][threadIdx.x];
+      float rv[NRV], l[B];
+#pragma unroll
+      for (int e = 0; e < NRV; ++e) rv[e] = __ldg(rrow + e);
+      // L' = L - muL rounded once to fp32 (level 0 is the fp32 input, where
+      // the fp32 subtraction is that rounding; coarser levels via fp64)
+#pragma unroll
+      for (int cc = 0; cc < B; ++cc) {
+        if constexpr (F32) l[cc] = lrow[cc] - muf;
+        else l[cc] = (float)(lrow[cc] - (double)muf);
+      }
+#pragma unroll
+      for (int cc = 0; cc < B; ++cc) {
+        sumL += (double)l[cc];
+#pragma unroll
+        for (int zi = 0; zi < MAXW; ++zi)
+          S[zi] = fmaf(l[cc], rv[DIR > 0 ? cc + MAXW - 1 - zi : cc + zi], S[zi]);
+      }
+    }
+    const float sl = (float)sumL;
+    const float2* __restrict__ Mrow = a.Mp + a.pc + (int64_t)i * a.ldp;
+    float best = -1.f;
+    int bz = lo;
+#pragma unroll
+    for (int zi = 0; zi < MAXW; ++zi) {
+      if (zi < nw) {
+        const int z = lo + zi;
+        const float2 m = Mrow[DIR > 0 ? j - z : j + z];
+        const float cp = fma_sat(fmaf(-sl, m.x, S[zi]) * kL, m.y, 0.5f);
+        if (cp > best) best = cp, bz = z;
+      }
+    }
+    const float cs = 2.f * best - 1.f;   // c = 2 c' - 1
+    const bool low = (double)cs <= a.alpha;
+    const int64_t o = (int64_t)i * a.ldo + j;
+    if (low) {
+      wc[(int64_t)i * a.ldw + j] = kWcLow;
+      nlow = (i >= a.rows.cnt_lo && i < a.rows.cnt_hi) ? 1u : 0u;
+    } else {
+      a.dout[o] = (int16_t)bz;
+      a.cout[o] = cs;
+      a.low[o] = 0;
+      wc[(int64_t)i * a.ldw + j] = kWcDone;
+    }
   }
   const int slot[1] = {kCntRefined};
   const unsigned long long val[1] = {nlow};
@@ -521,6 +633,18 @@ int sweep4_th() {
 
 namespace {
 
+template <int B, int DIR, bool F32>
+cudaError_t launch_prior_select(const SweepArgs& a, int th, dim3 pg, cudaStream_t s) {
+  const dim3 blk(32, 8);
+  switch (a.radius) {
+    case 0:
+    case 1: return launch_pdl(prior_select_kernel<B, DIR, 3, F32>, pg, blk, 0, s, a, th);
+    case 2: return launch_pdl(prior_select_kernel<B, DIR, 5, F32>, pg, blk, 0, s, a, th);
+    case 3: return launch_pdl(prior_select_kernel<B, DIR, 7, F32>, pg, blk, 0, s, a, th);
+    default: return launch_pdl(prior_select_kernel<B, DIR, 15, F32>, pg, blk, 0, s, a, th);
+  }
+}
+
 template <int B, int DIR, int G>
 cudaError_t launch4(const SweepArgs& a, cudaStream_t s) {
   const int th = sweep4_th();
@@ -530,6 +654,12 @@ cudaError_t launch4(const SweepArgs& a, cudaStream_t s) {
   const S4Layout<B, G> lay(th, nw, passes * nw);
   static SmemAttr attr;
   if (cudaError_t e = attr.ensure(sweep4_kernel<B, DIR, G>, lay.bytes); e != cudaSuccess) return e;
+  if (a.wc != nullptr) {   // trusted windows first (prior_select_kernel)
+    dim3 pg((a.W + 31) / 32, (a.rows.hi - a.rows.lo + 7) / 8);
+    cudaError_t e = a.L32 != nullptr ? launch_prior_select<B, DIR, true>(a, th, pg, s)
+                                      : launch_prior_select<B, DIR, false>(a, th, pg, s);
+    if (e != cudaSuccess) return e;
+  }
   // CTA rows on the whole-image grid (row bands bit-identical to whole runs)
   SweepArgs b = a;
   b.rows.lo = (a.rows.lo / th) * th;
@@ -546,7 +676,7 @@ bool sweep4_supported(const SweepArgs& a, bool force) {
   return (force || (int64_t)a.H * a.W >= 400000) && a.mode == kSweepPipeline &&
          a.muL != nullptr && a.isL != nullptr && a.tile_flags != nullptr &&
          (a.block == 5 || a.block == 7 || a.block == 9 || a.block == 11) && a.d >= 1 &&
-         a.d <= 4095;
+         a.d <= 4095 && a.radius <= 7;   // prior_select_kernel: windows of <= 15
 }
 
 int g_group = -1;

@@ -59,13 +59,15 @@ def counts_close(a, b, rel=2e-3):
 
 
 def classify_mismatches(d_gpu, d_ref, left, right, block, d_max, sign="middlebury",
-                        tol=1e-4, return_pixels=False, c_gpu=None, alpha=0.9):
+                        tol=1e-4, return_pixels=False, c_gpu=None, alpha=0.9, c_ref=None):
     """Explain level-0 disparity mismatches.
 
     A mismatch is a *near tie* when the reference's own cost or its clipped
     3x3-averaged cost differs by < ``tol`` between the two disparities, or
-    (with ``c_gpu``) when its final cost lies within ``tol`` of ``alpha`` (an
-    alpha-gate near tie: refine and median run only for C <= alpha).  It is
+    (with ``c_gpu`` / ``c_ref``) when the GPU's or the reference's final cost
+    lies within ``tol`` of ``alpha`` (an alpha-gate near tie: refine and
+    median run only for C <= alpha; the side that kept the pixel unrefined
+    still holds its selection cost, so one of the two maps shows it).  It is
     a *median descendant* when its 5x5 median window holds a near-tie
     mismatch or any alpha-gate near-tie pixel (the gate decides which
     neighbours qualify, matcher.py:345-352).  Returns (n_mismatch, n_near_tie, n_descendant, n_unexplained)
@@ -90,8 +92,10 @@ def classify_mismatches(d_gpu, d_ref, left, right, block, d_max, sign="middlebur
     ties = np.array(ties)
     gate = np.zeros(d_ref.shape, dtype=bool)
     if c_gpu is not None:
-        gate = np.abs(np.asarray(c_gpu, np.float64) - alpha) < tol
-        ties |= gate[bad[:, 0], bad[:, 1]]
+        gate |= np.abs(np.asarray(c_gpu, np.float64) - alpha) < tol
+    if c_ref is not None:
+        gate |= np.abs(np.asarray(c_ref, np.float64) - alpha) < tol
+    ties |= gate[bad[:, 0], bad[:, 1]]
     tie_px = np.concatenate([bad[ties], np.argwhere(gate)])
     desc = 0
     other = []

@@ -71,13 +71,20 @@ def _inputs(name, g):
     return cfg, left, right
 
 
-def _prior_descendants(gpu, cfg, left, right, pixels, ref_d):
-    """How many of ``pixels`` (unexplained level-0 mismatches) the GPU gets
-    right when level 0 reruns from the reference's level-1 maps (C oracle,
-    pinned to the reference)."""
+def _reference_maps(cfg, left, right):
+    """Level-0 (d, c) and level-1 maps of the C oracle (pinned to the
+    reference): the full reference cost map for the alpha-gate check and the
+    level-1 prior for the teacher-forced rerun."""
     from oracle import c_oracle as CO
     _, _, _, maps = CO.run_pipeline(left, right, cfg.d_max, cfg.levels, cfg.block,
                                     radius=cfg.radius, levels_out=True)
+    return maps
+
+
+def _prior_descendants(gpu, cfg, left, right, pixels, ref_d, maps):
+    """How many of ``pixels`` (unexplained level-0 mismatches) the GPU gets
+    right when level 0 reruns from the reference's level-1 maps (C oracle,
+    pinned to the reference)."""
     eng = gpu.CostEngine(left.astype(np.float64), right.astype(np.float64), cfg.block,
                          cfg.d_max)
     d_hat, c_hat = gpu.upsample_prior(maps[1][0], maps[1][1], left.shape)
@@ -108,9 +115,18 @@ def test_full_size_config_matches_reference(gpu, name, path):
     rows = g["cost_rows"] if "cost_rows" in g else slice(None)
     frac_d = float(np.mean(d != ref_d))
     frac, cerr, med = parity_report(d[rows], c[rows], ref_d[rows], g["cost"], 1e-4)
+    c_ref = g["cost"] if "cost_rows" not in g else None
     n, ties, desc, unexplained, other = classify_mismatches(
-        d, ref_d, left, right, cfg.block, cfg.d_max, return_pixels=True, c_gpu=c)
-    prior_desc = _prior_descendants(gpu, cfg, left, right, other, ref_d) if unexplained else 0
+        d, ref_d, left, right, cfg.block, cfg.d_max, return_pixels=True, c_gpu=c, c_ref=c_ref)
+    prior_desc = 0
+    if unexplained:
+        maps = _reference_maps(cfg, left, right)
+        if c_ref is None:   # the golden keeps some cost rows only: the oracle's full map
+            n, ties, desc, unexplained, other = classify_mismatches(
+                d, ref_d, left, right, cfg.block, cfg.d_max, return_pixels=True, c_gpu=c,
+                c_ref=maps[0][1])
+        if unexplained:
+            prior_desc = _prior_descendants(gpu, cfg, left, right, other, ref_d, maps)
     msg = (f"{name}/{path}: {n} disparity mismatches ({frac_d:.5%}: {ties} near ties, {desc} "
            f"median descendants, {prior_desc} level-1 prior descendants, "
            f"{unexplained - prior_desc} other), cost-discrepant {frac:.5%} of the "

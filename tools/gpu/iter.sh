@@ -1,0 +1,13 @@
+# build-measure iteration on one B200: quick timings, ncu per-kernel table
+# of one pipeline run, then the parity suites (-x).  OUT=gpurun_out/$1
+OUT=gpurun_out/${1:-iter}; mkdir -p $OUT
+shift
+CFGS=${CFGS:-"C2 C3"}
+timeout 300 python tools/quick_time.py $CFGS > $OUT/qt.log 2>&1
+M=gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active,sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active,smsp__issue_active.avg.pct_of_peak_sustained_active,l1tex__data_pipe_lsu_wavefronts_mem_shared.sum,l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum
+for c in ${NCU_CFGS:-C3}; do
+  timeout 600 ncu --clock-control none --metrics $M --csv --log-file $OUT/stages_$c.csv python tools/prof_once.py $c > $OUT/stages_$c.log 2>&1
+done
+if [ -z "$NOTEST" ]; then
+timeout 1500 python -m pytest tests -x -q -m gpu -s $TESTARGS > $OUT/gpu.log 2>&1; echo gpu_rc=$? >> $OUT/gpu.log
+fi
