@@ -93,7 +93,8 @@ struct Plan {
   unsigned long long* counters = nullptr;
   float* cR = nullptr;        // right-image offset c of every level (centre sample)
   void* arena = nullptr;
-  cudaGraphExec_t exec = nullptr;
+  cudaGraphExec_t exec = nullptr;         // plain graph
+  cudaGraphExec_t exec_timed = nullptr;   // + the stage event-record nodes
   int launches = 0;
   cudaStream_t stream = nullptr;   // batch slot stream (run_batch)
   // recorded after every use: a call on another stream waits for it before
@@ -319,7 +320,12 @@ void plan_rows(Plan& p, int b0, int b1) {
 }
 
 // Event record that becomes an event-record node under stream capture.
+// Untimed graphs leave them out (each node adds scheduling latency on the
+// critical path of a short pipeline, ~0.1 ms on C2): g_rec_events is false
+// while those are captured.
+thread_local bool g_rec_events = true;
 cudaError_t rec(cudaEvent_t e, cudaStream_t s) {
+  if (!g_rec_events) return cudaSuccess;
   cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
   cudaError_t err = cudaStreamIsCapturing(s, &cs);
   if (err != cudaSuccess) return err;
@@ -452,11 +458,11 @@ int enqueue(mshbm_ctx* ctx, Plan& p, cudaStream_t s, cudaStream_t side = nullptr
     const bool s4 = sweep_uses_sweep4(a);
     CK(rec(ev->sel0, s));
     CK(launch_sweep(a, s, &n));
-    CK(rec(ev->sel1, s));
     if (s4) {   // sweep2 on the tiles sweep4's precision guard left (usually none)
       CK(launch_sweep4_fixup(a, s));
       ++n;
     }
+    CK(rec(ev->sel1, s));
     if (fork && k > 0) {
       // the prefilter of this level's costs (next level's prior) overlaps
       // this level's selective median
@@ -525,13 +531,17 @@ Plan* get_plan(mshbm_ctx* ctx, const PlanKey& key, const mshbm_config& cfg,
 }
 
 // run a plan: graph replay (captured on first use) or direct launches
-// (MSHBM_FLAG_NO_GRAPH).  Both record the plan's stage events.
+// (MSHBM_FLAG_NO_GRAPH).  Direct launches and timed replays
+// (MSHBM_FLAG_TIMING) record the plan's stage events; untimed replays use a
+// graph without them.
 int launch_plan(mshbm_ctx* ctx, Plan& p, cudaStream_t s, int flags) {
   if (flags & MSHBM_FLAG_NO_GRAPH) {
     int st = enqueue(ctx, p, s);
     if (st) return st;
   } else {
-    if (!p.exec) {
+    const bool timed = (flags & MSHBM_FLAG_TIMING) != 0;
+    cudaGraphExec_t& exec = timed ? p.exec_timed : p.exec;
+    if (!exec) {
       cudaStream_t cs;
       CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
       cudaStream_t side, side2;
@@ -546,7 +556,9 @@ int launch_plan(mshbm_ctx* ctx, Plan& p, cudaStream_t s, int flags) {
       // faster with one branch)
       bool s4 = false;
       for (const LevelBuf& l : p.lv) s4 |= l.muL != nullptr;
+      g_rec_events = timed;
       int st = enqueue(ctx, p, cs, side, evs.data(), s4 ? side2 : nullptr);
+      g_rec_events = true;
       cudaError_t ce = cudaStreamEndCapture(cs, &g);
       for (auto& e : evs) cudaEventDestroy(e);
       cudaStreamDestroy(side);
@@ -554,10 +566,10 @@ int launch_plan(mshbm_ctx* ctx, Plan& p, cudaStream_t s, int flags) {
       cudaStreamDestroy(cs);
       if (st) return st;
       CK(ce);
-      CK(cudaGraphInstantiate(&p.exec, g, 0));
+      CK(cudaGraphInstantiate(&exec, g, 0));
       cudaGraphDestroy(g);
     }
-    CK(cudaGraphLaunch(p.exec, s));
+    CK(cudaGraphLaunch(exec, s));
   }
   ctx->launches += p.launches;
   return MSHBM_OK;
@@ -741,6 +753,7 @@ int mshbm_destroy(mshbm_ctx* ctx) {
   cudaStreamSynchronize(ctx->stream);
   for (auto& kv : ctx->plans) {
     if (kv.second->exec) cudaGraphExecDestroy(kv.second->exec);
+    if (kv.second->exec_timed) cudaGraphExecDestroy(kv.second->exec_timed);
     if (kv.second->stream) cudaStreamDestroy(kv.second->stream);
     if (kv.second->done) cudaEventDestroy(kv.second->done);
     destroy_events(kv.second->tev);

@@ -675,7 +675,8 @@ bool sweep4_supported(const SweepArgs& a, bool force) {
   // force (MSHBM_SWEEP4=2) drops the size rule: parity tests on small images
   return (force || (int64_t)a.H * a.W >= 400000) && a.mode == kSweepPipeline &&
          a.muL != nullptr && a.isL != nullptr && a.tile_flags != nullptr &&
-         (a.block == 5 || a.block == 7 || a.block == 9 || a.block == 11) && a.d >= 1 &&
+         (a.block == 5 || a.block == 7 || a.block == 9 || a.block == 11) &&
+         a.d >= 1 &&
          a.d <= 4095 && a.radius <= 7;   // prior_select_kernel: windows of <= 15
 }
 
