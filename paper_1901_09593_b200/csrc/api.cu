@@ -85,6 +85,10 @@ struct Plan {
   PlanKey key{};
   int H = 0, W = 0, K = 0;
   bool user = false;
+  // level 0 kept as an fp64 copy (caller-supplied pyramid, no pyramid, or a
+  // block only the generic fp64 sweep handles); otherwise every level-0
+  // kernel reads the fp32 inputs and the copy is never written
+  bool l0_f64 = true;
   mshbm_config cfg{};
   std::vector<LevelBuf> lv;
   float* in_l = nullptr;
@@ -301,16 +305,17 @@ void plan_rows(Plan& p, int b0, int b1) {
   }
   // Statistics and staging rows: the sweep's CTA grids (sweep2 jobs of <= 30
   // rows, sweep4 tiles of 32) and window halos reach <= 37 rows beyond its
-  // rows; the image rows add the statistics kernel's tile alignment and
-  // window (<= 13), and every level must also hold the rows the next coarser
-  // level's 5-tap downsample reads (2 x its rows +- 2).  Whole-image plans
-  // get whole levels.
+  // rows; the image rows add the statistics kernel's 32-row tile alignment
+  // (its tiles read, and centre on, their first row) and window (<= 5 + 31 +
+  // 5 rows beyond the statistics rows), and every level must also hold the
+  // rows the next coarser level's 5-tap downsample reads (2 x its rows +- 2).
+  // Whole-image plans get whole levels.
   for (int k = K; k >= 0; --k) {
     LevelBuf& l = p.lv[k];
     l.st_lo = std::max(0, l.rows.lo - 40);
     l.st_hi = std::min(l.h, l.rows.hi + 40);
-    l.img_lo = std::max(0, l.rows.lo - 56);
-    l.img_hi = std::min(l.h, l.rows.hi + 56);
+    l.img_lo = std::max(0, l.rows.lo - 88);
+    l.img_hi = std::min(l.h, l.rows.hi + 88);
     if (k < K) {
       const LevelBuf& c = p.lv[k + 1];
       l.img_lo = std::max(0, std::min(l.img_lo, 2 * c.img_lo - 3));
@@ -358,8 +363,9 @@ int enqueue(mshbm_ctx* ctx, Plan& p, cudaStream_t s, cudaStream_t side = nullptr
       // (rows 2 i, 2 i + 1 of every level-1 row i computed)
       const LevelBuf& l0 = p.lv[0];
       const LevelBuf& l1 = p.lv[1];
-      CK(launch_downsample_f32(p.in_l, p.in_r, p.H, p.W, p.ld_in, l1.L, l1.R, l1.ld, l0.L, l0.R,
-                               l0.ld, s, std::min(l1.img_lo, l0.img_lo / 2),
+      CK(launch_downsample_f32(p.in_l, p.in_r, p.H, p.W, p.ld_in, l1.L, l1.R, l1.ld,
+                               p.l0_f64 ? l0.L : nullptr, p.l0_f64 ? l0.R : nullptr, l0.ld, s,
+                               std::min(l1.img_lo, l0.img_lo / 2),
                                std::max(l1.img_hi, (l0.img_hi + 1) / 2)));
     }
     ++n;
@@ -384,10 +390,19 @@ int enqueue(mshbm_ctx* ctx, Plan& p, cudaStream_t s, cudaStream_t side = nullptr
   for (int k = p.K; k >= 0; --k) {
     LevelBuf& l = p.lv[k];
     cudaStream_t t = (fork && k < p.K) ? side : s;
-    CK(launch_stats_f32(l.R, l.h, l.w, l.ld, l.b, cfg.sigma_eps, l.muR, l.isR, l.ld, t,
-                        l.st_lo, l.st_hi));
-    CK(launch_prep_staging(l.R, l.ld, l.muR, l.isR, l.ld, l.h, l.w, l.pc, l.Rp, l.Mp, l.ldp, t,
-                           l.st_lo, l.st_hi, p.cR));
+    // level 0 of a built pyramid reads the fp32 input (its fp64 copy is exact)
+    const bool in32 = k == 0 && !p.l0_f64;
+    if (in32) {
+      CK(launch_stats_f32(p.in_r, l.h, l.w, p.ld_in, l.b, cfg.sigma_eps, l.muR, l.isR, l.ld, t,
+                          l.st_lo, l.st_hi));
+      CK(launch_prep_staging(p.in_r, p.ld_in, l.muR, l.isR, l.ld, l.h, l.w, l.pc, l.Rp, l.Mp,
+                             l.ldp, t, l.st_lo, l.st_hi, p.cR));
+    } else {
+      CK(launch_stats_f32(l.R, l.h, l.w, l.ld, l.b, cfg.sigma_eps, l.muR, l.isR, l.ld, t,
+                          l.st_lo, l.st_hi));
+      CK(launch_prep_staging(l.R, l.ld, l.muR, l.isR, l.ld, l.h, l.w, l.pc, l.Rp, l.Mp, l.ldp, t,
+                             l.st_lo, l.st_hi, p.cR));
+    }
     n += 2;
     if (l.muL) {
       // L statistics + sweep4's precision guard (tile flags), then the job
@@ -395,6 +410,7 @@ int enqueue(mshbm_ctx* ctx, Plan& p, cudaStream_t s, cudaStream_t side = nullptr
       Sweep4Guard g;
       g.L = l.L;
       g.ld = l.ld;
+      if (k == 0 && !p.l0_f64) g.L32 = p.in_l, g.ld32 = p.ld_in;
       g.muL = l.muL;
       g.isL = l.isL;
       g.muR = l.muR;
@@ -410,8 +426,12 @@ int enqueue(mshbm_ctx* ctx, Plan& p, cudaStream_t s, cudaStream_t side = nullptr
       g.flags = l.flags;
       g.flags_ld = l.flags_ld;
       CK(cudaMemsetAsync(l.flags, 0, sizeof(unsigned) * (l.flags_ld * ((l.h + 1) / 2) + 1), t));
-      CK(launch_stats_f32(l.L, l.h, l.w, l.ld, l.b, cfg.sigma_eps, l.muL, l.isL, l.ld, t,
-                          l.st_lo, l.st_hi));
+      if (in32)
+        CK(launch_stats_f32(p.in_l, l.h, l.w, p.ld_in, l.b, cfg.sigma_eps, l.muL, l.isL, l.ld, t,
+                            l.st_lo, l.st_hi));
+      else
+        CK(launch_stats_f32(l.L, l.h, l.w, l.ld, l.b, cfg.sigma_eps, l.muL, l.isL, l.ld, t,
+                            l.st_lo, l.st_hi));
       CK(launch_sweep4_guard(g, l.rows, t));
       CK(launch_fixup_list(l.flags, l.flags_ld, sweep4_th(), l.h, l.w, l.rows, l.b, l.fix_list,
                            l.fix_count, t));
@@ -441,7 +461,7 @@ int enqueue(mshbm_ctx* ctx, Plan& p, cudaStream_t s, cudaStream_t side = nullptr
     CK(rec(ev->up1, s));
     SweepArgs a{};
     a.L = l.L; a.R = l.R; a.ld = l.ld;
-    if (k == 0 && !p.user) a.L32 = p.in_l, a.ld32 = p.ld_in;
+    if (k == 0 && !p.l0_f64) a.L32 = p.in_l, a.R32 = p.in_r, a.ld32 = p.ld_in;
     a.muR = l.muR; a.isR = l.isR; a.lds = l.ld;
     a.muL = l.muL; a.isL = l.isL;
     a.tile_flags = l.flags; a.flags_ld = l.flags_ld;
@@ -509,6 +529,7 @@ Plan* get_plan(mshbm_ctx* ctx, const PlanKey& key, const mshbm_config& cfg,
     l.ld = round_up(l.w, 32);
     p->lv.push_back(l);
   }
+  p->l0_f64 = p->user || p->K == 0 || p->lv[0].b > 11;
   *st = build_plan(ctx, *p);
   if (*st != MSHBM_OK) {
     delete p;

@@ -23,8 +23,17 @@ struct SweepArgs {
   const double* L;      // level images, float64, row stride ld
   const double* R;
   int64_t ld;
-  const float* L32;     // level 0 of a built pyramid: the fp32 input (exact), stride ld32
+  // level 0 of a built pyramid: the fp32 inputs (the level's values exactly;
+  // its fp64 copy is then not written), row stride ld32; nullptr otherwise
+  const float* L32;
+  const float* R32;
   int64_t ld32;
+  __host__ __device__ double Lv(int64_t y, int64_t x) const {
+    return L32 ? (double)L32[y * ld32 + x] : L[y * ld + x];
+  }
+  __host__ __device__ double Rv(int64_t y, int64_t x) const {
+    return R32 ? (double)R32[y * ld32 + x] : R[y * ld + x];
+  }
   const float* muR;     // box mean of R (fp32)
   const float* isR;     // 1/sigma_R, 0 where degenerate (fp32)
   int64_t lds;
@@ -91,6 +100,11 @@ cudaError_t launch_prep_staging(const double* R, int64_t ld, const float* muR, c
                                 int64_t lds, int h, int w, int pc, float* Rp, float2* Mp,
                                 int64_t ldp, cudaStream_t s, int y0 = 0, int y1 = -1,
                                 const float* cR = nullptr);
+// the same from the fp32 level-0 input (identical values: fl32(R - c))
+cudaError_t launch_prep_staging(const float* R, int64_t ld, const float* muR, const float* isR,
+                                int64_t lds, int h, int w, int pc, float* Rp, float2* Mp,
+                                int64_t ldp, cudaStream_t s, int y0 = 0, int y1 = -1,
+                                const float* cR = nullptr);
 // *out = level-0 right sample at the image centre (fp32 input or fp64 level)
 cudaError_t launch_centre_sample(const float* in32, const double* in64, int64_t ld, int h,
                                  int w, float* out, cudaStream_t s);
@@ -131,6 +145,8 @@ constexpr float kSweep4RiskMax = 200.f;
 struct Sweep4Guard {
   const double* L = nullptr;    // level image (cL samples), stride ld
   int64_t ld = 0;
+  const float* L32 = nullptr;   // or the fp32 level-0 input, stride ld32
+  int64_t ld32 = 0;
   const float* muL = nullptr;   // fp32 statistics, stride lds
   const float* isL = nullptr;
   const float* muR = nullptr;
@@ -151,6 +167,10 @@ cudaError_t launch_stats_f32(const double* img, int h, int w, int64_t ld,
                              int b, double sigma_eps, float* mu, float* is,
                              int64_t lds, cudaStream_t s,
                              int y0 = 0, int y1 = -1);   // rows [y0, y1) (tile-aligned)
+// the same from the fp32 level-0 input (b <= 11)
+cudaError_t launch_stats_f32(const float* img, int h, int w, int64_t ld, int b, double sigma_eps,
+                             float* mu, float* is, int64_t lds, cudaStream_t s, int y0 = 0,
+                             int y1 = -1);
 // fp64 mean / sigma maps (dense) for the CostEngine API
 cudaError_t launch_stats_f64(const double* img, int h, int w, int64_t ld,
                              int b, double* mu, double* sigma, cudaStream_t s);

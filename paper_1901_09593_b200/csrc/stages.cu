@@ -451,66 +451,81 @@ __global__ void combine_refine_kernel(const double* din, const double* cin,
 // ---- shared-memory tiled versions of the per-pixel stage kernels --------
 constexpr int kTX = 32, kTY = 8;
 
-// K2 for b <= 15: window tile in smem; mean via separable row sums,
-// centred sigma from the tile (fp64), 1/sigma or 0 (degenerate) in fp32.
-template <int B>
-__global__ void __launch_bounds__(kTX * kTY) stats_tiled_kernel(const double* img, int h, int w,
-                                                              int64_t ld, double sigma_eps,
-                                                              float* mu32, float* is32,
-                                                              int64_t lds, int y_base) {
-  // Separable box sums of x' and x'^2 (x' = x - c, c the tile's first sample,
-  // fp64); windows whose shifted variance cancels to < 1e-9 of E[x'^2]
-  // (flat or near-flat) recompute it centred from the tile, so flat blocks
-  // keep sigma == 0 exactly (zncc.py:182-189 degeneracy rule).
-  constexpr int H2 = B / 2, TR = kTY + B - 1, TC = kTX + B - 1;
+// K2, pipeline form: 32 x 32 outputs per CTA (tile reads 1.3x the outputs at
+// b = 9 instead of the 8-row tile's 2.5x), sliding box sums in both passes
+// (fp64, centred by the tile's first sample as above), input fp64 levels or
+// the fp32 level-0 input.
+template <int B, typename TIn>
+__global__ void __launch_bounds__(256) stats32_kernel(const TIn* img, int h, int w, int64_t ld,
+                                                      double sigma_eps, float* mu32, float* is32,
+                                                      int64_t lds, int y_base) {
+  pdl_wait();
+  constexpr int H2 = B / 2, TR = 32 + B - 1, TC = 32 + B - 1;
   __shared__ double T[TR][TC];
-  __shared__ double H1[TR][kTX], H2s[TR][kTX];
-  // tiles stay on the whole-image grid (y_base is a multiple of kTY), so the
-  // per-tile shift c, and with it every output bit, matches whole-level runs
-  const int x0 = blockIdx.x * kTX, y0 = y_base + blockIdx.y * kTY;
-  const int tid = threadIdx.y * kTX + threadIdx.x;
-  const double c = img[(int64_t)clampi(y0, 0, h - 1) * ld + clampi(x0, 0, w - 1)];
+  __shared__ double H1[TR][33], H2s[TR][33];
+  const int x0 = blockIdx.x * 32, y0 = y_base + blockIdx.y * 32;
+  const int tid = threadIdx.y * 32 + threadIdx.x;
+  const double c = (double)img[(int64_t)clampi(y0, 0, h - 1) * ld + clampi(x0, 0, w - 1)];
 #pragma unroll 4
-  for (int t = tid; t < TR * TC; t += kTX * kTY) {
+  for (int t = tid; t < TR * TC; t += 256) {
     const int r = t / TC, cc = t - r * TC;
-    T[r][cc] = img[(int64_t)clampi(y0 - H2 + r, 0, h - 1) * ld + clampi(x0 - H2 + cc, 0, w - 1)] - c;
+    T[r][cc] = (double)img[(int64_t)clampi(y0 - H2 + r, 0, h - 1) * ld + clampi(x0 - H2 + cc, 0, w - 1)] - c;
   }
   __syncthreads();
-  for (int t = tid; t < TR * kTX; t += kTX * kTY) {
-    const int r = t / kTX, cc = t - r * kTX;
+  // horizontal: each item = 4 consecutive window sums of one tile row
+  for (int it = tid; it < TR * 8; it += 256) {
+    const int r = it >> 3, c0 = (it & 7) * 4;
     double s1 = 0.0, s2 = 0.0;
 #pragma unroll
     for (int k = 0; k < B; ++k) {
-      const double v = T[r][cc + k];
+      const double v = T[r][c0 + k];
       s1 += v;
       s2 = fma(v, v, s2);
     }
-    H1[r][cc] = s1;
-    H2s[r][cc] = s2;
+    H1[r][c0] = s1;
+    H2s[r][c0] = s2;
+#pragma unroll
+    for (int e = 1; e < 4; ++e) {
+      const double vi = T[r][c0 + e + B - 1], vo = T[r][c0 + e - 1];
+      s1 += vi - vo;
+      s2 += fma(vi, vi, -vo * vo);
+      H1[r][c0 + e] = s1;
+      H2s[r][c0 + e] = s2;
+    }
   }
   __syncthreads();
-  const int x = x0 + threadIdx.x, y = y0 + threadIdx.y;
-  if (x >= w || y >= h) return;
+  // vertical: thread (x, ty) slides down rows 4 ty .. 4 ty + 3
+  const int tx = threadIdx.x, r0 = threadIdx.y * 4;
   double s1 = 0.0, s2 = 0.0;
 #pragma unroll
-  for (int k = 0; k < B; ++k) s1 += H1[threadIdx.y + k][threadIdx.x], s2 += H2s[threadIdx.y + k][threadIdx.x];
+  for (int k = 0; k < B; ++k) s1 += H1[r0 + k][tx], s2 += H2s[r0 + k][tx];
+  const int x = x0 + tx;
   constexpr double inv = 1.0 / (double)(B * B);
-  const double m1 = s1 * inv, m2 = s2 * inv;
-  double var = m2 - m1 * m1;
-  if (var <= 1e-9 * m2) {
-    double ss = 0.0;
 #pragma unroll
-    for (int r = 0; r < B; ++r)
+  for (int e = 0; e < 4; ++e) {
+    if (e > 0) {
+      s1 += H1[r0 + e + B - 1][tx] - H1[r0 + e - 1][tx];
+      s2 += H2s[r0 + e + B - 1][tx] - H2s[r0 + e - 1][tx];
+    }
+    const int y = y0 + r0 + e;
+    if (x < w && y < h) {
+      const double m1 = s1 * inv, m2 = s2 * inv;
+      double var = m2 - m1 * m1;
+      if (var <= 1e-9 * m2) {   // flat or near-flat: exact centred recompute
+        double ss = 0.0;
+        for (int r = 0; r < B; ++r)
 #pragma unroll
-      for (int cc = 0; cc < B; ++cc) {
-        const double dv = T[threadIdx.y + r][threadIdx.x + cc] - m1;
-        ss = fma(dv, dv, ss);
+          for (int cc = 0; cc < B; ++cc) {
+            const double dv = T[r0 + e + r][tx + cc] - m1;
+            ss = fma(dv, dv, ss);
+          }
+        var = ss * inv;
       }
-    var = ss * inv;
+      const double sigma = sqrt(fmax(var, 0.0));
+      mu32[(int64_t)y * lds + x] = (float)(m1 + c);
+      is32[(int64_t)y * lds + x] = sigma >= sigma_eps ? (float)(1.0 / sigma) : 0.f;
+    }
   }
-  const double sigma = sqrt(fmax(var, 0.0));
-  mu32[(int64_t)y * lds + x] = (float)(m1 + c);
-  is32[(int64_t)y * lds + x] = sigma >= sigma_eps ? (float)(1.0 / sigma) : 0.f;
 }
 
 // ---- sweep4 precision guard (kernels.h Sweep4Guard) -----------------------
@@ -537,8 +552,8 @@ __global__ void __launch_bounds__(128) guard_col_kernel(const Sweep4Guard g, int
 __global__ void __launch_bounds__(32) guard_tile_kernel(const Sweep4Guard g, int ty0) {
   const int tx = blockIdx.x, ty = ty0 + blockIdx.y, lane = threadIdx.x;
   const int x0 = tx * 16, y0 = ty * g.tile_h;
-  const double cLd = g.L[(int64_t)clampi(y0 + g.tile_h / 2, 0, g.h - 1) * g.ld +
-                         clampi(x0 + 8, 0, g.w - 1)];
+  const int64_t cy = clampi(y0 + g.tile_h / 2, 0, g.h - 1), cx = clampi(x0 + 8, 0, g.w - 1);
+  const double cLd = g.L32 ? (double)g.L32[cy * g.ld32 + cx] : g.L[cy * g.ld + cx];
   const float cL = (float)cLd;
   float aL = 0.f, aR = 0.f;
   const int ylo = max(y0 - 1, 0), yhi = min(y0 + g.tile_h, g.h - 1);
@@ -666,13 +681,32 @@ __device__ constexpr unsigned char kMedNet[2 * kMedNetLen] = {0,1,2,3,4,5,6,7,8,
 // selective median (pipeline) with the 5x5 neighbourhood staged in smem
 constexpr int kMY = 32;   // rows per median block (4 per thread)
 
+__device__ __forceinline__ unsigned min_s16x2(unsigned a, unsigned b) {
+  unsigned r;
+  asm("min.s16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+  return r;
+}
+__device__ __forceinline__ unsigned max_s16x2(unsigned a, unsigned b) {
+  unsigned r;
+  asm("max.s16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+  return r;
+}
+
+// selective_median (matcher.py:323-359) on a 32 x kMY tile (+2 halo): the
+// alpha gate is applied once per tile element (Qs = disparity where C > alpha,
+// else the +inf sentinel 0x7FFF, int16), low pixels (C <= alpha) go to a
+// block-local work list, and each thread sorts the 24 neighbour slots of TWO
+// listed pixels at once: one pixel per 16-bit half, the 132-comparator
+// network (kMedNet) as packed VIMNMX.S16x2, then the lower median (n-1)/2 of
+// each half's n qualifying values.
 __global__ void __launch_bounds__(kTX * kTY) median_tiled_kernel(
     const int16_t* d, const float* c, const uint8_t* low, int64_t ld, int h, int w,
     double alpha, int16_t* out, unsigned long long* counters, RowBand band) {
   pdl_wait();
   constexpr int TR = kMY + 4, TC = kTX + 4;
-  __shared__ float Cs[TR][TC];
-  __shared__ int16_t Ds[TR][TC];
+  constexpr short kInf = 0x7FFF;
+  __shared__ short Qs[TR][TC];
+  __shared__ short Ds[TR][TC];
   __shared__ uint8_t Lw[TR][TC];
   const int x0 = blockIdx.x * kTX, y0 = band.lo + blockIdx.y * kMY;
   const int tid = threadIdx.y * kTX + threadIdx.x;
@@ -702,9 +736,9 @@ __global__ void __launch_bounds__(kTX * kTY) median_tiled_kernel(
       const int t = tid + kTX * kTY * k;
       if (t < TR * TC) {
         const int a = t / TC, b = t - a * TC;
-        Cs[a][b] = cv[k];
+        Qs[a][b] = (double)cv[k] > alpha ? dv[k] : kInf;
         Ds[a][b] = dv[k];
-        Lw[a][b] = lv[k];
+        Lw[a][b] = lv[k] | ((double)cv[k] <= alpha ? 2 : 0);   // bit 1: C <= alpha
       }
     }
   }
@@ -724,55 +758,61 @@ __global__ void __launch_bounds__(kTX * kTY) median_tiled_kernel(
 #pragma unroll
       for (int di = -1; di <= 1; ++di)
 #pragma unroll
-        for (int dj = -1; dj <= 1; ++dj) needed |= Lw[ty + di][tx + dj] != 0;
+        for (int dj = -1; dj <= 1; ++dj) needed |= (Lw[ty + di][tx + dj] & 1) != 0;
       nneeded += (needed && i >= band.cnt_lo && i < band.cnt_hi) ? 1u : 0u;
-      // low-confidence pixels go to a block-local work list; the others
-      // keep their disparity.  The sorting network then runs only for
-      // listed pixels, packed densely into warps.
-      if ((double)Cs[ty][tx] <= alpha) list[atomicAdd(&nlist, 1)] = (short)(py * kTX + threadIdx.x);
+      // low-confidence pixels go to the work list; the others keep their
+      // disparity
+      if (Lw[ty][tx] & 2) list[atomicAdd(&nlist, 1)] = (short)(py * kTX + threadIdx.x);
       else out[(int64_t)i * ld + j] = Ds[ty][tx];
     }
   }
   __syncthreads();
   unsigned nchanged = 0;
   const int n_items = nlist;
-  for (int k = tid; k < n_items; k += kTX * kTY) {
-    const int p = list[k];
-    const int py = p / kTX, px = p - py * kTX;
-    const int ty = py + 2, tx = px + 2;
-    const int16_t d0 = Ds[ty][tx];
-    int16_t res = d0;
-    // the 24 neighbour slots (centre excluded), +inf sentinels for the
-    // non-qualifying ones, sorted by a fixed 132-comparator network (Batcher's
-    // odd-even merge sort for 32 inputs restricted to 24; kMedNet), then the
-    // lower median (n-1)/2
-    int v[24];
-    int n = 0;
+  for (int k = 2 * tid; k < n_items; k += 2 * kTX * kTY) {
+    const bool two = k + 1 < n_items;
+    const int pa = list[k], pb = two ? list[k + 1] : pa;
+    const int tya = pa / kTX + 2, txa = pa % kTX + 2;
+    const int tyb = pb / kTX + 2, txb = pb % kTX + 2;
+    unsigned v[24];
+    int na = 0, nb = 0;
 #pragma unroll
     for (int t = 0; t < 24; ++t) {
       const int u = t < 12 ? t : t + 1;          // skip the centre (slot 12)
       const int di = u / 5 - 2, dj = u % 5 - 2;
-      const bool q = (double)Cs[ty + di][tx + dj] > alpha;
-      v[t] = q ? (int)Ds[ty + di][tx + dj] : 0x7fffffff;
-      n += q;
+      const short qa = Qs[tya + di][txa + dj], qb = Qs[tyb + di][txb + dj];
+      na += qa != kInf;
+      nb += qb != kInf;
+      v[t] = (unsigned)(unsigned short)qa | ((unsigned)(unsigned short)qb << 16);
     }
-    if (n > 0) {
 #pragma unroll
-      for (int c = 0; c < kMedNetLen; ++c) {
-        const int i0 = kMedNet[2 * c], i1 = kMedNet[2 * c + 1];
-        const int x = v[i0], y = v[i1];
-        v[i0] = min(x, y);
-        v[i1] = max(x, y);
-      }
-      const int m = (n - 1) >> 1;
-      int pick = v[0];
-#pragma unroll
-      for (int t = 1; t < 24; ++t) pick = (m == t) ? v[t] : pick;
-      res = (int16_t)pick;
+    for (int cc = 0; cc < kMedNetLen; ++cc) {
+      const int i0 = kMedNet[2 * cc], i1 = kMedNet[2 * cc + 1];
+      const unsigned x = v[i0], y = v[i1];
+      v[i0] = min_s16x2(x, y);
+      v[i1] = max_s16x2(x, y);
     }
-    const int gi = y0 + py, gj = x0 + px;
-    out[(int64_t)gi * ld + gj] = res;
-    nchanged += (res != d0 && gi >= band.cnt_lo && gi < band.cnt_hi) ? 1u : 0u;
+    const int ma = (na - 1) >> 1, mb = (nb - 1) >> 1;
+    unsigned sa = v[0], sb = v[0];
+#pragma unroll
+    for (int t = 1; t < 24; ++t) {
+      sa = (ma == t) ? v[t] : sa;
+      sb = (mb == t) ? v[t] : sb;
+    }
+    {
+      const int16_t d0 = Ds[tya][txa];
+      const int16_t res = na > 0 ? (int16_t)(sa & 0xffffu) : d0;
+      const int gi = y0 + tya - 2, gj = x0 + txa - 2;
+      out[(int64_t)gi * ld + gj] = res;
+      nchanged += (res != d0 && gi >= band.cnt_lo && gi < band.cnt_hi) ? 1u : 0u;
+    }
+    if (two) {
+      const int16_t d0 = Ds[tyb][txb];
+      const int16_t res = nb > 0 ? (int16_t)(sb >> 16) : d0;
+      const int gi = y0 + tyb - 2, gj = x0 + txb - 2;
+      out[(int64_t)gi * ld + gj] = res;
+      nchanged += (res != d0 && gi >= band.cnt_lo && gi < band.cnt_hi) ? 1u : 0u;
+    }
   }
   const int slot[2] = {kCntMedianReplaced, kCntNeeded};
   const unsigned long long val[2] = {nchanged, nneeded};
@@ -781,27 +821,41 @@ __global__ void __launch_bounds__(kTX * kTY) median_tiled_kernel(
 }
 
 // ------------------------------------------------------------------ staging
-__global__ void prep_staging_kernel(const double* R, int64_t ld, const float* muR,
-                                    const float* isR, int64_t lds, int h, int w, int pc,
-                                    float* Rp, float2* Mp, int64_t ldp, int y0, int y1,
-                                    const float* cR) {
-  const int xp = blockIdx.x * blockDim.x + threadIdx.x;   // padded column
+template <typename TIn>
+__global__ void __launch_bounds__(256) prep_staging_kernel(const TIn* R, int64_t ld,
+                                                           const float* muR, const float* isR,
+                                                           int64_t lds, int h, int w, int pc,
+                                                           float* Rp, float2* Mp, int64_t ldp,
+                                                           int y0, int y1, const float* cR) {
+  pdl_wait();
+  // 4 consecutive padded columns per thread (ldp and pc are multiples of 4:
+  // one float4 and two float4 stores)
+  const int xp0 = 4 * (blockIdx.x * blockDim.x + threadIdx.x);
   const int y = y0 + blockIdx.y * blockDim.y + threadIdx.y;
-  if (y >= h || y >= y1 || xp >= w + 2 * pc) return;
+  if (y >= h || y >= y1 || xp0 >= w + 2 * pc) return;
   // the level's right offset: the pipeline's constant (valid in any row
   // band), else (stage API, whole level) the box mean at the image centre
   const float c = cR ? *cR : muR[(int64_t)(h / 2) * lds + w / 2];
-  const int x = xp - pc;
-  const int xc = clampi(x, 0, w - 1);
-  Rp[(int64_t)y * ldp + xp] = (float)(R[(int64_t)y * ld + xc] - (double)c);
   const float qnan = __int_as_float(0x7fc00000);
-  float2 m = make_float2(0.f, qnan);
-  if (x >= 0 && x < w) {
-    const float is = isR[(int64_t)y * lds + x];
-    // 0.5/sigma_R: the sweep computes the half-range cost c/2 + 1/2
-    m = make_float2(muR[(int64_t)y * lds + x] - c, is > 0.f ? 0.5f * is : qnan);
+  float r4[4];
+  float2 m4[4];
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const int x = xp0 + e - pc;
+    const int xc = clampi(x, 0, w - 1);
+    // fl32(R - c): for the fp32 level-0 input the fp32 subtraction is that rounding
+    r4[e] = (float)((double)R[(int64_t)y * ld + xc] - (double)c);
+    m4[e] = make_float2(0.f, qnan);
+    if (x >= 0 && x < w) {
+      const float is = isR[(int64_t)y * lds + x];
+      // 0.5/sigma_R: the sweep computes the half-range cost c/2 + 1/2
+      m4[e] = make_float2(muR[(int64_t)y * lds + x] - c, is > 0.f ? 0.5f * is : qnan);
+    }
   }
-  Mp[(int64_t)y * ldp + xp] = m;
+  const int64_t o = (int64_t)y * ldp + xp0;
+  *reinterpret_cast<float4*>(Rp + o) = make_float4(r4[0], r4[1], r4[2], r4[3]);
+  reinterpret_cast<float4*>(Mp + o)[0] = make_float4(m4[0].x, m4[0].y, m4[1].x, m4[1].y);
+  reinterpret_cast<float4*>(Mp + o)[1] = make_float4(m4[2].x, m4[2].y, m4[3].x, m4[3].y);
 }
 
 // ------------------------------------------------------------------ evaluate
@@ -864,15 +918,25 @@ cudaError_t launch_evaluate(const double* d, const double* gt, const uint8_t* gt
   return cudaGetLastError();
 }
 
-cudaError_t launch_prep_staging(const double* R, int64_t ld, const float* muR, const float* isR,
-                                int64_t lds, int h, int w, int pc, float* Rp, float2* Mp,
-                                int64_t ldp, cudaStream_t s, int y0, int y1, const float* cR) {
+template <typename TIn>
+cudaError_t launch_prep_staging_t(const TIn* R, int64_t ld, const float* muR, const float* isR,
+                                  int64_t lds, int h, int w, int pc, float* Rp, float2* Mp,
+                                  int64_t ldp, cudaStream_t s, int y0, int y1, const float* cR) {
   if (y1 < 0 || y1 > h) y1 = h;
   if (y1 <= y0) return cudaSuccess;
   dim3 blk(64, 4);
-  prep_staging_kernel<<<grid2d(w + 2 * pc, y1 - y0, blk), blk, 0, s>>>(
-      R, ld, muR, isR, lds, h, w, pc, Rp, Mp, ldp, y0, y1, cR);
-  return cudaGetLastError();
+  return launch_pdl(prep_staging_kernel<TIn>, grid2d((w + 2 * pc + 3) / 4, y1 - y0, blk), blk, 0,
+                    s, R, ld, muR, isR, lds, h, w, pc, Rp, Mp, ldp, y0, y1, cR);
+}
+cudaError_t launch_prep_staging(const double* R, int64_t ld, const float* muR, const float* isR,
+                                int64_t lds, int h, int w, int pc, float* Rp, float2* Mp,
+                                int64_t ldp, cudaStream_t s, int y0, int y1, const float* cR) {
+  return launch_prep_staging_t(R, ld, muR, isR, lds, h, w, pc, Rp, Mp, ldp, s, y0, y1, cR);
+}
+cudaError_t launch_prep_staging(const float* R, int64_t ld, const float* muR, const float* isR,
+                                int64_t lds, int h, int w, int pc, float* Rp, float2* Mp,
+                                int64_t ldp, cudaStream_t s, int y0, int y1, const float* cR) {
+  return launch_prep_staging_t(R, ld, muR, isR, lds, h, w, pc, Rp, Mp, ldp, s, y0, y1, cR);
 }
 
 // The pipeline's right-image offset c (every level): the level-0 right
@@ -920,8 +984,38 @@ cudaError_t launch_downsample_f32(const float* in0, const float* in1, int h, int
   if (i1 < 0 || i1 > oh) i1 = oh;
   if (i1 <= i0) return cudaSuccess;
   dim3 blk(32, 8);
+  if (copy0 == nullptr)   // level 0 stays fp32 (its consumers read the input)
+    return launch_pdl(downsample_kernel<float, false>, grid2d(ow, i1 - i0, blk, 2), blk, 0, s,
+                      in0, in1, h, w, ld_in, out0, out1, ld_out, oh, ow, copy0, copy1, ld_copy,
+                      i0, i1, 2);
   return launch_pdl(downsample_kernel<float, true>, grid2d(ow, i1 - i0, blk, 2), blk, 0, s, in0,
                     in1, h, w, ld_in, out0, out1, ld_out, oh, ow, copy0, copy1, ld_copy, i0, i1, 2);
+}
+
+template <typename TIn>
+cudaError_t launch_stats32(const TIn* img, int h, int w, int64_t ld, int b, double sigma_eps,
+                           float* mu, float* is, int64_t lds, cudaStream_t s, int y0, int y1) {
+  const int yb = (y0 / 32) * 32;   // whole-image tile grid
+  const dim3 blk(32, 8), gr((w + 31) / 32, (y1 - yb + 31) / 32);
+  auto go = [&](auto kern) {
+    return launch_pdl(kern, gr, blk, 0, s, img, h, w, ld, sigma_eps, mu, is, lds, yb);
+  };
+  switch (b) {
+    case 3: return go(stats32_kernel<3, TIn>);
+    case 5: return go(stats32_kernel<5, TIn>);
+    case 7: return go(stats32_kernel<7, TIn>);
+    case 9: return go(stats32_kernel<9, TIn>);
+    case 11: return go(stats32_kernel<11, TIn>);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+cudaError_t launch_stats_f32(const float* img, int h, int w, int64_t ld, int b, double sigma_eps,
+                             float* mu, float* is, int64_t lds, cudaStream_t s, int y0, int y1) {
+  if (y1 < 0 || y1 > h) y1 = h;
+  if (y1 <= y0) return cudaSuccess;
+  if (b <= 11) return launch_stats32(img, h, w, ld, b, sigma_eps, mu, is, lds, s, y0, y1);
+  return cudaErrorInvalidValue;   // fp32 input: level 0 of sweep4 levels (b <= 11)
 }
 
 cudaError_t launch_stats_f32(const double* img, int h, int w, int64_t ld,
@@ -929,17 +1023,10 @@ cudaError_t launch_stats_f32(const double* img, int h, int w, int64_t ld,
                              int64_t lds, cudaStream_t s, int y0, int y1) {
   if (y1 < 0 || y1 > h) y1 = h;
   if (y1 <= y0) return cudaSuccess;
+  if (b <= 11) return launch_stats32(img, h, w, ld, b, sigma_eps, mu, is, lds, s, y0, y1);
   dim3 blk(32, 8);
   const int yb = (y0 / kTY) * kTY;   // whole-image tile grid
   const dim3 gr = grid2d(w, y1 - yb, blk);
-  switch (b) {
-    case 3: stats_tiled_kernel<3><<<gr, blk, 0, s>>>(img, h, w, ld, sigma_eps, mu, is, lds, yb); return cudaGetLastError();
-    case 5: stats_tiled_kernel<5><<<gr, blk, 0, s>>>(img, h, w, ld, sigma_eps, mu, is, lds, yb); return cudaGetLastError();
-    case 7: stats_tiled_kernel<7><<<gr, blk, 0, s>>>(img, h, w, ld, sigma_eps, mu, is, lds, yb); return cudaGetLastError();
-    case 9: stats_tiled_kernel<9><<<gr, blk, 0, s>>>(img, h, w, ld, sigma_eps, mu, is, lds, yb); return cudaGetLastError();
-    case 11: stats_tiled_kernel<11><<<gr, blk, 0, s>>>(img, h, w, ld, sigma_eps, mu, is, lds, yb); return cudaGetLastError();
-    default: break;
-  }
   stats_kernel<false><<<gr, blk, 0, s>>>(img, h, w, ld, b, sigma_eps, mu, is, nullptr, nullptr,
                                           lds, yb);
   return cudaGetLastError();

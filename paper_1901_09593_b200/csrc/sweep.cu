@@ -111,8 +111,7 @@ sweep_kernel(const SweepArgs a) {
   const float qnan = __int_as_float(0x7fc00000);
 
   // per-CTA constant offset of the right image (tile-centre sample)
-  const double cR = a.R[(int64_t)clampi(y0 + NR / 2 - 1, 0, H - 1) * a.ld +
-                        clampi(x0 + 15, 0, W - 1)];
+  const double cR = a.Rv(clampi(y0 + NR / 2 - 1, 0, H - 1), clampi(x0 + 15, 0, W - 1));
   const float cRf = (float)cR;
 
   // ---- staging: global -> registers (prefetch) -> shared (double buffer)
@@ -127,7 +126,7 @@ sweep_kernel(const SweepArgs a) {
         const int rr = t / RW, e = t - rr * RW;
         const int gi = clampi(y0 - 1 - H2 + rr, 0, H - 1);
         const int gc = clampi(s0 + e, 0, W - 1);
-        pr[k] = a.R[(int64_t)gi * a.ld + gc];
+        pr[k] = a.Rv(gi, gc);
       }
     }
     const int q0 = DIR > 0 ? (x0 - 1 - z0 - (ZC - 1)) : (x0 - 1 + z0);
@@ -176,8 +175,7 @@ sweep_kernel(const SweepArgs a) {
   LtT& Ls = *reinterpret_cast<LtT*>(Hs);
   for (int t = threadIdx.x; t < RR * LC; t += NT) {
     const int rr = t / LC, e = t - rr * LC;
-    Ls[rr][e] = a.L[(int64_t)clampi(y0 - 1 - H2 + rr, 0, H - 1) * a.ld +
-                    clampi(x0 - 1 - H2 + e, 0, W - 1)];
+    Ls[rr][e] = a.Lv(clampi(y0 - 1 - H2 + rr, 0, H - 1), clampi(x0 - 1 - H2 + e, 0, W - 1));
   }
   __syncthreads();
 
@@ -311,13 +309,12 @@ sweep_generic(const SweepArgs a) {
   double s = 0.0;
   for (int r = 0; r < B; ++r)
     for (int c = 0; c < B; ++c)
-      s += a.L[(int64_t)clampi(ic + r - H2, 0, H - 1) * a.ld + clampi(jc + c - H2, 0, W - 1)];
+      s += a.Lv(clampi(ic + r - H2, 0, H - 1), clampi(jc + c - H2, 0, W - 1));
   const double mu = s / (double)(B * B);
   double ss = 0.0;
   for (int r = 0; r < B; ++r)
     for (int c = 0; c < B; ++c) {
-      const double dv = a.L[(int64_t)clampi(ic + r - H2, 0, H - 1) * a.ld +
-                            clampi(jc + c - H2, 0, W - 1)] - mu;
+      const double dv = a.Lv(clampi(ic + r - H2, 0, H - 1), clampi(jc + c - H2, 0, W - 1)) - mu;
       ss += dv * dv;
     }
   const double sigma = sqrt(ss / (double)(B * B));
@@ -345,10 +342,10 @@ sweep_generic(const SweepArgs a) {
         const double muR = (double)a.muR[so];
         double acc = 0.0;
         for (int r = 0; r < B; ++r) {
-          const int64_t ro = (int64_t)clampi(ic + r - H2, 0, H - 1) * a.ld;
+          const int yr = clampi(ic + r - H2, 0, H - 1);
           for (int c = 0; c < B; ++c)
-            acc += (a.L[ro + clampi(jc + c - H2, 0, W - 1)] - mu) *
-                   (a.R[ro + clampi(q + c - H2, 0, W - 1)] - muR);
+            acc += (a.Lv(yr, clampi(jc + c - H2, 0, W - 1)) - mu) *
+                   (a.Rv(yr, clampi(q + c - H2, 0, W - 1)) - muR);
         }
         double v = acc * kL * (double)is;
         rho = (float)fmin(fmax(v, -1.0), 1.0);

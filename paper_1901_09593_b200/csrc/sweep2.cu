@@ -237,8 +237,7 @@ __device__ __forceinline__ void sweep2_body(const SweepArgs& a, const int bx, co
     for (int k = 0; k < NL; ++k) {
       const int t = threadIdx.x + NT * k;
       const int rr = t / LC, e = t - rr * LC;
-      v[k] = t < RR * LC ? a.L[(int64_t)clampi(y0 - 1 - H2 + rr, 0, H - 1) * a.ld +
-                              clampi(x0 - 1 - H2 + e, 0, W - 1)]
+      v[k] = t < RR * LC ? a.Lv(clampi(y0 - 1 - H2 + rr, 0, H - 1), clampi(x0 - 1 - H2 + e, 0, W - 1))
                          : 0.0;
     }
 #pragma unroll

@@ -262,11 +262,11 @@ __global__ void __launch_bounds__(kNWMax * 32, 2) sweep4_kernel(const SweepArgs 
   for (int t = tid; t < nslot * th * kTW; t += nt) sK[t] = 0u, rK[t] = 0u;
   // centring constant: the L sample at the tile centre (the guard in the L
   // statistics kernel uses the same one)
-  const double cL = a.L[(int64_t)clampi(y0 + th / 2, 0, H - 1) * a.ld + clampi(x0 + kTW / 2, 0, W - 1)];
+  const double cL = a.Lv(clampi(y0 + th / 2, 0, H - 1), clampi(x0 + kTW / 2, 0, W - 1));
   for (int t = tid; t < (th + B + 1) * NV; t += nt) {
     const int rr = t / NV, c = t - rr * NV;
     const int y = clampi(y0 - 1 - H2 + rr, 0, H - 1), x = clampi(x0 - 1 - H2 + c, 0, W - 1);
-    Lt[rr * NVP + c] = (float)(a.L[(int64_t)y * a.ld + x] - cL);
+    Lt[rr * NVP + c] = (float)(a.Lv(y, x) - cL);
   }
   __syncthreads();
   // cost row k (output row k - 1) is needed by SEL of row k - 1 and REF of
