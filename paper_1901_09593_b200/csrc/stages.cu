@@ -74,6 +74,58 @@ __global__ void downsample_kernel(const T* in0, const T* in1, int h, int w, int6
   }
 }
 
+// gaussian_downsample, pipeline form: a 32 x 16 output tile per CTA.  The
+// replicate-clamped input region (35 x 67) is staged in shared memory with
+// coalesced row loads, then the vertical 5-tap pass (only the kept rows)
+// and the horizontal pass (only the kept columns) -- the same arithmetic
+// and order as downsample_kernel, so the values are identical.
+template <typename T>
+__global__ void __launch_bounds__(256) downsample_tile_kernel(const T* in0, const T* in1, int h,
+                                                              int w, int64_t ldi, double* out0,
+                                                              double* out1, int64_t ldo, int oh,
+                                                              int ow, int i0, int i1) {
+  pdl_wait();
+  constexpr int OW = 32, OH = 16, IR = 2 * OH + 3, IC = 2 * OW + 3;
+  __shared__ double X[IR][IC];
+  // kept columns 2J + b in two planes by parity: Ve[I][m] = column 2m,
+  // Vo[I][m] = column 2m + 1, so the horizontal pass reads consecutive
+  // doubles across lanes
+  __shared__ double Ve[OH][OW + 2], Vo[OH][OW + 2];
+  const T* in = blockIdx.z ? in1 : in0;
+  double* out = blockIdx.z ? out1 : out0;
+  const int J0 = blockIdx.x * OW, I0 = i0 + blockIdx.y * OH;
+  const int tid = threadIdx.x;
+  for (int t = tid; t < IR * IC; t += 256) {
+    const int r = t / IC, c = t - r * IC;
+    const int y = clampi(2 * I0 - 2 + r, 0, h - 1), x = clampi(2 * J0 - 2 + c, 0, w - 1);
+    X[r][c] = (double)in[(int64_t)y * ldi + x];
+  }
+  __syncthreads();
+  const double k[5] = {1.0 / 16.0, 4.0 / 16.0, 6.0 / 16.0, 4.0 / 16.0, 1.0 / 16.0};
+  for (int t = tid; t < OH * IC; t += 256) {
+    const int I = t / IC, c = t - I * IC;
+    double v = 0.0;
+#pragma unroll
+    for (int a = 0; a < 5; ++a) v += k[a] * X[2 * I + a][c];
+    if (c & 1) Vo[I][c >> 1] = v;
+    else Ve[I][c >> 1] = v;
+  }
+  __syncthreads();
+  for (int t = tid; t < OH * OW; t += 256) {
+    const int I = t / OW, J = t - I * OW;
+    const int gi = I0 + I, gj = J0 + J;
+    if (gi >= i1 || gi >= oh || gj >= ow) continue;
+    // columns 2J .. 2J + 4 = Ve[J], Vo[J], Ve[J + 1], Vo[J + 1], Ve[J + 2]
+    double acc = 0.0;
+    acc += k[0] * Ve[I][J];
+    acc += k[1] * Vo[I][J];
+    acc += k[2] * Ve[I][J + 1];
+    acc += k[3] * Vo[I][J + 1];
+    acc += k[4] * Ve[I][J + 2];
+    out[(int64_t)gi * ldo + gj] = acc;
+  }
+}
+
 // ------------------------------------------------------------------ K2
 // Box mean and centred sigma of the b x b replicate-padded window
 // (zncc.py:185-189 computes the same quantities via uniform_filter raw
@@ -461,7 +513,8 @@ __global__ void __launch_bounds__(256) stats32_kernel(const TIn* img, int h, int
                                                       int64_t lds, int y_base) {
   pdl_wait();
   constexpr int H2 = B / 2, TR = 32 + B - 1, TC = 32 + B - 1;
-  __shared__ double T[TR][TC];
+  constexpr int TCP = TC | 1;   // odd row pitch (doubles): lanes on consecutive rows hit distinct banks
+  __shared__ double T[TR][TCP];
   __shared__ double H1[TR][33], H2s[TR][33];
   const int x0 = blockIdx.x * 32, y0 = y_base + blockIdx.y * 32;
   const int tid = threadIdx.y * 32 + threadIdx.x;
@@ -473,8 +526,9 @@ __global__ void __launch_bounds__(256) stats32_kernel(const TIn* img, int h, int
   }
   __syncthreads();
   // horizontal: each item = 4 consecutive window sums of one tile row
+  // (consecutive lanes on consecutive rows)
   for (int it = tid; it < TR * 8; it += 256) {
-    const int r = it >> 3, c0 = (it & 7) * 4;
+    const int r = it % TR, c0 = (it / TR) * 4;
     double s1 = 0.0, s2 = 0.0;
 #pragma unroll
     for (int k = 0; k < B; ++k) {
@@ -521,9 +575,10 @@ __global__ void __launch_bounds__(256) stats32_kernel(const TIn* img, int h, int
           }
         var = ss * inv;
       }
-      const double sigma = sqrt(fmax(var, 0.0));
+      // sigma >= eps <=> var >= eps^2 (no sqrt for the test); 1/sigma
+      // through the fp64 reciprocal square root, rounded once to fp32
       mu32[(int64_t)y * lds + x] = (float)(m1 + c);
-      is32[(int64_t)y * lds + x] = sigma >= sigma_eps ? (float)(1.0 / sigma) : 0.f;
+      is32[(int64_t)y * lds + x] = var >= sigma_eps * sigma_eps ? (float)rsqrt(var) : 0.f;
     }
   }
 }
@@ -762,9 +817,16 @@ __global__ void __launch_bounds__(kTX * kTY) median_tiled_kernel(
       nneeded += (needed && i >= band.cnt_lo && i < band.cnt_hi) ? 1u : 0u;
       // low-confidence pixels go to the work list; the others keep their
       // disparity
-      if (Lw[ty][tx] & 2) list[atomicAdd(&nlist, 1)] = (short)(py * kTX + threadIdx.x);
-      else out[(int64_t)i * ld + j] = Ds[ty][tx];
+      if (!(Lw[ty][tx] & 2)) out[(int64_t)i * ld + j] = Ds[ty][tx];
     }
+    // the list keeps each warp's row in order (one atomic per warp), so the
+    // pixel pairs sorted together are neighbours with overlapping windows
+    const bool lw = i < band.hi && i < h && j < w && (Lw[py + 2][threadIdx.x + 2] & 2);
+    const unsigned m = __ballot_sync(0xffffffffu, lw);
+    int base = 0;
+    if (threadIdx.x == 0 && m) base = atomicAdd(&nlist, __popc(m));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (lw) list[base + __popc(m & ((1u << threadIdx.x) - 1u))] = (short)(py * kTX + threadIdx.x);
   }
   __syncthreads();
   unsigned nchanged = 0;
@@ -960,10 +1022,9 @@ cudaError_t launch_downsample(const double* in0, const double* in1, int h,
   const int oh = (h + 1) / 2, ow = (w + 1) / 2;
   if (i1 < 0 || i1 > oh) i1 = oh;
   if (i1 <= i0) return cudaSuccess;
-  dim3 blk(32, 8);
-  return launch_pdl(downsample_kernel<double, false>, grid2d(ow, i1 - i0, blk, in1 ? 2 : 1), blk,
-                    0, s, in0, in1, h, w, ld_in, out0, out1, ld_out, oh, ow, (double*)nullptr,
-                    (double*)nullptr, (int64_t)0, i0, i1, 2);
+  const dim3 g((ow + 31) / 32, (i1 - i0 + 15) / 16, in1 ? 2 : 1);
+  return launch_pdl(downsample_tile_kernel<double>, g, dim3(256), 0, s, in0, in1, h, w, ld_in,
+                    out0, out1, ld_out, oh, ow, i0, i1);
 }
 
 // binomial_smooth (pyramid.py:65-68): the same separable 5-tap filter at
@@ -985,9 +1046,8 @@ cudaError_t launch_downsample_f32(const float* in0, const float* in1, int h, int
   if (i1 <= i0) return cudaSuccess;
   dim3 blk(32, 8);
   if (copy0 == nullptr)   // level 0 stays fp32 (its consumers read the input)
-    return launch_pdl(downsample_kernel<float, false>, grid2d(ow, i1 - i0, blk, 2), blk, 0, s,
-                      in0, in1, h, w, ld_in, out0, out1, ld_out, oh, ow, copy0, copy1, ld_copy,
-                      i0, i1, 2);
+    return launch_pdl(downsample_tile_kernel<float>, dim3((ow + 31) / 32, (i1 - i0 + 15) / 16, 2),
+                      dim3(256), 0, s, in0, in1, h, w, ld_in, out0, out1, ld_out, oh, ow, i0, i1);
   return launch_pdl(downsample_kernel<float, true>, grid2d(ow, i1 - i0, blk, 2), blk, 0, s, in0,
                     in1, h, w, ld_in, out0, out1, ld_out, oh, ow, copy0, copy1, ld_copy, i0, i1, 2);
 }
