@@ -274,6 +274,13 @@ __global__ void __launch_bounds__(kNWMax * 32, 2) sweep4_kernel(const SweepArgs 
   const unsigned long long needc = ((unsigned long long)selm << 1) |
                                    ((unsigned long long)refm << 2) |
                                    ((unsigned long long)refm << 1) | (unsigned long long)refm;
+  // the sweep stops after the last needed cost row (a row band's bottom
+  // halo tile needs its first rows only).  It always starts at row 0: the
+  // fp32 sliding sums then hold the same values whichever rows a run needs,
+  // so row bands stay bit-identical to whole-image runs (a data-dependent
+  // start row measured no faster on whole images).
+  constexpr int k0 = 0;
+  const int kend = 64 - __clzll((long long)needc);
   // per cost pixel: the sum of L' over its window (fp64 sums of the fp32
   // values, so the centring cancels the rounding of L'), separable through
   // per-row horizontal sums, and kL = 1/(b^2 sigma_L)
@@ -343,10 +350,10 @@ __global__ void __launch_bounds__(kNWMax * 32, 2) sweep4_kernel(const SweepArgs 
 
     if (tid == 0) {
       fence_proxy_async();
-      const int nr0 = min(B + G, th + B + 1), nm0 = min(G, th + 2);
+      const int nr0 = min(B + G, th + B + 1 - k0), nm0 = min(G, th + 2 - k0);
       mbar_expect_tx(bars, nr0 * rbytes + nm0 * mbytes);
-      for (int rr = 0; rr < nr0; ++rr) stage_r(rr, bars);
-      for (int k = 0; k < nm0; ++k) stage_m(k, bars);
+      for (int rr = k0; rr < k0 + nr0; ++rr) stage_r(rr, bars);
+      for (int k = k0; k < k0 + nm0; ++k) stage_m(k, bars);
     }
     mbar_wait(bars, phase & 1u);
     phase ^= 1u;
@@ -357,8 +364,8 @@ __global__ void __launch_bounds__(kNWMax * 32, 2) sweep4_kernel(const SweepArgs 
       for (int c = 0; c < NV; ++c) V[c] = 0.f;
 #pragma unroll
       for (int r = 0; r < B; ++r) {
-        const float4* lr = reinterpret_cast<const float4*>(Lt + r * NVP);
-        const float* rrow = Rr + r * lay.rwp + lb;
+        const float4* lr = reinterpret_cast<const float4*>(Lt + (k0 + r) * NVP);
+        const float* rrow = Rr + ((k0 + r) % RB) * lay.rwp + lb;
 #pragma unroll
         for (int c4 = 0; c4 < NVP / 4; ++c4) {
           const float4 l4 = lr[c4];
@@ -413,13 +420,13 @@ __global__ void __launch_bounds__(kNWMax * 32, 2) sweep4_kernel(const SweepArgs 
       }
     };
 #pragma unroll 1
-    for (int k = 0; k < th + 2; k += G) {
-      if (k > 0) {
+    for (int k = k0; k < kend; k += G) {
+      if (k > k0) {
         mbar_wait(bars, phase & 1u);
         phase ^= 1u;
         __syncthreads();   // every warp done with the previous group (its slots are reused)
       }
-      if (tid == 0 && k + G <= th + 1) {
+      if (tid == 0 && k + G < kend) {
         fence_proxy_async();
         const int r0 = k + B + G, r1 = min(k + B + 2 * G, th + B + 1);
         const int m0 = k + G, m1 = min(k + 2 * G, th + 2);
@@ -429,7 +436,7 @@ __global__ void __launch_bounds__(kNWMax * 32, 2) sweep4_kernel(const SweepArgs 
       }
 #pragma unroll 1
       for (int g = 0; g < G; ++g) {
-        if (k + g < th + 2) step(k + g);
+        if (k + g < kend) step(k + g);
       }
     }
   }
