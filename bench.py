@@ -411,27 +411,35 @@ class Workload:
         lib.check(st, self.ctx)
 
 
-def sweep4_row_step_flops(b: int) -> int:
-    """Implemented FP32 flops of one sweep4 row step of one lane (one z) over
-    the 16 output pixels of a CTA tile (csrc/sweep4.cu, FFMA = 2 flops):
-      V slide   2 FFMA per tile column, NV = 16 + b + 1 columns   4 NV
-      S sums    two sliding chains over the NC = 18 cost columns  2 (b + 16)
-      cost      FFMA + FMUL + FFMA.sat per cost column            5 NC
-      WTA       per pixel: key FADD; 3x3: 2 FADD + FADD + FFMA;
-                vertical 3-sum carry FADD                         16 x 7
-    Divided by 16 this is the implemented count per (pixel, disparity) of
-    the dense sweep (SURVEY 8d asks a sliding-sum design to declare its own
-    count); tools/flop_check.py checks it against ncu's FP32 instruction
-    counts."""
-    nv, nc = 16 + b + 1, 18
-    return 4 * nv + 2 * (b + 16) + 5 * nc + 16 * 7
+FLOPS_JSON = os.path.join(ROOT, "profiles", "r02_flops.json")
 
 
-def impl_flops_per_pde(kernel: str, b: int) -> float:
-    if kernel == "sweep4_kernel":
-        return sweep4_row_step_flops(b) / 16.0
-    # sweep2: b^2 + b + 1 FMAs per two pixels + normalise / WTA (~11 flops)
-    return (b * b + b + 1) + 11.0
+def implemented_work(cfg_name):
+    """Implemented FP32 flops and DRAM bytes of the level-0 selection stage
+    (prior_select_kernel + sweep4_kernel, or sweep2_kernel on levels sweep4
+    does not take) for one pair of the workload, counted by ncu on the GPU
+    box (tools/flop_check.py: FADD + FMUL + 2 FFMA predicated-on thread
+    instructions; dram__bytes_read + dram__bytes_write).  The counts depend
+    only on the seeded input, so the committed capture holds for this run.
+    SURVEY 8(d) asks a sliding-sum design to declare its implemented count;
+    this is it, measured rather than modelled.  None if not captured."""
+    try:
+        with open(FLOPS_JSON) as f:
+            rec = json.load(f).get(cfg_name)
+    except (OSError, ValueError):
+        return None
+    if not rec:
+        return None
+    sys.path.insert(0, os.path.join(ROOT, "tools"))
+    from flop_check import summary
+    sm = summary(rec)
+    flops, dram = sm["flops"], sm["dram_bytes"]
+    kern = sm["kernel"]
+    if "prior_select" in sm:
+        flops += sm["prior_select"]["flops"]
+        dram += sm["prior_select"]["dram_bytes"]
+        kern = "prior_select_kernel + " + kern
+    return {"flops": flops, "dram_bytes": dram, "kernels": kern, "ncu_us": sm["us"]}
 
 
 def measure(wl, steps, flush, stream, barrier, max_over_ranks, use_flush=True):
@@ -549,29 +557,35 @@ def run_ours(args, cfg):
     pms = C.c_double()
     _lib.check(_lib.lib().mshbm_probe_fp32_peak(local, 20000, C.byref(tf), C.byref(pms)))
     kname = sweep_kernel_name(l0)
-    dense_pde = l0.pixels * (l0.d_max + 1)
-    impl = impl_flops_per_pde(kname, l0.block)
-    impl_flops = dense_pde * impl
-    achieved = impl_flops / (sweep_ms * 1e-3) / 1e12
+    work = implemented_work(cfg.name)
     direct_flops = l0.evals * flops_per_pde(l0.block)
     direct = direct_flops / (sweep_ms * 1e-3) / 1e12
     per_pair_ms = ms / max(1, wl.pairs_per_step / ws) if wl.kind != "bands" else ms
-    traffic = TRAFFIC.get(cfg.name)
     hbm_peak = hbm_peak_gbs()
-    roof = {"bound": "fp32", "kernel": "%s<b=%d> (level 0)" % (kname, l0.block),
+    if work is not None:
+        achieved = work["flops"] / (sweep_ms * 1e-3) / 1e12
+        traffic = work["dram_bytes"]
+        basis = ("implemented count: FADD + FMUL + 2 FFMA predicated-on thread instructions of "
+                 f"{work['kernels']} for this workload's pair, counted by ncu "
+                 "(tools/flop_check.py, profiles/r02_flops.json)")
+    else:
+        achieved, traffic, basis = direct, None, "direct-form count (no ncu capture committed)"
+    roof = {"bound": "fp32",
+            "kernel": "level-0 selection stage: %s<b=%d> (+ prior_select_kernel, fixup)" %
+                      (kname, l0.block),
             "achieved": achieved, "peak": tf.value, "unit": "TFLOP/s",
             "frac": achieved / tf.value,
             "traffic": traffic,
-            "traffic_source": "ncu --set full dram__bytes_read.sum + dram__bytes_write.sum of "
-                              "this launch (profiles/r02_ncu_sweep_*.md)" if traffic else None,
+            "traffic_source": ("ncu dram__bytes_read.sum + dram__bytes_write.sum of the stage's "
+                               "kernels (profiles/r02_flops.json)") if traffic else None,
             "hbm_time_ms": (traffic / (hbm_peak * 1e9) * 1e3) if traffic else None,
             "peak_source": "measured live: mshbm_probe_fp32_peak FFMA probe on this GPU "
                            "(MEASURED_PEAKS.json has no FP32 figure)",
-            "algorithmic_flops_per_launch": impl_flops,
-            "algorithmic_basis": f"implemented count: dense level-0 PDE W*H*(D+1) = {dense_pde} "
-                                 f"x {impl:.4g} flops per PDE (bench.sweep4_row_step_flops, "
-                                 "checked against ncu FP32 instruction counts, tools/flop_check.py)",
+            "algorithmic_flops_per_launch": work["flops"] if work else direct_flops,
+            "algorithmic_basis": basis,
             "launch_ms": sweep_ms,
+            "launch_ms_source": "CUDA events around the level-0 selection stage (timed graph "
+                                "replay, median of 5)",
             "share_of_step": sweep_ms / per_pair_ms if wl.kind != "bands" or ws == 1 else None,
             "direct_equivalent": {
                 "achieved": direct, "frac": direct / tf.value, "flops_per_launch": direct_flops,
@@ -638,11 +652,6 @@ def hbm_peak_gbs() -> float:
             return float(json.load(f)["hbm_gbs"])
     except (OSError, KeyError, ValueError):
         return 6552.0
-
-
-# dram__bytes_read.sum + dram__bytes_write.sum of the level-0 sweep launch from
-# the committed ncu --set full captures (profiles/), per config
-TRAFFIC = {"C2": 43133696 + 835584}   # r01_sweep4_c2_ncu.md (ncu --set full, L0 sweep)
 
 
 def sweep_kernel_name(level) -> str:
