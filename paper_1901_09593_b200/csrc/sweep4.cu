@@ -525,24 +525,59 @@ __global__ void __launch_bounds__(kNWMax * 32, 2) sweep4_kernel(const SweepArgs 
 
 // Trusted-window selection of a sweep4 level (matcher.py:263-320, prior
 // window +-r), before the dense sweep.  For every trusted pixel the <= 2r+1
-// candidates [c - r, c + r] & [0, d] are scored directly, centred per pixel
-// (L' = L - muL rounded once; S = sum L' R' - (sum L') (muR(q) - c), the
-// fp64 sum of L' cancelling its rounding), ascending z with a strict >, so
-// ties keep the smallest z.  Non-low pixels get their final outputs here and
-// are marked kWcDone (the sweep skips them); low pixels are marked kWcLow
-// and counted (the sweep computes only their 3x3-summed refinement,
-// matcher.py:196-233); untrusted pixels keep kWcNone.  Tiles the precision
-// guard flagged are left whole to the sweep2 fixup.  One thread per pixel,
-// the right span of one window row in registers.
+// candidates [c - r, c + r] & [0, d] are scored directly, ascending z with a
+// strict >, so ties keep the smallest z.  Non-low pixels get their final
+// outputs here and are marked kWcDone (the sweep skips them); low pixels are
+// marked kWcLow and counted (the sweep computes only their 3x3-summed
+// refinement, matcher.py:196-233); untrusted pixels keep kWcNone.  Tiles the
+// precision guard flagged are left whole to the sweep2 fixup.
+//
+// Centring: with L'' = fl32(L - m) for any constant m near the window's mean
+// (one rounding per value) and R' = fl32(R - c) (staging), the centred
+// cross sum of a window W is
+//   sum_W L'' R' - (sum_W L'') (muR(q) - c)
+// (sum_W R' = b^2 (muR(q) - c)), whichever m was subtracted; sum_W L'' is
+// accumulated in fp64, so it cancels the rounding of the centring exactly.
+// The 2x nearest-neighbour prior gives the pixels (2m, j) and (2m+1, j) the
+// same window centre, so one thread scores both: their windows share b - 1
+// rows, L'' is centred once (on the upper pixel's mean) and every shared row
+// feeds both, (b + 1) x b x (2r + 1) FMAs for two pixels instead of
+// 2 x b^2 x (2r + 1).  A 32 x 16-pixel tile of L is staged in shared memory;
+// the right span of one window row sits in registers.
+// one window row r (image row y) of one window centre: acc[zi] += sum over
+// the row of L''(cc) R'(cc -+ (lo + zi)), rs += sum of the row's L'' (fp64)
+template <int B, int DIR, int MAXW, typename LT>
+__device__ __forceinline__ void psel_row(const SweepArgs& a, const LT* lrow,
+                                         const float* __restrict__ Rp, int y, float m,
+                                         float (&acc)[MAXW], double& rs) {
+  constexpr int NRV = B + MAXW - 1;
+  const float* __restrict__ rrow = Rp + (int64_t)clampi(y, 0, a.H - 1) * a.ldp;
+  float rv[NRV], l[B];
+#pragma unroll
+  for (int e = 0; e < NRV; ++e) rv[e] = __ldg(rrow + e);
+#pragma unroll
+  for (int cc = 0; cc < B; ++cc) {
+    if constexpr (std::is_same<LT, float>::value) l[cc] = lrow[cc] - m;
+    else l[cc] = (float)(lrow[cc] - (double)m);
+  }
+#pragma unroll
+  for (int cc = 0; cc < B; ++cc) {
+    rs += (double)l[cc];
+#pragma unroll
+    for (int zi = 0; zi < MAXW; ++zi)
+      acc[zi] = fmaf(l[cc], rv[DIR > 0 ? cc + MAXW - 1 - zi : cc + zi], acc[zi]);
+  }
+}
+
 template <int B, int DIR, int MAXW, bool F32>
-__global__ void __launch_bounds__(256, 4) prior_select_kernel(const SweepArgs a, const int th) {
+__global__ void __launch_bounds__(256, 3) prior_select_kernel(const SweepArgs a, const int th) {
   pdl_wait();
-  constexpr int H2 = B / 2, NRV = B + MAXW - 1;
-  constexpr int TR = 8 + B - 1, TC = 32 + B - 1;   // left tile (replicate-clamped)
+  constexpr int H2 = B / 2;
+  constexpr int TR = 16 + B - 1, TC = 32 + B - 1;   // left tile (replicate-clamped)
   using LT = typename std::conditional<F32, float, double>::type;
   __shared__ LT Ls[TR][TC];
-  const int x0 = blockIdx.x * 32, y0 = a.rows.lo + blockIdx.y * 8;
-  const int j = x0 + threadIdx.x, i = y0 + threadIdx.y;
+  const int x0 = blockIdx.x * 32, y0 = (a.rows.lo & ~1) + blockIdx.y * 16;
+  const int j = x0 + threadIdx.x, iA = y0 + 2 * threadIdx.y;
   const int H = a.H, W = a.W;
   for (int t = threadIdx.x + 32 * threadIdx.y; t < TR * TC; t += 256) {
     const int rr = t / TC, cc = t - rr * TC;
@@ -553,46 +588,21 @@ __global__ void __launch_bounds__(256, 4) prior_select_kernel(const SweepArgs a,
   __syncthreads();
   int* wc = const_cast<int*>(a.wc);
   unsigned nlow = 0;
-  int c = kWcNone;
-  if (i < a.rows.hi && i < H && j < W) c = wc[(int64_t)i * a.ldw + j];
-  if (c > kWcLow &&
-      !(a.tile_flags != nullptr && a.tile_flags[(int64_t)(i / th) * a.flags_ld + (j >> 4)] != 0)) {
-    const int lo = max(c - a.radius, 0), hi = min(c + a.radius, a.d);
-    const int nw = hi - lo + 1;   // >= 1: trusted windows meet [0, d] (prior)
+  // trusted window centre of pixel (i, j) in this stage's rows, else kWcNone
+  auto centre = [&](int i) -> int {
+    if (i < a.rows.lo || i >= a.rows.hi || i >= H || j >= W) return kWcNone;
+    const int c = wc[(int64_t)i * a.ldw + j];
+    if (c <= kWcLow) return kWcNone;
+    if (a.tile_flags != nullptr && a.tile_flags[(int64_t)(i / th) * a.flags_ld + (j >> 4)] != 0)
+      return kWcNone;
+    return c;
+  };
+  const int cA = centre(iA), cB = centre(iA + 1);
+  // score pixel i's window [lo, lo + nw) from its cross sums S and the fp64
+  // sum of its L'' values; write / mark it
+  auto finish = [&](int i, int lo, int nw, const float (&S)[MAXW], double sumL) {
     const float is = a.isL[(int64_t)i * a.lds + j];
     const float kL = is > 0.f ? is * (1.0f / (float)(B * B)) : __int_as_float(0x7fc00000);
-    const float muf = a.muL[(int64_t)i * a.lds + j];
-    float S[MAXW];
-#pragma unroll
-    for (int zi = 0; zi < MAXW; ++zi) S[zi] = 0.f;
-    double sumL = 0.0;
-    // first staged right column of this pixel's window rows: z = lo + zi
-    // reads column j - H2 + cc - z (middlebury) or j - H2 + cc + z (paper)
-    const int base = DIR > 0 ? (j - H2 - (lo + MAXW - 1)) : (j - H2 + lo);
-    const float* __restrict__ Rp = a.Rp + a.pc + base;
-#pragma unroll 1
-    for (int r = 0; r < B; ++r) {
-      const int y = clampi(i - H2 + r, 0, H - 1);
-      const float* __restrict__ rrow = Rp + (int64_t)y * a.ldp;
-      const LT* lrow = &Ls[threadIdx.y + r][threadIdx.x];
-      float rv[NRV], l[B];
-#pragma unroll
-      for (int e = 0; e < NRV; ++e) rv[e] = __ldg(rrow + e);
-      // L' = L - muL rounded once to fp32 (level 0 is the fp32 input, where
-      // the fp32 subtraction is that rounding; coarser levels via fp64)
-#pragma unroll
-      for (int cc = 0; cc < B; ++cc) {
-        if constexpr (F32) l[cc] = lrow[cc] - muf;
-        else l[cc] = (float)(lrow[cc] - (double)muf);
-      }
-#pragma unroll
-      for (int cc = 0; cc < B; ++cc) {
-        sumL += (double)l[cc];
-#pragma unroll
-        for (int zi = 0; zi < MAXW; ++zi)
-          S[zi] = fmaf(l[cc], rv[DIR > 0 ? cc + MAXW - 1 - zi : cc + zi], S[zi]);
-      }
-    }
     const float sl = (float)sumL;
     const float2* __restrict__ Mrow = a.Mp + a.pc + (int64_t)i * a.ldp;
     float best = -1.f;
@@ -601,8 +611,8 @@ __global__ void __launch_bounds__(256, 4) prior_select_kernel(const SweepArgs a,
     for (int zi = 0; zi < MAXW; ++zi) {
       if (zi < nw) {
         const int z = lo + zi;
-        const float2 m = Mrow[DIR > 0 ? j - z : j + z];
-        const float cp = fma_sat(fmaf(-sl, m.x, S[zi]) * kL, m.y, 0.5f);
+        const float2 mm = Mrow[DIR > 0 ? j - z : j + z];
+        const float cp = fma_sat(fmaf(-sl, mm.x, S[zi]) * kL, mm.y, 0.5f);
         if (cp > best) best = cp, bz = z;
       }
     }
@@ -611,13 +621,51 @@ __global__ void __launch_bounds__(256, 4) prior_select_kernel(const SweepArgs a,
     const int64_t o = (int64_t)i * a.ldo + j;
     if (low) {
       wc[(int64_t)i * a.ldw + j] = kWcLow;
-      nlow = (i >= a.rows.cnt_lo && i < a.rows.cnt_hi) ? 1u : 0u;
+      nlow += (i >= a.rows.cnt_lo && i < a.rows.cnt_hi) ? 1u : 0u;
     } else {
       a.dout[o] = (int16_t)bz;
       a.cout[o] = cs;
       a.low[o] = 0;
       wc[(int64_t)i * a.ldw + j] = kWcDone;
     }
+  };
+  // one pass over the rows of one window centre c: rows iA - H2 .. iA + H2
+  // (+ one more for the pair), centred on pixel i0's fp32 mean
+  auto score = [&](int c, int i0, bool pair, bool fin0, bool fin1) {
+    const int lo = max(c - a.radius, 0), hi = min(c + a.radius, a.d);
+    const int nw = hi - lo + 1;   // >= 1: trusted windows meet [0, d] (prior)
+    const float m = a.muL[(int64_t)i0 * a.lds + j];
+    float S0[MAXW], P[MAXW], S1[MAXW];
+#pragma unroll
+    for (int zi = 0; zi < MAXW; ++zi) S0[zi] = 0.f, P[zi] = 0.f, S1[zi] = 0.f;
+    double sum0 = 0.0, sP = 0.0, sum1 = 0.0;
+    // first staged right column of the window rows: z = lo + zi reads column
+    // j - H2 + cc - z (middlebury) or j - H2 + cc + z (paper)
+    const int base = DIR > 0 ? (j - H2 - (lo + MAXW - 1)) : (j - H2 + lo);
+    const float* Rp = a.Rp + a.pc + base;
+    const LT* l0 = &Ls[i0 - y0][threadIdx.x];
+    // row 0: pixel i0 only; rows 1 .. b-1: shared; row b: pixel i0 + 1 only
+    psel_row<B, DIR, MAXW, LT>(a, l0, Rp, i0 - H2, m, S0, sum0);
+#pragma unroll 1
+    for (int r = 1; r < B; ++r) psel_row<B, DIR, MAXW, LT>(a, l0 + r * TC, Rp, i0 - H2 + r, m, P, sP);
+    if (pair) psel_row<B, DIR, MAXW, LT>(a, l0 + B * TC, Rp, i0 - H2 + B, m, S1, sum1);
+    float SA[MAXW];
+#pragma unroll
+    for (int zi = 0; zi < MAXW; ++zi) SA[zi] = S0[zi] + P[zi];
+    if (fin0) finish(i0, lo, nw, SA, sum0 + sP);
+    if (pair && fin1) {
+#pragma unroll
+      for (int zi = 0; zi < MAXW; ++zi) SA[zi] = P[zi] + S1[zi];
+      finish(i0 + 1, lo, nw, SA, sP + sum1);
+    }
+  };
+  // every lane with a trusted pixel runs the same pair pass (no divergent
+  // single-pixel paths); the 2x NN prior gives both pixels the same centre,
+  // so a second pass is only needed for centres that differ
+  if (cA != kWcNone || cB != kWcNone) {
+    const int c = cA != kWcNone ? cA : cB;
+    score(c, iA, true, cA != kWcNone, cB != kWcNone && cB == c);
+    if (cB != kWcNone && cB != c) score(cB, iA + 1, false, true, false);
   }
   const int slot[1] = {kCntRefined};
   const unsigned long long val[1] = {nlow};
@@ -662,7 +710,7 @@ cudaError_t launch4(const SweepArgs& a, cudaStream_t s) {
   static SmemAttr attr;
   if (cudaError_t e = attr.ensure(sweep4_kernel<B, DIR, G>, lay.bytes); e != cudaSuccess) return e;
   if (a.wc != nullptr) {   // trusted windows first (prior_select_kernel)
-    dim3 pg((a.W + 31) / 32, (a.rows.hi - a.rows.lo + 7) / 8);
+    dim3 pg((a.W + 31) / 32, (a.rows.hi - (a.rows.lo & ~1) + 15) / 16);
     cudaError_t e = a.L32 != nullptr ? launch_prior_select<B, DIR, true>(a, th, pg, s)
                                       : launch_prior_select<B, DIR, false>(a, th, pg, s);
     if (e != cudaSuccess) return e;
