@@ -570,7 +570,7 @@ __device__ __forceinline__ void psel_row(const SweepArgs& a, const LT* lrow,
 }
 
 template <int B, int DIR, int MAXW, bool F32>
-__global__ void __launch_bounds__(256, 3) prior_select_kernel(const SweepArgs a, const int th) {
+__global__ void __launch_bounds__(256, 4) prior_select_kernel(const SweepArgs a, const int th) {
   pdl_wait();
   constexpr int H2 = B / 2;
   constexpr int TR = 16 + B - 1, TC = 32 + B - 1;   // left tile (replicate-clamped)
