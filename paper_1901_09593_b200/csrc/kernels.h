@@ -142,6 +142,13 @@ cudaError_t launch_downsample_f32(const float* in0, const float* in1, int h, int
 // BASELINE configs stay far below the limit; the reference's smooth
 // low-contrast [0, 1] fixtures reach it.
 constexpr float kSweep4RiskMax = 200.f;
+// sweep4 tile rows (and the guard's tiles) are offset by kTileOff: tile ty
+// covers image rows [ty th - kTileOff, (ty + 1) th - kTileOff).  Row bands
+// start at multiples of 2^K, so a band's top median halo (its 2 rows above)
+// is the last 2 rows of the tile that ends at the band start, not a whole
+// extra tile.
+constexpr int kTileOff = 2;
+__host__ __device__ inline int tile_row(int y, int th) { return (y + kTileOff) / th; }
 struct Sweep4Guard {
   const double* L = nullptr;    // level image (cL samples), stride ld
   int64_t ld = 0;

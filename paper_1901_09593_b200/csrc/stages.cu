@@ -593,7 +593,7 @@ __global__ void __launch_bounds__(128) guard_col_kernel(const Sweep4Guard g, int
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= g.w) return;
   const int ty = ty0 + blockIdx.y;
-  const int y0 = ty * g.tile_h;
+  const int y0 = ty * g.tile_h - kTileOff;
   const float c = *g.cR;
   float m = 0.f;
   for (int y = max(y0 - 1, 0); y <= min(y0 + g.tile_h, g.h - 1); ++y) {
@@ -606,7 +606,7 @@ __global__ void __launch_bounds__(128) guard_col_kernel(const Sweep4Guard g, int
 // one warp per tile: max aL over the cost pixels x max aR over their right span
 __global__ void __launch_bounds__(32) guard_tile_kernel(const Sweep4Guard g, int ty0) {
   const int tx = blockIdx.x, ty = ty0 + blockIdx.y, lane = threadIdx.x;
-  const int x0 = tx * 16, y0 = ty * g.tile_h;
+  const int x0 = tx * 16, y0 = ty * g.tile_h - kTileOff;
   const int64_t cy = clampi(y0 + g.tile_h / 2, 0, g.h - 1), cx = clampi(x0 + 8, 0, g.w - 1);
   const double cLd = g.L32 ? (double)g.L32[cy * g.ld32 + cx] : g.L[cy * g.ld + cx];
   const float cL = (float)cLd;
@@ -1230,7 +1230,7 @@ cudaError_t launch_combine_refine(const double* din, const double* cin, int h,
 
 cudaError_t launch_sweep4_guard(const Sweep4Guard& g, RowBand rows, cudaStream_t s) {
   if (g.flags == nullptr || rows.hi <= rows.lo) return cudaSuccess;
-  const int ty0 = rows.lo / g.tile_h, ty1 = (rows.hi - 1) / g.tile_h;
+  const int ty0 = tile_row(rows.lo, g.tile_h), ty1 = tile_row(rows.hi - 1, g.tile_h);
   const int nty = ty1 - ty0 + 1;
   guard_col_kernel<<<dim3((g.w + 127) / 128, nty), 128, 0, s>>>(g, ty0);
   guard_tile_kernel<<<dim3((g.w + 15) / 16, nty), 32, 0, s>>>(g, ty0);

@@ -152,13 +152,13 @@ __device__ __forceinline__ void sweep2_body(const SweepArgs& a, const int bx, co
   const float qnan = __int_as_float(0x7fc00000);
   // sweep4 fixup: only pixels of the tiles sweep4's precision guard flagged
   auto flagged = [&](int i, int jj) {
-    return a.tile_flags[(int64_t)(i / a.tile_h) * a.flags_ld + jj / 16] != 0;
+    return a.tile_flags[(int64_t)tile_row(i, a.tile_h) * a.flags_ld + jj / 16] != 0;
   };
   if (a.fixup) {
     const int ilo = max(y0, 0), ihi = min(y0 + NROW - 3, H - 1);
     const int jlo = max(x0, 0), jhi = min(x0 + 29, W - 1);
     bool any = false;
-    for (int ti = ilo / a.tile_h; ti <= ihi / a.tile_h && !any; ++ti)
+    for (int ti = tile_row(ilo, a.tile_h); ti <= tile_row(ihi, a.tile_h) && !any; ++ti)
       for (int tj = jlo / 16; tj <= jhi / 16; ++tj)
         any |= a.tile_flags[(int64_t)ti * a.flags_ld + tj] != 0;
     if (!any || ilo > ihi || jlo > jhi) return;   // uniform over the CTA
@@ -466,7 +466,7 @@ __global__ void __launch_bounds__(256) fixup_list_kernel(const unsigned* flags, 
   const int ilo = max(y0, 0), ihi = min(y0 + job_rows - 1, h - 1);
   const int jlo = x0, jhi = min(x0 + 29, w - 1);
   bool any = false;
-  for (int ti = ilo / tile_h; ti <= ihi / tile_h && !any; ++ti)
+  for (int ti = tile_row(ilo, tile_h); ti <= tile_row(ihi, tile_h) && !any; ++ti)
     for (int tj = jlo / 16; tj <= jhi / 16; ++tj) any |= flags[(int64_t)ti * flags_ld + tj] != 0;
   if (any && ilo <= ihi && jlo <= jhi) list[atomicAdd(count, 1)] = j;
 }

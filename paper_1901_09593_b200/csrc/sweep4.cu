@@ -236,7 +236,8 @@ __global__ void __launch_bounds__(kNWMax * 32, 2) sweep4_kernel(const SweepArgs 
   // centring amplification (kernels.h Sweep4Guard, evaluated by the L
   // statistics kernel on the statistics branch).  Flagged tiles are left to the per-pixel-centred
   // sweep2 fixup launch (launch_sweep4_fixup), which may run concurrently.
-  if (a.tile_flags != nullptr && a.tile_flags[(int64_t)(y0 / th) * a.flags_ld + blockIdx.x] != 0)
+  if (a.tile_flags != nullptr &&
+      a.tile_flags[(int64_t)tile_row(y0, th) * a.flags_ld + blockIdx.x] != 0)
     return;   // uniform: the whole CTA leaves
   // ---- which output rows need what.  Pixel states (wc): kWcDone = trusted,
   // not low, finished by prior_select_kernel; kWcLow = trusted and low: only
@@ -593,7 +594,8 @@ __global__ void __launch_bounds__(256, 4) prior_select_kernel(const SweepArgs a,
     if (i < a.rows.lo || i >= a.rows.hi || i >= H || j >= W) return kWcNone;
     const int c = wc[(int64_t)i * a.ldw + j];
     if (c <= kWcLow) return kWcNone;
-    if (a.tile_flags != nullptr && a.tile_flags[(int64_t)(i / th) * a.flags_ld + (j >> 4)] != 0)
+    if (a.tile_flags != nullptr &&
+        a.tile_flags[(int64_t)tile_row(i, th) * a.flags_ld + (j >> 4)] != 0)
       return kWcNone;
     return c;
   };
@@ -717,7 +719,7 @@ cudaError_t launch4(const SweepArgs& a, cudaStream_t s) {
   }
   // CTA rows on the whole-image grid (row bands bit-identical to whole runs)
   SweepArgs b = a;
-  b.rows.lo = (a.rows.lo / th) * th;
+  b.rows.lo = tile_row(a.rows.lo, th) * th - kTileOff;
   dim3 grid((a.W + kTW - 1) / kTW, (b.rows.hi - b.rows.lo + th - 1) / th);
   return launch_pdl(sweep4_kernel<B, DIR, G>, grid, dim3(32 * nw), lay.bytes, s, b, th);
 }
