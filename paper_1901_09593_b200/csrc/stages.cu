@@ -94,25 +94,45 @@ __global__ void __launch_bounds__(256) downsample_tile_kernel(const T* in0, cons
   const T* in = blockIdx.z ? in1 : in0;
   double* out = blockIdx.z ? out1 : out0;
   const int J0 = blockIdx.x * OW, I0 = i0 + blockIdx.y * OH;
-  const int tid = threadIdx.x;
-  for (int t = tid; t < IR * IC; t += 256) {
-    const int r = t / IC, c = t - r * IC;
-    const int y = clampi(2 * I0 - 2 + r, 0, h - 1), x = clampi(2 * J0 - 2 + c, 0, w - 1);
-    X[r][c] = (double)in[(int64_t)y * ldi + x];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;   // 32 x 8, no index divisions
+  {
+    // every load of the thread in flight before the shared-memory stores
+    constexpr int NRW = (IR + 7) / 8, NCL = (IC + 31) / 32;
+    T v[NRW][NCL];
+    int xc[NCL];
+#pragma unroll
+    for (int q = 0; q < NCL; ++q) xc[q] = clampi(2 * J0 - 2 + tx + 32 * q, 0, w - 1);
+#pragma unroll
+    for (int p = 0; p < NRW; ++p) {
+      const int r = ty + 8 * p;
+      const T* row = in + (int64_t)clampi(2 * I0 - 2 + r, 0, h - 1) * ldi;
+#pragma unroll
+      for (int q = 0; q < NCL; ++q)
+        if (r < IR && tx + 32 * q < IC) v[p][q] = row[xc[q]];
+    }
+#pragma unroll
+    for (int p = 0; p < NRW; ++p)
+#pragma unroll
+      for (int q = 0; q < NCL; ++q) {
+        const int r = ty + 8 * p, c = tx + 32 * q;
+        if (r < IR && c < IC) X[r][c] = (double)v[p][q];
+      }
   }
   __syncthreads();
   const double k[5] = {1.0 / 16.0, 4.0 / 16.0, 6.0 / 16.0, 4.0 / 16.0, 1.0 / 16.0};
-  for (int t = tid; t < OH * IC; t += 256) {
-    const int I = t / IC, c = t - I * IC;
-    double v = 0.0;
+  for (int I = ty; I < OH; I += 8) {
+    for (int c = tx; c < IC; c += 32) {
+      double v = 0.0;
 #pragma unroll
-    for (int a = 0; a < 5; ++a) v += k[a] * X[2 * I + a][c];
-    if (c & 1) Vo[I][c >> 1] = v;
-    else Ve[I][c >> 1] = v;
+      for (int a = 0; a < 5; ++a) v += k[a] * X[2 * I + a][c];
+      if (c & 1) Vo[I][c >> 1] = v;
+      else Ve[I][c >> 1] = v;
+    }
   }
   __syncthreads();
-  for (int t = tid; t < OH * OW; t += 256) {
-    const int I = t / OW, J = t - I * OW;
+#pragma unroll
+  for (int q = 0; q < OH / 8; ++q) {
+    const int I = ty + 8 * q, J = tx;
     const int gi = I0 + I, gj = J0 + J;
     if (gi >= i1 || gi >= oh || gj >= ow) continue;
     // columns 2J .. 2J + 4 = Ve[J], Vo[J], Ve[J + 1], Vo[J + 1], Ve[J + 2]

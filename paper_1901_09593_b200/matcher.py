@@ -449,7 +449,7 @@ def run_batch(lefts, rights, config: MatchConfig, n_streams: int = 4, trace: boo
 
 
 def run_pipeline_band(left, right, config: MatchConfig, row_begin: int, row_end: int,
-                      trace: bool = True):
+                      trace: bool = True, timed: bool = False):
     """Level-0 rows [row_begin, row_end) of run_pipeline (BASELINE C5 bands).
 
     Bit-identical to the same rows of the whole-image result; limits must be
@@ -473,7 +473,7 @@ def run_pipeline_band(left, right, config: MatchConfig, row_begin: int, row_end:
     tr = (_lib.LevelTraceC * (K.value + 1))() if trace else None
     _lib.check(_lib.lib().mshbm_run_pipeline_band(
         ctx, lt.data_ptr(), rt.data_ptr(), h, w, w, C.byref(cfg), int(row_begin), int(row_end),
-        d16.data_ptr(), c32.data_ptr(), w, tr, C.byref(K), _lib.IO_DEVICE, 0,
-        _lib.current_stream()), ctx)
-    t = _trace_from(tr, K.value, False, time.perf_counter()) if trace else None
+        d16.data_ptr(), c32.data_ptr(), w, tr, C.byref(K), _lib.IO_DEVICE,
+        _lib.FLAG_TIMING if (trace and timed) else 0, _lib.current_stream()), ctx)
+    t = _trace_from(tr, K.value, trace and timed, time.perf_counter()) if trace else None
     return d16, c32, t
