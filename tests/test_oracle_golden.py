@@ -93,3 +93,58 @@ def test_pipeline_matches_reference(name):
 def test_golden_set_complete():
     names = sorted(os.path.basename(p) for p in glob.glob(os.path.join(GOLDEN, "pipe_*.npz")))
     assert len(names) >= 9
+
+
+def _stage_api():
+    return np.load(os.path.join(GOLDEN, "stage_api.npz"))
+
+
+def test_oracle_plane_volume_matches_reference():
+    """CostEngine.plane / full_volume (zncc.py:202-249) incl. the paper sign
+    and a flat patch: the oracle's planes equal the reference's volumes."""
+    g = _stage_api()
+    for i in range(4):
+        b, d, paper = (int(v) for v in g[f"vol_p_{i}"])
+        e = O.Engine(g[f"vol_l_{i}"], g[f"vol_r_{i}"], b, d,
+                     sign="paper" if paper else "middlebury")
+        vol = np.stack([e.plane(z) for z in range(d + 1)])
+        np.testing.assert_allclose(vol, g[f"vol_{i}"], atol=1e-12, rtol=0)
+
+
+def test_oracle_dsi_entries_and_slices_match_reference():
+    """dsi_entry / dsi_slice / averaged_dsi (zncc.py:304-350) restated on the
+    oracle engine's point and row paths."""
+    g = _stage_api()
+    e = O.Engine(g["pt_l"], g["pt_r"], 3, 4)
+    h, w = g["pt_l"].shape
+    for k, (i, j, z) in enumerate(g["pt_ijz"]):
+        got = e.at(np.array([i]), np.array([j]), np.array([z]))[0]
+        assert abs(got - g["pt_entry"][k]) <= 1e-12
+        np.testing.assert_allclose(e.dsi_rows(np.array([i]), np.array([j]))[0],
+                                   g["pt_slice"][k], atol=1e-12, rtol=0)
+        nb = [(i + di, j + dj) for di in (-1, 0, 1) for dj in (-1, 0, 1)
+              if 0 <= i + di < h and 0 <= j + dj < w]
+        avg = e.dsi_rows(np.array([a for a, _ in nb]), np.array([b for _, b in nb])).sum(0)
+        np.testing.assert_allclose(avg, g["pt_avg"][k], atol=1e-12, rtol=0)
+    # an empty (all-outside) neighbourhood falls back to the pixel's own row
+    np.testing.assert_allclose(e.dsi_rows(np.array([0]), np.array([0]))[0], g["pt_avg_far"],
+                               atol=1e-12, rtol=0)
+
+
+def test_oracle_binomial_smooth_matches_reference():
+    g = _stage_api()
+    for i in range(3):
+        np.testing.assert_allclose(O.binomial_smooth(g[f"bs_in_{i}"]), g[f"bs_out_{i}"],
+                                   atol=1e-12, rtol=0)
+
+
+def test_oracle_match_level_with_prior_matches_reference():
+    """match_level_with_prior (matcher.py:362-369) = select -> refine ->
+    median, composed from the oracle's stages."""
+    g = _stage_api()
+    e = O.Engine(g["ml_l"], g["ml_r"], 5, 14)
+    d, c, _ = O.select_with_prior(e, g["ml_dhat"], g["ml_chat"], 0.9)
+    d, c = O.refine_level(e, d, c, 0.9)
+    d = O.selective_median(d, c, 0.9)
+    np.testing.assert_array_equal(d, g["ml_d"])
+    np.testing.assert_allclose(c, g["ml_c"], atol=1e-12, rtol=0)
