@@ -61,5 +61,39 @@ def main(path, title):
         print()
 
 
+def source_lines(path, top=25):
+    """Per-source-line share of executed warp instructions and of the warp
+    stall samples (ncu --page source --print-source cuda,sass)."""
+    txt = subprocess.run(["ncu", "-i", path, "--page", "source", "--csv", "--print-source",
+                          "cuda,sass"], capture_output=True, text=True).stdout
+    cur, hdr, res = None, None, {}
+
+    def num(x):
+        try:
+            return int(x)
+        except ValueError:
+            return 0
+    for r in csv.reader(io.StringIO(txt)):
+        if len(r) >= 2 and r[0] == "File Path":
+            cur = r[1].split("/")[-1]
+            continue
+        if len(r) >= 2 and r[0] == "Line No":
+            hdr = r
+            continue
+        if hdr is None or len(r) < 8 or r[0] == "":
+            continue
+        res[(cur, num(r[0]))] = (num(r[7]), num(r[4]), r[1].strip()[:90])
+    tot = sum(v[0] for v in res.values()) or 1
+    ts = sum(v[1] for v in res.values()) or 1
+    print(f"Top source lines by executed warp instructions ({tot} total; stall samples {ts}):\n")
+    print("| file:line | instr share | stall-sample share | source |\n|---|---|---|---|")
+    for (f, ln), (ni, ns, src) in sorted(res.items(), key=lambda x: -x[1][0])[:top]:
+        src = src.replace("|", "\\|")
+        print(f"| {f}:{ln} | {100 * ni / tot:.1f}% | {100 * ns / ts:.1f}% | `{src}` |")
+    print()
+
+
 if __name__ == "__main__":
     main(sys.argv[1], sys.argv[2] if len(sys.argv) > 2 else sys.argv[1])
+    if "--lines" in sys.argv:
+        source_lines(sys.argv[1])
