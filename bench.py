@@ -354,8 +354,7 @@ class Workload:
             else:
                 d, c, _ = gpu.run_pipeline_band(self.L, self.R, self.mc, self.b0, self.b1,
                                                 trace=False)
-                gpu.sharding.gather_bands(d, self.bands, self.rank, self.ws)
-                gpu.sharding.gather_bands(c, self.bands, self.rank, self.ws)
+                gpu.sharding.gather_maps(d, c, self.bands, self.rank, self.ws)
 
     def e2e_pipelined(self, stream, n):
         """n pair-steps through one mshbm_run_batch call (MSHBM_IO_HOST, 4 slot

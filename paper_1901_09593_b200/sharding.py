@@ -14,7 +14,7 @@ from __future__ import annotations
 
 import copy
 
-__all__ = ["shard_pairs", "plan_bands", "merge_traces", "gather_bands"]
+__all__ = ["shard_pairs", "plan_bands", "merge_traces", "gather_bands", "gather_maps"]
 
 
 def shard_pairs(n_pairs: int, world: int, rank: int) -> list[int]:
@@ -76,3 +76,33 @@ def gather_bands(local, bands, rank, world, group=None):
         return None
     parts = [g.view(pad.dtype)[: b1 - b0] for g, (b0, b1) in zip(gather_list, bands)]
     return torch.cat(parts, dim=0)
+
+
+def gather_maps(d, c, bands, rank, world, group=None):
+    """Gather a rank's disparity (int16) and cost (fp32) bands to rank 0 in
+    ONE collective: each rank sends its two maps as one byte buffer (padded
+    to the tallest band only when bands differ in height).  Rank 0 returns
+    the (H, W) disparity and cost maps, other ranks (None, None)."""
+    import torch
+    import torch.distributed as dist
+    if world == 1:
+        return d, c
+    rows = max(b1 - b0 for b0, b1 in bands)
+    w = d.shape[1]
+    nd, nc = rows * w * 2, rows * w * 4
+    wire = torch.zeros(nd + nc, dtype=torch.uint8, device=d.device)
+    n = d.shape[0] * w
+    wire[: 2 * n] = d.reshape(-1).view(torch.uint8)
+    wire[nd: nd + 4 * n] = c.reshape(-1).view(torch.uint8)
+    gather_list = [torch.empty_like(wire) for _ in range(world)] if rank == 0 else None
+    dist.gather(wire, gather_list, dst=0, group=group)
+    if rank != 0:
+        return None, None
+    H = bands[-1][1]
+    dout = torch.empty((H, w), dtype=torch.int16, device=d.device)
+    cout = torch.empty((H, w), dtype=torch.float32, device=d.device)
+    for g, (b0, b1) in zip(gather_list, bands):
+        m = (b1 - b0) * w
+        dout[b0:b1] = g[: 2 * m].view(torch.int16).view(b1 - b0, w)
+        cout[b0:b1] = g[nd: nd + 4 * m].view(torch.float32).view(b1 - b0, w)
+    return dout, cout

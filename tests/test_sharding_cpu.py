@@ -77,8 +77,12 @@ def _gather_worker(rank, world, port, q):
     full = torch.arange(h * w, dtype=torch.int16).reshape(h, w)
     out = sharding.gather_bands(full[b0:b1].clone(), bands, rank, world)
     costs = sharding.gather_bands(full[b0:b1].float() * 0.5, bands, rank, world)
+    # both maps in one collective (bench.py's C5 path); bands of unequal height
+    d2, c2 = sharding.gather_maps(full[b0:b1].clone(), full[b0:b1].float() * 0.25, bands,
+                                  rank, world)
     if rank == 0:
-        q.put((bool(torch.equal(out, full)), bool(torch.equal(costs, full.float() * 0.5))))
+        q.put((bool(torch.equal(out, full)), bool(torch.equal(costs, full.float() * 0.5)),
+               bool(torch.equal(d2, full)), bool(torch.equal(c2, full.float() * 0.25))))
     dist.barrier()
     dist.destroy_process_group()
 
@@ -93,4 +97,4 @@ def test_gather_bands_gloo_world2():
     for p in procs:
         p.join(timeout=120)
         assert p.exitcode == 0
-    assert q.get(timeout=10) == (True, True)
+    assert q.get(timeout=10) == (True, True, True, True)
