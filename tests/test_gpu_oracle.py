@@ -30,6 +30,9 @@ CASES = [
     (50, 40, 60, 1, 9, 2, "middlebury", 6),     # width < d_max
     (60, 90, 20, 1, 13, 1, "middlebury", 7),    # generic fallback kernel
     (128, 160, 16, 2, 7, 1, "middlebury", 8),
+    (72, 96, 24, 1, 7, 5, "paper", 9),          # radius 5: the 15-wide trusted-window path
+    (88, 100, 40, 2, 9, 4, "middlebury", 10),
+    (61, 77, 16, 1, 5, 2, "middlebury", 11),    # odd height: a lone last pixel row
 ]
 
 
