@@ -72,7 +72,11 @@ struct SweepArgs {
   int fix_nbx;
   // raw outputs (dense H x W): full, window, 3x3-summed winners
   int16_t* fz; float* fc; int16_t* wz; float* wcst; int16_t* nz; float* nc;
+  // set by launch_sweep4 (s4_plan): the lanes hold z in [0, s4_ze); s4_tail:
+  // z = d is evaluated once per tile after the sweep
+  int s4_ze, s4_tail;
 };
+
 cudaError_t launch_sweep(const SweepArgs& a, cudaStream_t s, int* n_launch);
 // whether launch_sweep runs sweep4 for these arguments; if so the caller must
 // also launch launch_sweep4_fixup (same inputs; may run concurrently)

@@ -86,7 +86,7 @@ __device__ __forceinline__ void fence_proxy_async() {
 }
 
 // Shared-memory layout (runtime TH, warps per pass and key slots).
-template <int B, int G = 2>
+template <int B, int G = 2, int ZZ = 1>
 struct S4Layout {
   static constexpr int NV = kTW + B + 1;        // V columns (TW + 2 cost columns + b - 1)
   static constexpr int NVP = (NV + 3) & ~3;     // row pitch (float4 broadcast loads)
@@ -97,8 +97,10 @@ struct S4Layout {
   __host__ __device__ S4Layout(int th_, int nw, int nzw_) : th(th_), nzw(nzw_) {
     // ring rows start 16-byte aligned in global memory: up to 3 (R) / 1 (Mp)
     // extra leading elements, and the copy is rounded up to 16 bytes
-    rwp = (NV + 32 * nw - 1 + 3 + 3 + 3) & ~3;
-    mwp = (NC + 32 * nw - 1 + 1 + 1 + 1) & ~1;
+    // (ZZ = 2: lanes read whole pairs from the even element at or below
+    // their first one, up to 2 more elements either side)
+    rwp = (NV + 32 * ZZ * nw - 1 + 3 + 3 + 3 + (ZZ > 1 ? 4 : 0)) & ~3;
+    mwp = (NC + 32 * ZZ * nw - 1 + 1 + 1 + 1 + (ZZ > 1 ? 4 : 0)) & ~1;
     size_t o = 0;
     o_bar = o; o += 16;   // the tile's row masks (sel, ref) + the ring's mbarrier
     o_pp = o; o += sizeof(float4) * (th + 2) * (NC / 2);
@@ -198,22 +200,120 @@ __device__ __forceinline__ void row_step(
   }
 }
 
-template <int B, int DIR, int G>
-__global__ void __launch_bounds__(kNWMax * 32, 2) sweep4_kernel(const SweepArgs a, const int th_) {
+// Two disparities per lane (ZZ = 2): lane l of warp w owns z0 = zlo + 2 l and
+// z0 + 1.  Adjacent disparities read adjacent right samples, so one LDS.64 /
+// LDS.128 per lane feeds both (half the shared-memory wavefronts per
+// evaluated disparity of the one-disparity layout), the broadcast L' / Pp
+// loads are shared, and the lane's two keys are merged before the REDUX.
+// Per (pixel, z) the arithmetic and its order are those of row_step, so the
+// results are bit-identical.  t-index of the value of column c for
+// disparity e of the lane: c + S + (DIR > 0 ? 1 - e : e), S = the parity pad
+// of the lane's first element (compile-time, see sweep4_kernel).
+template <int DIR>
+__device__ __forceinline__ constexpr int zoff(int e) { return DIR > 0 ? 1 - e : e; }
+
+template <int B, int DIR>
+__device__ __forceinline__ void row_step2(
+    const int k, const bool SEL, const bool REF, float (&V)[2][S4Layout<B>::NV],
+    float (&X)[2][kTW], float (&Y)[2][kTW], const float4* __restrict__ Pp,
+    const float4* __restrict__ mrow4, const float (&half)[2], const unsigned (&laneK)[2],
+    const bool lane0, unsigned* __restrict__ sk, unsigned* __restrict__ rk) {
+  using SL = S4Layout<B>;
+  constexpr int NC = SL::NC;
+  constexpr int sM = DIR > 0 ? 0 : 1;
+  constexpr int NT4 = (NC + 1 + sM + 1) / 2;
+  float cp[2][NC];
+#pragma unroll
+  for (int e = 0; e < 2; ++e) {
+    constexpr int M = NC / 2;
+    float a0 = 0.f, a1 = 0.f;
+#pragma unroll
+    for (int c = 0; c < B; ++c) a0 += V[e][c], a1 += V[e][M + c];
+    cp[e][0] = a0;
+    cp[e][M] = a1;
+#pragma unroll
+    for (int u = 1; u < M; ++u) {
+      a0 += V[e][u + B - 1] - V[e][u - 1];
+      a1 += V[e][M + u + B - 1] - V[e][M + u - 1];
+      cp[e][u] = a0;
+      cp[e][M + u] = a1;
+    }
+  }
+  float2 mt[2 * NT4];
+#pragma unroll
+  for (int i = 0; i < NT4; ++i) {
+    const float4 q = mrow4[i];
+    mt[2 * i] = make_float2(q.x, q.y);
+    mt[2 * i + 1] = make_float2(q.z, q.w);
+  }
+  const float4* prow = Pp + k * (NC / 2);
+#pragma unroll
+  for (int u2 = 0; u2 < NC / 2; ++u2) {
+    const float4 pp = prow[u2];
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const float2 m0 = mt[2 * u2 + sM + zoff<DIR>(e)], m1 = mt[2 * u2 + 1 + sM + zoff<DIR>(e)];
+      cp[e][2 * u2] = fma_sat(fmaf(-pp.x, m0.x, cp[e][2 * u2]) * pp.y, m0.y, half[e]);
+      cp[e][2 * u2 + 1] = fma_sat(fmaf(-pp.z, m1.x, cp[e][2 * u2 + 1]) * pp.w, m1.y, half[e]);
+    }
+  }
+  if (SEL) {
+    unsigned* srow = sk + (k - 1) * kTW;
+#pragma unroll
+    for (int p = 0; p < kTW; ++p) {
+      const unsigned k0 = (__float_as_uint(cp[0][p + 1] + 1.0f) << 6) + laneK[0];
+      const unsigned k1 = (__float_as_uint(cp[1][p + 1] + 1.0f) << 6) + laneK[1];
+      const unsigned r = __reduce_max_sync(kFull, max(k0, k1));
+      if (lane0) srow[p] = r;
+    }
+  }
+  unsigned* rrow = rk + (k - 2) * kTW;
+  if (REF) {
+#pragma unroll
+    for (int p = 0; p < kTW; ++p) {
+      unsigned key[2];
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const float h = (cp[e][p] + cp[e][p + 1]) + cp[e][p + 2];
+        const float n = Y[e][p] + h;
+        key[e] = (__float_as_uint(fmaf(n, 0.0625f, 1.0f)) << 6) + laneK[e];
+        Y[e][p] = X[e][p] + h;
+        X[e][p] = h;
+      }
+      const unsigned r = __reduce_max_sync(kFull, max(key[0], key[1]));
+      if (lane0) rrow[p] = r;
+    }
+  } else {
+#pragma unroll
+    for (int e = 0; e < 2; ++e)
+#pragma unroll
+      for (int p = 0; p < kTW; ++p) {
+        const float h = (cp[e][p] + cp[e][p + 1]) + cp[e][p + 2];
+        Y[e][p] = X[e][p] + h;
+        X[e][p] = h;
+      }
+  }
+}
+
+template <int B, int DIR, int G, int ZZ, int NWM, int REGS>
+__global__ void __launch_bounds__(NWM * 32) __maxnreg__(REGS) sweep4_kernel(const SweepArgs a, const int th_) {
   pdl_wait();
   const int th = th_;
-  using SL = S4Layout<B, G>;
+  using SL = S4Layout<B, G, ZZ>;
   constexpr int H2 = B / 2, NV = SL::NV, NVP = SL::NVP, NC = SL::NC, RB = SL::RB;
+  constexpr int ZW = 32 * ZZ;                 // disparities per warp
+  constexpr int SH = ZZ == 1 ? 5 : 6;         // key bits holding the warp-local z
   extern __shared__ float4 smem4[];
   char* smem = reinterpret_cast<char*>(smem4);
   const int nw = blockDim.x >> 5;
   const int d = a.d;
   // d a multiple of 32: the lanes cover z < d and the tail disparity z = d
   // (which would cost a whole warp with one useful lane) is evaluated once
-  // per tile after the sweep, as a separable box sum
-  const bool tail = (d & 31) == 0;
-  const int nz = tail ? d : d + 1;                          // disparities on lanes
-  const int nslot = ((nz + 32 * nw - 1) / (32 * nw)) * nw;  // passes x warps
+  // per tile after the sweep, as a separable box sum, when that saves a
+  // warp slot (the launcher's choice, s4_plan)
+  const bool tail = a.s4_tail != 0;
+  const int nz = a.s4_ze;                                     // disparities on lanes
+  const int nslot = ((nz + ZW * nw - 1) / (ZW * nw)) * nw;    // passes x warps
   const SL lay(th, nw, nslot);
   unsigned long long* bars = reinterpret_cast<unsigned long long*>(smem + lay.o_bar) + 1;
   unsigned* sK = reinterpret_cast<unsigned*>(smem + lay.o_sk);
@@ -231,45 +331,70 @@ __global__ void __launch_bounds__(kNWMax * 32, 2) sweep4_kernel(const SweepArgs 
   const int H = a.H, W = a.W;
   const float qnan = __int_as_float(0x7fc00000);
 
+  // ---- prologue.  Every global load it needs is issued before the first
+  // barrier (the guard flag, the pixel states, the left tile, 1/sigma_L), so
+  // the CTA pays one global-memory latency instead of four in a row.
+  //
   // Precision guard: the sliding sums multiply tile-centred values, so their
   // fp32 rounding error relative to the cost scales with the tile's
   // centring amplification (kernels.h Sweep4Guard, evaluated by the L
   // statistics kernel on the statistics branch).  Flagged tiles are left to the per-pixel-centred
   // sweep2 fixup launch (launch_sweep4_fixup), which may run concurrently.
-  if (a.tile_flags != nullptr &&
-      a.tile_flags[(int64_t)tile_row(y0, th) * a.flags_ld + blockIdx.x] != 0)
-    return;   // uniform: the whole CTA leaves
-  // ---- which output rows need what.  Pixel states (wc): kWcDone = trusted,
-  // not low, finished by prior_select_kernel; kWcLow = trusted and low: only
-  // the 3x3-summed refinement; kWcNone (or no prior) = untrusted: full-range
-  // selection + refinement.  masks[0] bit o: row o holds an untrusted pixel
-  // (SEL), masks[1] bit o: a pixel needing refinement (REF).  Rows outside
-  // the stage's rows need nothing.
-  if (tid < 2) masks[tid] = 0u;
-  __syncthreads();
-  for (int t = tid; t < th * kTW; t += nt) {
+  const unsigned flagged =
+      a.tile_flags != nullptr ? a.tile_flags[(int64_t)tile_row(y0, th) * a.flags_ld + blockIdx.x] : 0u;
+  // Pixel states (wc): kWcDone = trusted, not low, finished by
+  // prior_select_kernel; kWcLow = trusted and low: only the 3x3-summed
+  // refinement; kWcNone (or no prior) = untrusted: full-range selection +
+  // refinement.  Rows outside the stage's rows need nothing.
+  constexpr int kWcPer = 8;   // pixel states per thread held in registers
+  int wcv[kWcPer];
+  auto state = [&](int t) -> int {
     const int o = t / kTW, p = t - o * kTW;
     const int y = y0 + o, x = x0 + p;
-    if (y < a.rows.lo || y >= a.rows.hi || y >= H || x >= W) continue;
-    const int c = a.wc != nullptr ? a.wc[(int64_t)y * a.ldw + x] : kWcNone;
-    if (c == kWcNone) atomicOr(&masks[0], 1u << o);
-    if (c == kWcNone || c == kWcLow) atomicOr(&masks[1], 1u << o);
-  }
-  __syncthreads();
-  const unsigned selm = masks[0], refm = masks[1];
-  if ((selm | refm) == 0u) return;   // uniform: every pixel finished (or none here)
-  // ---- prologue: winner slots, left tile L' = L - cL
+    if (t >= th * kTW || y < a.rows.lo || y >= a.rows.hi || y >= H || x >= W) return kWcDone;
+    return a.wc != nullptr ? a.wc[(int64_t)y * a.ldw + x] : kWcNone;
+  };
+#pragma unroll
+  for (int i = 0; i < kWcPer; ++i) wcv[i] = state(tid + i * nt);
+  if (tid < 2) masks[tid] = 0u;
   if (tid == 0) mbar_init(bars, 1);
-  for (int t = tid; t < nslot * th * kTW; t += nt) sK[t] = 0u, rK[t] = 0u;
-  // centring constant: the L sample at the tile centre (the guard in the L
-  // statistics kernel uses the same one)
+  // left tile L' = L - cL; centring constant: the L sample at the tile centre
+  // (the guard in the L statistics kernel uses the same one)
   const double cL = a.Lv(clampi(y0 + th / 2, 0, H - 1), clampi(x0 + kTW / 2, 0, W - 1));
+#pragma unroll 4
   for (int t = tid; t < (th + B + 1) * NV; t += nt) {
     const int rr = t / NV, c = t - rr * NV;
     const int y = clampi(y0 - 1 - H2 + rr, 0, H - 1), x = clampi(x0 - 1 - H2 + c, 0, W - 1);
     Lt[rr * NVP + c] = (float)(a.Lv(y, x) - cL);
   }
+  // kL = 1/(b^2 sigma_L) per cost pixel (NaN: degenerate or outside the image)
+#pragma unroll 4
+  for (int t = tid; t < (th + 2) * NC; t += nt) {
+    const int k = t / NC, u = t - k * NC;
+    const int y = y0 - 1 + k, x = x0 - 1 + u;
+    float kL = qnan;
+    if (y >= 0 && y < H && x >= 0 && x < W) {
+      const float is = a.isL[(int64_t)y * a.lds + x];
+      if (is > 0.f) kL = is * (1.0f / (float)(B * B));
+    }
+    reinterpret_cast<float*>(Pp)[2 * t + 1] = kL;
+  }
+  for (int t = tid; t < nslot * th * kTW; t += nt) sK[t] = 0u, rK[t] = 0u;   // winner slots
+  if (flagged != 0u) return;   // uniform: the whole CTA leaves
   __syncthreads();
+  // masks[0] bit o: row o holds an untrusted pixel (SEL), masks[1] bit o: a
+  // pixel needing refinement (REF)
+  auto mark = [&](int t, int c) {
+    const int o = t / kTW;
+    if (c == kWcNone) atomicOr(&masks[0], 1u << o);
+    if (c == kWcNone || c == kWcLow) atomicOr(&masks[1], 1u << o);
+  };
+#pragma unroll
+  for (int i = 0; i < kWcPer; ++i) mark(tid + i * nt, wcv[i]);
+  for (int t = tid + kWcPer * nt; t < th * kTW; t += nt) mark(t, state(t));
+  __syncthreads();
+  const unsigned selm = masks[0], refm = masks[1];
+  if ((selm | refm) == 0u) return;   // uniform: every pixel finished (or none here)
   // cost row k (output row k - 1) is needed by SEL of row k - 1 and REF of
   // rows k - 2, k - 1, k; rows nobody needs skip the cost and reductions
   const unsigned long long needc = ((unsigned long long)selm << 1) |
@@ -297,35 +422,27 @@ __global__ void __launch_bounds__(kNWMax * 32, 2) sweep4_kernel(const SweepArgs 
   __syncthreads();
   for (int t = tid; t < (th + 2) * NC; t += nt) {
     const int k = t / NC, u = t - k * NC;
-    const int y = y0 - 1 + k, x = x0 - 1 + u;
     double s = 0.0;
 #pragma unroll
     for (int r = 0; r < B; ++r) s += Hs[(k + r) * NC + u];
-    float kL = qnan;
-    if (y >= 0 && y < H && x >= 0 && x < W) {
-      const float is = a.isL[(int64_t)y * a.lds + x];
-      if (is > 0.f) kL = is * (1.0f / (float)(B * B));
-    }
-    float* pf = reinterpret_cast<float*>(Pp) + 2 * t;
-    pf[0] = (float)s;
-    pf[1] = kL;
+    reinterpret_cast<float*>(Pp)[2 * t] = (float)s;
   }
   __syncthreads();   // Pp, Lt, the mbarriers
 
   const float* __restrict__ Rp = a.Rp + a.pc;
   const float2* __restrict__ Mp = a.Mp + a.pc;
   unsigned phase = 0;
-  for (int zp = 0, pass = 0; zp < nz; zp += 32 * nw, ++pass) {
+  for (int zp = 0, pass = 0; zp < nz; zp += ZW * nw, ++pass) {
     // warps of this pass that hold at least one z <= d
-    const int nwp = min(nw, (nz - 1 - zp) / 32 + 1);
-    const int zlo = zp + 32 * wp;
-    const int z = zlo + lane;
+    const int nwp = min(nw, (nz - 1 - zp) / ZW + 1);
+    const int zlo = zp + ZW * wp;
+    const int z = zlo + ZZ * lane;   // the lane's (first) disparity
     // every z of the warp has its right centre outside the image for every
     // cost column of the tile: costs are all -1 there, and lower warps hold
     // smaller z with costs >= -1, so skipping the warp is exact (its key
     // slots stay 0 = no candidate)
     const bool active = wp < nwp && (DIR > 0 ? (zlo <= x0 + kTW) : (zlo <= W - x0));
-    const int span = 32 * nwp - 1;
+    const int span = ZW * nwp - 1;
     // image column of ring element 0 (R ring: tile V columns, Mp ring: cost
     // columns), moved down to a 16-byte boundary of the padded row
     int rc0 = DIR > 0 ? (x0 - 1 - H2 - zp - span) : (x0 - 1 - H2 + zp);
@@ -335,9 +452,16 @@ __global__ void __launch_bounds__(kNWMax * 32, 2) sweep4_kernel(const SweepArgs 
     mc0 -= mmis;
     const unsigned rbytes = (unsigned)(((NV + span + rmis + 3) & ~3) * sizeof(float));
     const unsigned mbytes = (unsigned)(((NC + span + mmis + 1) & ~1) * sizeof(float2));
-    // lane base into the rings: element index of column c for this z
-    const int lb = (DIR > 0 ? (span - (z - zp)) : (z - zp)) + rmis;
-    const int mb = (DIR > 0 ? (span - (z - zp)) : (z - zp)) + mmis;
+    // lane base into the rings: element index of column c for this z.
+    // ZZ = 2: the lane's first element (that of z + 1 for DIR > 0) moved down
+    // to an even index, so whole pairs load with LDS.64 / LDS.128; the parity
+    // pads sR, sM are compile-time constants because x0, zp and the padding
+    // column a.pc are even
+    constexpr int sR = ZZ == 1 ? 0 : (DIR > 0 ? (H2 & 1) : ((H2 + 1) & 1));
+    constexpr int sM = ZZ == 1 ? 0 : (DIR > 0 ? 0 : 1);
+    const int lb = (DIR > 0 ? (span - (z - zp)) - (ZZ - 1) : (z - zp)) + rmis - sR;
+    const int mb = (DIR > 0 ? (span - (z - zp)) - (ZZ - 1) : (z - zp)) + mmis - sM;
+    if (ZZ > 1 && ((lb | mb) & 1)) __trap();
 
     auto stage_r = [&](int rr, unsigned long long* bar) {
       const int y = clampi(y0 - 1 - H2 + rr, 0, H - 1);
@@ -359,34 +483,72 @@ __global__ void __launch_bounds__(kNWMax * 32, 2) sweep4_kernel(const SweepArgs 
     mbar_wait(bars, phase & 1u);
     phase ^= 1u;
 
-    float V[NV];
+    float V[ZZ][NV];
+    constexpr int NT2 = (NV + 1 + sR + 1) / 2;   // ZZ = 2: float2 loads per ring row
+    // ring row -> the lane's NV + 1 (+ pad) consecutive samples
+    auto load_r = [&](const float* rowp, float (&t)[2 * NT2]) {
+      const float2* rp = reinterpret_cast<const float2*>(rowp + lb);
+#pragma unroll
+      for (int i = 0; i < NT2; ++i) {
+        const float2 v = rp[i];
+        t[2 * i] = v.x;
+        t[2 * i + 1] = v.y;
+      }
+    };
     if (active) {
 #pragma unroll
-      for (int c = 0; c < NV; ++c) V[c] = 0.f;
+      for (int e = 0; e < ZZ; ++e)
+#pragma unroll
+        for (int c = 0; c < NV; ++c) V[e][c] = 0.f;
 #pragma unroll
       for (int r = 0; r < B; ++r) {
         const float4* lr = reinterpret_cast<const float4*>(Lt + (k0 + r) * NVP);
-        const float* rrow = Rr + ((k0 + r) % RB) * lay.rwp + lb;
+        if constexpr (ZZ == 1) {
+          const float* rrow = Rr + ((k0 + r) % RB) * lay.rwp + lb;
 #pragma unroll
-        for (int c4 = 0; c4 < NVP / 4; ++c4) {
-          const float4 l4 = lr[c4];
-          const float lv[4] = {l4.x, l4.y, l4.z, l4.w};
+          for (int c4 = 0; c4 < NVP / 4; ++c4) {
+            const float4 l4 = lr[c4];
+            const float lv[4] = {l4.x, l4.y, l4.z, l4.w};
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const int c = 4 * c4 + e;
-            if (c < NV) V[c] = fmaf(lv[e], rrow[c], V[c]);
+            for (int e = 0; e < 4; ++e) {
+              const int c = 4 * c4 + e;
+              if (c < NV) V[0][c] = fmaf(lv[e], rrow[c], V[0][c]);
+            }
+          }
+        } else {
+          float t[2 * NT2];
+          load_r(Rr + ((k0 + r) % RB) * lay.rwp, t);
+#pragma unroll
+          for (int c4 = 0; c4 < NVP / 4; ++c4) {
+            const float4 l4 = lr[c4];
+            const float lv[4] = {l4.x, l4.y, l4.z, l4.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const int c = 4 * c4 + e;
+              if (c < NV) {
+                V[0][c] = fmaf(lv[e], t[c + sR + zoff<DIR>(0)], V[0][c]);
+                V[1][c] = fmaf(lv[e], t[c + sR + zoff<DIR>(1)], V[1][c]);
+              }
+            }
           }
         }
       }
     }
-    const unsigned laneK = (unsigned)(31 - lane) + 32u - (0x3F800000u << 5);
-    const float half = z < nz ? 0.5f : -1.0e30f;
-    const bool lane0 = lane == 0;
+    bool lane0 = lane == 0;
+    unsigned laneK[ZZ];
+    float half[ZZ];
+#pragma unroll
+    for (int e = 0; e < ZZ; ++e) {
+      laneK[e] = (unsigned)(ZW - 1 - (ZZ * lane + e)) + (1u << SH) - (0x3F800000u << SH);
+      half[e] = z + e < nz ? 0.5f : -1.0e30f;
+    }
     unsigned* sk = sK + (pass * nw + wp) * th * kTW;
     unsigned* rk = rK + (pass * nw + wp) * th * kTW;
-    float X[kTW], Y[kTW];
+    float X[ZZ][kTW], Y[ZZ][kTW];
 #pragma unroll
-    for (int p = 0; p < kTW; ++p) X[p] = 0.f, Y[p] = 0.f;
+    for (int e = 0; e < ZZ; ++e)
+#pragma unroll
+      for (int p = 0; p < kTW; ++p) X[e][p] = 0.f, Y[e][p] = 0.f;
 
     // Rows are consumed in groups of G steps: one mbarrier wait and one CTA
     // barrier per group; the ring holds the group's b + G R rows and G Mp
@@ -396,25 +558,51 @@ __global__ void __launch_bounds__(kNWMax * 32, 2) sweep4_kernel(const SweepArgs 
     auto step = [&](int k) {
       if (active) {
         if ((needc >> k) & 1ull) {
-          const float2* mrow = Mr + (k % (2 * G)) * lay.mwp + mb;
           const bool sl = k >= 1 && ((selm >> (k - 1)) & 1u);
           const bool rf = k >= 2 && ((refm >> (k - 2)) & 1u);
-          row_step<B>(k, sl, rf, V, X, Y, Pp, mrow, half, laneK, lane0, sk, rk);
+          const float2* mrow = Mr + (k % (2 * G)) * lay.mwp + mb;
+          if constexpr (ZZ == 1)
+            row_step<B>(k, sl, rf, V[0], X[0], Y[0], Pp, mrow, half[0], laneK[0], lane0, sk, rk);
+          else
+            row_step2<B, DIR>(k, sl, rf, V, X, Y, Pp, reinterpret_cast<const float4*>(mrow), half,
+                              laneK, lane0, sk, rk);
         }
         // slide V down one row: + row k + B, - row k
         if (k <= th) {
           const float4* lin = reinterpret_cast<const float4*>(Lt + (k + B) * NVP);
           const float4* lout = reinterpret_cast<const float4*>(Lt + k * NVP);
-          const float* rin = Rr + ((k + B) % RB) * lay.rwp + lb;
-          const float* rout = Rr + (k % RB) * lay.rwp + lb;
+          if constexpr (ZZ == 1) {
+            const float* rin = Rr + ((k + B) % RB) * lay.rwp + lb;
+            const float* rout = Rr + (k % RB) * lay.rwp + lb;
 #pragma unroll
-          for (int c4 = 0; c4 < NVP / 4; ++c4) {
-            const float4 i4 = lin[c4], o4 = lout[c4];
-            const float iv[4] = {i4.x, i4.y, i4.z, i4.w}, ov[4] = {o4.x, o4.y, o4.z, o4.w};
+            for (int c4 = 0; c4 < NVP / 4; ++c4) {
+              const float4 i4 = lin[c4], o4 = lout[c4];
+              const float iv[4] = {i4.x, i4.y, i4.z, i4.w}, ov[4] = {o4.x, o4.y, o4.z, o4.w};
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const int c = 4 * c4 + e;
-              if (c < NV) V[c] = fmaf(iv[e], rin[c], fmaf(-ov[e], rout[c], V[c]));
+              for (int e = 0; e < 4; ++e) {
+                const int c = 4 * c4 + e;
+                if (c < NV) V[0][c] = fmaf(iv[e], rin[c], fmaf(-ov[e], rout[c], V[0][c]));
+              }
+            }
+          } else {
+            float tin[2 * NT2], tout[2 * NT2];
+            load_r(Rr + ((k + B) % RB) * lay.rwp, tin);
+            load_r(Rr + (k % RB) * lay.rwp, tout);
+#pragma unroll
+            for (int c4 = 0; c4 < NVP / 4; ++c4) {
+              const float4 i4 = lin[c4], o4 = lout[c4];
+              const float iv[4] = {i4.x, i4.y, i4.z, i4.w}, ov[4] = {o4.x, o4.y, o4.z, o4.w};
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const int c = 4 * c4 + e;
+                if (c < NV) {
+#pragma unroll
+                  for (int q = 0; q < 2; ++q) {
+                    const int j = c + sR + zoff<DIR>(q);
+                    V[q][c] = fmaf(iv[e], tin[j], fmaf(-ov[e], tout[j], V[q][c]));
+                  }
+                }
+              }
             }
           }
         }
@@ -487,26 +675,26 @@ __global__ void __launch_bounds__(kNWMax * 32, 2) sweep4_kernel(const SweepArgs 
     int zs = -1, nbz = 0;
     for (int w = 0; w < nslot; ++w) {
       const unsigned ks = sK[w * th * kTW + t], kr = rK[w * th * kTW + t];
-      if ((ks >> 5) > (bs >> 5)) bs = ks, zs = 32 * w + 31 - (int)(ks & 31u);
-      if ((kr >> 5) > (br >> 5)) br = kr, nbz = 32 * w + 31 - (int)(kr & 31u);
+      if ((ks >> SH) > (bs >> SH)) bs = ks, zs = ZW * w + ZW - 1 - (int)(ks & (unsigned)(ZW - 1));
+      if ((kr >> SH) > (br >> SH)) br = kr, nbz = ZW * w + ZW - 1 - (int)(kr & (unsigned)(ZW - 1));
     }
     if (zs < 0) {
       // no candidate on an active warp: every right centre is outside the
       // image, all -1 (value 1), smallest z
-      bs = 1u << 5;
+      bs = 1u << SH;
       zs = 0;
     }
     if (tail) {   // z = d last: it wins only if strictly better
       const float* ct = Ct + o * NC + p;
       const unsigned vd = __float_as_uint(ct[NC + 1] + 1.0f) - 0x3F800000u + 1u;
-      if (vd > (bs >> 5)) bs = vd << 5, zs = d;
+      if (vd > (bs >> SH)) bs = vd << SH, zs = d;
       const float nsum = (((ct[0] + ct[1]) + ct[2]) + ((ct[NC] + ct[NC + 1]) + ct[NC + 2])) +
                          ((ct[2 * NC] + ct[2 * NC + 1]) + ct[2 * NC + 2]);
       const unsigned vn = __float_as_uint(fmaf(nsum, 0.0625f, 1.0f)) - 0x3F800000u + 1u;
-      if (vn > (br >> 5)) br = vn << 5, nbz = d;
+      if (vn > (br >> SH)) br = vn << SH, nbz = d;
     }
-    const float cs = 2.f * __uint_as_float((bs >> 5) - 1u + 0x3F800000u) - 3.f;  // c = 2 c' - 1
-    const float n1 = __uint_as_float((br >> 5) - 1u + 0x3F800000u);
+    const float cs = 2.f * __uint_as_float((bs >> SH) - 1u + 0x3F800000u) - 3.f;  // c = 2 c' - 1
+    const float n1 = __uint_as_float((br >> SH) - 1u + 0x3F800000u);
     const float nsum = (n1 - 1.0f) * 16.0f;
     const int members = ((i > 0) + 1 + (i < H - 1)) * ((j > 0) + 1 + (j < W - 1));
     const float nbc = 2.f * nsum / (float)members - 1.f;
@@ -702,26 +890,38 @@ cudaError_t launch_prior_select(const SweepArgs& a, int th, dim3 pg, cudaStream_
   }
 }
 
-template <int B, int DIR, int G>
-cudaError_t launch4(const SweepArgs& a, cudaStream_t s) {
+int env_int(const char* name, int dflt) {
+  const char* v = getenv(name);
+  return v ? atoi(v) : dflt;
+}
+
+// CTA shape for `nz` disparities on the lanes, `zw` per warp, <= nwmax warps
+// per CTA: passes x warps (the kernel's key slots)
+struct S4Shape {
+  int passes, nw;
+  int slots() const { return passes * nw; }
+};
+S4Shape s4_shape(int nz, int zw, int nwmax) {
+  const int nzw = (nz + zw - 1) / zw;
+  S4Shape r;
+  r.passes = (nzw + nwmax - 1) / nwmax;
+  r.nw = (nzw + r.passes - 1) / r.passes;
+  return r;
+}
+
+// NWM warps per CTA at most, REGS registers per thread at most
+template <int B, int DIR, int G, int ZZ, int NWM, int REGS>
+cudaError_t launch4(const SweepArgs& a, S4Shape sh, cudaStream_t s) {
   const int th = sweep4_th();
-  const int nzw = ((a.d & 31) == 0 ? a.d : a.d + 1 + 31) / 32;   // tail z = d off the lanes
-  const int passes = (nzw + kNWMax - 1) / kNWMax;
-  const int nw = (nzw + passes - 1) / passes;
-  const S4Layout<B, G> lay(th, nw, passes * nw);
+  const S4Layout<B, G, ZZ> lay(th, sh.nw, sh.slots());
   static SmemAttr attr;
-  if (cudaError_t e = attr.ensure(sweep4_kernel<B, DIR, G>, lay.bytes); e != cudaSuccess) return e;
-  if (a.wc != nullptr) {   // trusted windows first (prior_select_kernel)
-    dim3 pg((a.W + 31) / 32, (a.rows.hi - (a.rows.lo & ~1) + 15) / 16);
-    cudaError_t e = a.L32 != nullptr ? launch_prior_select<B, DIR, true>(a, th, pg, s)
-                                      : launch_prior_select<B, DIR, false>(a, th, pg, s);
-    if (e != cudaSuccess) return e;
-  }
+  if (cudaError_t e = attr.ensure(sweep4_kernel<B, DIR, G, ZZ, NWM, REGS>, lay.bytes); e != cudaSuccess)
+    return e;
   // CTA rows on the whole-image grid (row bands bit-identical to whole runs)
   SweepArgs b = a;
   b.rows.lo = tile_row(a.rows.lo, th) * th - kTileOff;
   dim3 grid((a.W + kTW - 1) / kTW, (b.rows.hi - b.rows.lo + th - 1) / th);
-  return launch_pdl(sweep4_kernel<B, DIR, G>, grid, dim3(32 * nw), lay.bytes, s, b, th);
+  return launch_pdl(sweep4_kernel<B, DIR, G, ZZ, NWM, REGS>, grid, dim3(32 * sh.nw), lay.bytes, s, b, th);
 }
 
 }  // namespace
@@ -737,6 +937,8 @@ bool sweep4_supported(const SweepArgs& a, bool force) {
          a.d <= 4095 && a.radius <= 7;   // prior_select_kernel: windows of <= 15
 }
 
+namespace {
+
 int g_group = -1;
 int sweep4_group() {
   if (g_group < 0) {
@@ -747,12 +949,75 @@ int sweep4_group() {
   return g_group;
 }
 
+int g_zz = -1;
+int sweep4_zz() {
+  if (g_zz < 0) {
+    g_zz = env_int("MSHBM_SWEEP4_ZZ", 0);   // disparities per lane (1 or 2; 0: by shape)
+    if (g_zz != 1 && g_zz != 2) g_zz = 0;
+  }
+  return g_zz;
+}
+
+// How launch_sweep4 lays the search range [0, d] out.  zz: disparities per
+// lane.  Two per lane (64 per warp, 168 registers: 3 warps per scheduler)
+// halve the shared-memory wavefronts per evaluated disparity and win when
+// the CTAs fill the SM's four schedulers evenly (2, 3 or 4 warps, <= 4 so
+// that 3 CTAs are resident) without idle lanes beyond what one disparity
+// per lane (32 per warp, 128 registers, <= 8 warps) would leave; measured:
+// C5 (d = 512) 41.7 -> 34.3 ms, C3 (d = 288, 4.5 warps of 64) no gain.
+// tail: z = d is evaluated once per tile after the sweep instead of on a
+// lane when it would be a warp's only disparity (d a multiple of the warp's
+// range).
+// Two per lane need even ring bases: padded rows (a.pc, a.ldp) in multiples
+// of 4 elements (prep_staging lays them out so).
+struct S4Plan {
+  int zz, tail, ze;
+  S4Shape shape;
+};
+S4Plan s4_plan(const SweepArgs& a) {
+  auto plan = [&](int zz, int nwmax) {
+    const int zw = 32 * zz;
+    S4Plan p;
+    p.zz = zz;
+    p.tail = a.d % zw == 0;   // z = d would take a warp of its own through a pass
+    p.ze = p.tail ? a.d : a.d + 1;
+    p.shape = s4_shape(p.ze, zw, nwmax);
+    return p;
+  };
+  static const int nw1 = max(1, min(8, env_int("MSHBM_SWEEP4_NW", 8)));
+  static const int nw2 = max(1, min(4, env_int("MSHBM_SWEEP4_NW", 4)));
+  const S4Plan p1 = plan(1, nw1), p2 = plan(2, nw2);
+  const bool even = (a.pc & 3) == 0 && (a.ldp & 3) == 0;
+  const int zz = sweep4_zz();   // 0: choose, 1 / 2: forced
+  const bool pick2 = zz == 2 || (zz == 0 && p2.shape.nw >= 2 &&
+                                 64 * p2.shape.slots() <= 32 * p1.shape.slots());
+  return even && pick2 ? p2 : p1;
+}
+
+template <int B, int DIR>
+cudaError_t launch4_d(const SweepArgs& a0, cudaStream_t s) {
+  const int th = sweep4_th();
+  if (a0.wc != nullptr) {   // trusted windows first (prior_select_kernel)
+    dim3 pg((a0.W + 31) / 32, (a0.rows.hi - (a0.rows.lo & ~1) + 15) / 16);
+    cudaError_t e = a0.L32 != nullptr ? launch_prior_select<B, DIR, true>(a0, th, pg, s)
+                                       : launch_prior_select<B, DIR, false>(a0, th, pg, s);
+    if (e != cudaSuccess) return e;
+  }
+  const S4Plan p = s4_plan(a0);
+  SweepArgs a = a0;
+  a.s4_tail = p.tail;
+  a.s4_ze = p.ze;
+  if (p.zz == 2) return launch4<B, DIR, 2, 2, 4, 168>(a, p.shape, s);
+  if (sweep4_group() == 2) return launch4<B, DIR, 2, 1, 8, 128>(a, p.shape, s);
+  return launch4<B, DIR, 4, 1, 8, 128>(a, p.shape, s);
+}
+
 template <int B>
 cudaError_t launch4_b(const SweepArgs& a, cudaStream_t s) {
-  const bool mb = a.dir > 0;
-  if (sweep4_group() == 2) return mb ? launch4<B, 1, 2>(a, s) : launch4<B, -1, 2>(a, s);
-  return mb ? launch4<B, 1, 4>(a, s) : launch4<B, -1, 4>(a, s);
+  return a.dir > 0 ? launch4_d<B, 1>(a, s) : launch4_d<B, -1>(a, s);
 }
+
+}  // namespace
 
 cudaError_t launch_sweep4(const SweepArgs& a, cudaStream_t s) {
   switch (a.block) {
