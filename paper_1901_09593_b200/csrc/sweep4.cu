@@ -43,6 +43,7 @@ namespace {
 constexpr unsigned kFull = 0xffffffffu;
 constexpr int kTW = 16;          // output columns per CTA
 constexpr int kNWMax = 8;        // warps (x 32 disparities) per CTA and pass
+constexpr int kSplitG = 8;       // row steps per CTA barrier of the column-split pass
 
 __device__ __forceinline__ float fma_sat(float a, float b, float c) {
   float r;
@@ -123,14 +124,17 @@ struct S4Layout {
 // stores the warp's key per pixel into sk); REF: 3x3-summed winner of
 // output row k - 2 (into rk).  Rows whose pixels need neither skip the
 // reductions (the tile's row masks, see sweep4_kernel).
-template <int B>
+// TWW: the warp's share of the tile's columns (kTW, or kTW / warps in a
+// column-split pass: the caller offsets Pp, mrow, sk, rk by the warp's first
+// column); SH: key bits holding the warp-local z.
+template <int B, int TWW, int SH>
 __device__ __forceinline__ void row_step(
-    const int k, const bool SEL, const bool REF, float (&V)[S4Layout<B>::NV], float (&X)[kTW],
-    float (&Y)[kTW], const float4* __restrict__ Pp, const float2* __restrict__ mrow,
+    const int k, const bool SEL, const bool REF, float (&V)[TWW + B + 1], float (&X)[TWW],
+    float (&Y)[TWW], const float4* __restrict__ Pp, const float2* __restrict__ mrow,
     const float half, const unsigned laneK, const bool lane0, unsigned* __restrict__ sk,
     unsigned* __restrict__ rk) {
   using SL = S4Layout<B>;
-  constexpr int NC = SL::NC;
+  constexpr int NC = TWW + 2;
   // horizontal window sums S[u] = V[u] + ... + V[u + B - 1]: sliding, as two
   // independent chains (u < NC/2 from S[0], u >= NC/2 from S[NC/2]) over the
   // differences D[u] = V[u + B - 1] - V[u - 1], so the dependent FADD chain is
@@ -156,7 +160,7 @@ __device__ __forceinline__ void row_step(
   // image) saturates to 0, i.e. c = -1; out-of-image pixels read 0 in 3x3
   // sums.  Lanes with z > d use half = -1e30, so their c' is 0 as well: they
   // never beat a smaller z (ties go to the smaller z) and need no mask.
-  const float4* prow = Pp + k * (NC / 2);
+  const float4* prow = Pp + k * (SL::NC / 2);
 #pragma unroll
   for (int u2 = 0; u2 < NC / 2; ++u2) {
     const float4 pp = prow[u2];   // (sumL', kL) of cost columns 2 u2 and 2 u2 + 1
@@ -165,13 +169,13 @@ __device__ __forceinline__ void row_step(
     cp[2 * u2 + 1] = fma_sat(fmaf(-pp.z, m1.x, cp[2 * u2 + 1]) * pp.w, m1.y, half);
   }
   // selection (untrusted pixels: the full range [0, d], no window mask):
-  // key = (bits(c' + 1) - 0x3F800000 + 1) << 5 | (31 - lane), REDUX.MAX = the
-  // warp's first maximum
+  // key = (bits(c' + 1) - 0x3F800000 + 1) << SH | (2^SH - 1 - local z),
+  // REDUX.MAX = the warp's first maximum
   if (SEL) {
     unsigned* srow = sk + (k - 1) * kTW;
 #pragma unroll
-    for (int p = 0; p < kTW; ++p) {
-      const unsigned key = (__float_as_uint(cp[p + 1] + 1.0f) << 5) + laneK;
+    for (int p = 0; p < TWW; ++p) {
+      const unsigned key = (__float_as_uint(cp[p + 1] + 1.0f) << SH) + laneK;
       const unsigned r = __reduce_max_sync(kFull, key);
       if (lane0) srow[p] = r;
     }
@@ -181,10 +185,10 @@ __device__ __forceinline__ void row_step(
   unsigned* rrow = rk + (k - 2) * kTW;
   if (REF) {
 #pragma unroll
-    for (int p = 0; p < kTW; ++p) {
+    for (int p = 0; p < TWW; ++p) {
       const float h = (cp[p] + cp[p + 1]) + cp[p + 2];
       const float n = Y[p] + h;
-      const unsigned key = (__float_as_uint(fmaf(n, 0.0625f, 1.0f)) << 5) + laneK;
+      const unsigned key = (__float_as_uint(fmaf(n, 0.0625f, 1.0f)) << SH) + laneK;
       const unsigned r = __reduce_max_sync(kFull, key);
       if (lane0) rrow[p] = r;
       Y[p] = X[p] + h;
@@ -192,7 +196,7 @@ __device__ __forceinline__ void row_step(
     }
   } else {
 #pragma unroll
-    for (int p = 0; p < kTW; ++p) {
+    for (int p = 0; p < TWW; ++p) {
       const float h = (cp[p] + cp[p + 1]) + cp[p + 2];
       Y[p] = X[p] + h;
       X[p] = h;
@@ -312,8 +316,11 @@ __global__ void __launch_bounds__(NWM * 32) __maxnreg__(REGS) sweep4_kernel(cons
   // per tile after the sweep, as a separable box sum, when that saves a
   // warp slot (the launcher's choice, s4_plan)
   const bool tail = a.s4_tail != 0;
-  const int nz = a.s4_ze;                                     // disparities on lanes
-  const int nslot = ((nz + ZW * nw - 1) / (ZW * nw)) * nw;    // passes x warps
+  const int nz = a.s4_ze;    // disparities on lanes: [0, nz)
+  // [0, nzm) on the warps' own lanes (ZZ each); the rest, if any, in a
+  // column-split pass of all warps (run_pass below), one more key slot
+  const int nzm = a.s4_zm;
+  const int nslot = ((nzm + ZW * nw - 1) / (ZW * nw)) * nw + (nzm < nz ? 1 : 0);
   const SL lay(th, nw, nslot);
   unsigned long long* bars = reinterpret_cast<unsigned long long*>(smem + lay.o_bar) + 1;
   unsigned* sK = reinterpret_cast<unsigned*>(smem + lay.o_sk);
@@ -331,44 +338,46 @@ __global__ void __launch_bounds__(NWM * 32) __maxnreg__(REGS) sweep4_kernel(cons
   const int H = a.H, W = a.W;
   const float qnan = __int_as_float(0x7fc00000);
 
-  // ---- prologue.  Every global load it needs is issued before the first
-  // barrier (the guard flag, the pixel states, the left tile, 1/sigma_L), so
-  // the CTA pays one global-memory latency instead of four in a row.
-  //
   // Precision guard: the sliding sums multiply tile-centred values, so their
   // fp32 rounding error relative to the cost scales with the tile's
   // centring amplification (kernels.h Sweep4Guard, evaluated by the L
   // statistics kernel on the statistics branch).  Flagged tiles are left to the per-pixel-centred
   // sweep2 fixup launch (launch_sweep4_fixup), which may run concurrently.
-  const unsigned flagged =
-      a.tile_flags != nullptr ? a.tile_flags[(int64_t)tile_row(y0, th) * a.flags_ld + blockIdx.x] : 0u;
-  // Pixel states (wc): kWcDone = trusted, not low, finished by
-  // prior_select_kernel; kWcLow = trusted and low: only the 3x3-summed
-  // refinement; kWcNone (or no prior) = untrusted: full-range selection +
-  // refinement.  Rows outside the stage's rows need nothing.
-  constexpr int kWcPer = 8;   // pixel states per thread held in registers
-  int wcv[kWcPer];
-  auto state = [&](int t) -> int {
+  if (a.tile_flags != nullptr &&
+      a.tile_flags[(int64_t)tile_row(y0, th) * a.flags_ld + blockIdx.x] != 0)
+    return;   // uniform: the whole CTA leaves
+  // ---- which output rows need what.  Pixel states (wc): kWcDone = trusted,
+  // not low, finished by prior_select_kernel; kWcLow = trusted and low: only
+  // the 3x3-summed refinement; kWcNone (or no prior) = untrusted: full-range
+  // selection + refinement.  masks[0] bit o: row o holds an untrusted pixel
+  // (SEL), masks[1] bit o: a pixel needing refinement (REF).  Rows outside
+  // the stage's rows need nothing.
+  if (tid < 2) masks[tid] = 0u;
+  __syncthreads();
+  for (int t = tid; t < th * kTW; t += nt) {
     const int o = t / kTW, p = t - o * kTW;
     const int y = y0 + o, x = x0 + p;
-    if (t >= th * kTW || y < a.rows.lo || y >= a.rows.hi || y >= H || x >= W) return kWcDone;
-    return a.wc != nullptr ? a.wc[(int64_t)y * a.ldw + x] : kWcNone;
-  };
-#pragma unroll
-  for (int i = 0; i < kWcPer; ++i) wcv[i] = state(tid + i * nt);
-  if (tid < 2) masks[tid] = 0u;
+    if (y < a.rows.lo || y >= a.rows.hi || y >= H || x >= W) continue;
+    const int c = a.wc != nullptr ? a.wc[(int64_t)y * a.ldw + x] : kWcNone;
+    if (c == kWcNone) atomicOr(&masks[0], 1u << o);
+    if (c == kWcNone || c == kWcLow) atomicOr(&masks[1], 1u << o);
+  }
+  __syncthreads();
+  const unsigned selm = masks[0], refm = masks[1];
+  if ((selm | refm) == 0u) return;   // uniform: every pixel finished (or none here)
+  // ---- prologue: winner slots, left tile L' = L - cL, kL = 1/(b^2 sigma_L)
+  // per cost pixel (NaN: degenerate or outside the image); the global loads
+  // of both in one phase
   if (tid == 0) mbar_init(bars, 1);
-  // left tile L' = L - cL; centring constant: the L sample at the tile centre
-  // (the guard in the L statistics kernel uses the same one)
+  for (int t = tid; t < nslot * th * kTW; t += nt) sK[t] = 0u, rK[t] = 0u;
+  // centring constant: the L sample at the tile centre (the guard in the L
+  // statistics kernel uses the same one)
   const double cL = a.Lv(clampi(y0 + th / 2, 0, H - 1), clampi(x0 + kTW / 2, 0, W - 1));
-#pragma unroll 4
   for (int t = tid; t < (th + B + 1) * NV; t += nt) {
     const int rr = t / NV, c = t - rr * NV;
     const int y = clampi(y0 - 1 - H2 + rr, 0, H - 1), x = clampi(x0 - 1 - H2 + c, 0, W - 1);
     Lt[rr * NVP + c] = (float)(a.Lv(y, x) - cL);
   }
-  // kL = 1/(b^2 sigma_L) per cost pixel (NaN: degenerate or outside the image)
-#pragma unroll 4
   for (int t = tid; t < (th + 2) * NC; t += nt) {
     const int k = t / NC, u = t - k * NC;
     const int y = y0 - 1 + k, x = x0 - 1 + u;
@@ -379,22 +388,7 @@ __global__ void __launch_bounds__(NWM * 32) __maxnreg__(REGS) sweep4_kernel(cons
     }
     reinterpret_cast<float*>(Pp)[2 * t + 1] = kL;
   }
-  for (int t = tid; t < nslot * th * kTW; t += nt) sK[t] = 0u, rK[t] = 0u;   // winner slots
-  if (flagged != 0u) return;   // uniform: the whole CTA leaves
   __syncthreads();
-  // masks[0] bit o: row o holds an untrusted pixel (SEL), masks[1] bit o: a
-  // pixel needing refinement (REF)
-  auto mark = [&](int t, int c) {
-    const int o = t / kTW;
-    if (c == kWcNone) atomicOr(&masks[0], 1u << o);
-    if (c == kWcNone || c == kWcLow) atomicOr(&masks[1], 1u << o);
-  };
-#pragma unroll
-  for (int i = 0; i < kWcPer; ++i) mark(tid + i * nt, wcv[i]);
-  for (int t = tid + kWcPer * nt; t < th * kTW; t += nt) mark(t, state(t));
-  __syncthreads();
-  const unsigned selm = masks[0], refm = masks[1];
-  if ((selm | refm) == 0u) return;   // uniform: every pixel finished (or none here)
   // cost row k (output row k - 1) is needed by SEL of row k - 1 and REF of
   // rows k - 2, k - 1, k; rows nobody needs skip the cost and reductions
   const unsigned long long needc = ((unsigned long long)selm << 1) |
@@ -432,17 +426,31 @@ __global__ void __launch_bounds__(NWM * 32) __maxnreg__(REGS) sweep4_kernel(cons
   const float* __restrict__ Rp = a.Rp + a.pc;
   const float2* __restrict__ Mp = a.Mp + a.pc;
   unsigned phase = 0;
-  for (int zp = 0, pass = 0; zp < nz; zp += ZW * nw, ++pass) {
-    // warps of this pass that hold at least one z <= d
-    const int nwp = min(nw, (nz - 1 - zp) / ZW + 1);
-    const int zlo = zp + ZW * wp;
-    const int z = zlo + ZZ * lane;   // the lane's (first) disparity
+  // One pass over the tile's rows for the disparities [zp, zp + ZWp * nwp) on
+  // the lanes of nwp warps, ZZp per lane; winners into key slot `slot0 + wp`.
+  // TWW = kTW: every warp sweeps the whole tile width for its own 32 ZZp
+  // disparities.  TWW < kTW (column split, ZZp = 1, nwp = 1): all warps hold
+  // the same 32 disparities and each sweeps kTW / nw of the tile's columns:
+  // the rest of a search range that does not fill another warp, without an
+  // idle warp or a pass of one.
+  auto run_pass = [&](auto zz_c, auto tww_c, auto g_c, const int zp, const int nwp,
+                      const int slot0, const bool first) {
+    constexpr int ZZp = decltype(zz_c)::value, TWW = decltype(tww_c)::value;
+    // GP row steps per CTA barrier, ring rows RBp (the split pass's rows are short:
+    // more of them fit the same rings, so it synchronises less often)
+    constexpr int GP = decltype(g_c)::value, RBp = B + 2 * GP;
+    constexpr int ZWp = 32 * ZZp, SHp = SH;   // keys always in the kernel's format
+    constexpr bool kSplit = TWW < kTW;
+    constexpr int NVW = TWW + B + 1, NV4 = (NVW + 3) / 4;
+    const int col0 = kSplit ? TWW * wp : 0;   // the warp's first tile column
+    const int zlo = kSplit ? zp : zp + ZWp * wp;
+    const int z = zlo + ZZp * lane;   // the lane's (first) disparity
     // every z of the warp has its right centre outside the image for every
     // cost column of the tile: costs are all -1 there, and lower warps hold
     // smaller z with costs >= -1, so skipping the warp is exact (its key
     // slots stay 0 = no candidate)
-    const bool active = wp < nwp && (DIR > 0 ? (zlo <= x0 + kTW) : (zlo <= W - x0));
-    const int span = ZW * nwp - 1;
+    const bool active = (kSplit || wp < nwp) && (DIR > 0 ? (zlo <= x0 + kTW) : (zlo <= W - x0));
+    const int span = ZWp * nwp - 1;
     // image column of ring element 0 (R ring: tile V columns, Mp ring: cost
     // columns), moved down to a 16-byte boundary of the padded row
     int rc0 = DIR > 0 ? (x0 - 1 - H2 - zp - span) : (x0 - 1 - H2 + zp);
@@ -450,32 +458,35 @@ __global__ void __launch_bounds__(NWM * 32) __maxnreg__(REGS) sweep4_kernel(cons
     const int rmis = (a.pc + rc0) & 3, mmis = (a.pc + mc0) & 1;
     rc0 -= rmis;
     mc0 -= mmis;
+    // ring row pitches of this pass (the layout's for the warps' own passes)
+    const int rwp = kSplit ? ((NV + span + 3 + 3 + 3) & ~3) : lay.rwp;
+    const int mwp = kSplit ? ((NC + span + 1 + 1 + 1) & ~1) : lay.mwp;
     const unsigned rbytes = (unsigned)(((NV + span + rmis + 3) & ~3) * sizeof(float));
     const unsigned mbytes = (unsigned)(((NC + span + mmis + 1) & ~1) * sizeof(float2));
     // lane base into the rings: element index of column c for this z.
-    // ZZ = 2: the lane's first element (that of z + 1 for DIR > 0) moved down
+    // ZZp = 2: the lane's first element (that of z + 1 for DIR > 0) moved down
     // to an even index, so whole pairs load with LDS.64 / LDS.128; the parity
     // pads sR, sM are compile-time constants because x0, zp and the padding
     // column a.pc are even
-    constexpr int sR = ZZ == 1 ? 0 : (DIR > 0 ? (H2 & 1) : ((H2 + 1) & 1));
-    constexpr int sM = ZZ == 1 ? 0 : (DIR > 0 ? 0 : 1);
-    const int lb = (DIR > 0 ? (span - (z - zp)) - (ZZ - 1) : (z - zp)) + rmis - sR;
-    const int mb = (DIR > 0 ? (span - (z - zp)) - (ZZ - 1) : (z - zp)) + mmis - sM;
-    if (ZZ > 1 && ((lb | mb) & 1)) __trap();
+    constexpr int sR = ZZp == 1 ? 0 : (DIR > 0 ? (H2 & 1) : ((H2 + 1) & 1));
+    constexpr int sM = ZZp == 1 ? 0 : (DIR > 0 ? 0 : 1);
+    const int lb = (DIR > 0 ? (span - (z - zp)) - (ZZp - 1) : (z - zp)) + rmis - sR + col0;
+    const int mb = (DIR > 0 ? (span - (z - zp)) - (ZZp - 1) : (z - zp)) + mmis - sM + col0;
+    if (ZZp > 1 && ((lb | mb) & 1)) __trap();
 
     auto stage_r = [&](int rr, unsigned long long* bar) {
       const int y = clampi(y0 - 1 - H2 + rr, 0, H - 1);
-      bulk_g2s(Rr + (rr % RB) * lay.rwp, Rp + ((int64_t)y * a.ldp + rc0), rbytes, bar);
+      bulk_g2s(Rr + (rr % RBp) * rwp, Rp + ((int64_t)y * a.ldp + rc0), rbytes, bar);
     };
     auto stage_m = [&](int k, unsigned long long* bar) {
       const int y = clampi(y0 - 1 + k, 0, H - 1);
-      bulk_g2s(Mr + (k % (2 * G)) * lay.mwp, Mp + ((int64_t)y * a.ldp + mc0), mbytes, bar);
+      bulk_g2s(Mr + (k % (2 * GP)) * mwp, Mp + ((int64_t)y * a.ldp + mc0), mbytes, bar);
     };
-    if (pass > 0) __syncthreads();   // previous pass done with the rings
+    if (!first) __syncthreads();   // previous pass done with the rings
 
     if (tid == 0) {
       fence_proxy_async();
-      const int nr0 = min(B + G, th + B + 1 - k0), nm0 = min(G, th + 2 - k0);
+      const int nr0 = min(B + GP, th + B + 1 - k0), nm0 = min(GP, th + 2 - k0);
       mbar_expect_tx(bars, nr0 * rbytes + nm0 * mbytes);
       for (int rr = k0; rr < k0 + nr0; ++rr) stage_r(rr, bars);
       for (int k = k0; k < k0 + nm0; ++k) stage_m(k, bars);
@@ -483,8 +494,8 @@ __global__ void __launch_bounds__(NWM * 32) __maxnreg__(REGS) sweep4_kernel(cons
     mbar_wait(bars, phase & 1u);
     phase ^= 1u;
 
-    float V[ZZ][NV];
-    constexpr int NT2 = (NV + 1 + sR + 1) / 2;   // ZZ = 2: float2 loads per ring row
+    float V[ZZp][NVW];
+    constexpr int NT2 = (NVW + 1 + sR + 1) / 2;   // ZZp = 2: float2 loads per ring row
     // ring row -> the lane's NV + 1 (+ pad) consecutive samples
     auto load_r = [&](const float* rowp, float (&t)[2 * NT2]) {
       const float2* rp = reinterpret_cast<const float2*>(rowp + lb);
@@ -495,60 +506,62 @@ __global__ void __launch_bounds__(NWM * 32) __maxnreg__(REGS) sweep4_kernel(cons
         t[2 * i + 1] = v.y;
       }
     };
-    if (active) {
+    // V[.][c] += sign * L'(row, c) * R'(ring row, c -+ z) over the warp's columns
+    auto accum = [&](int lrow, int ring_row) {
+      const float4* lr = reinterpret_cast<const float4*>(Lt + lrow * NVP + col0);
+      if constexpr (ZZp == 1) {
+        const float* rrow = Rr + ring_row * rwp + lb;
 #pragma unroll
-      for (int e = 0; e < ZZ; ++e)
+        for (int c4 = 0; c4 < NV4; ++c4) {
+          const float4 l4 = lr[c4];
+          const float lv[4] = {l4.x, l4.y, l4.z, l4.w};
 #pragma unroll
-        for (int c = 0; c < NV; ++c) V[e][c] = 0.f;
-#pragma unroll
-      for (int r = 0; r < B; ++r) {
-        const float4* lr = reinterpret_cast<const float4*>(Lt + (k0 + r) * NVP);
-        if constexpr (ZZ == 1) {
-          const float* rrow = Rr + ((k0 + r) % RB) * lay.rwp + lb;
-#pragma unroll
-          for (int c4 = 0; c4 < NVP / 4; ++c4) {
-            const float4 l4 = lr[c4];
-            const float lv[4] = {l4.x, l4.y, l4.z, l4.w};
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const int c = 4 * c4 + e;
-              if (c < NV) V[0][c] = fmaf(lv[e], rrow[c], V[0][c]);
-            }
+          for (int e = 0; e < 4; ++e) {
+            const int c = 4 * c4 + e;
+            if (c < NVW) V[0][c] = fmaf(lv[e], rrow[c], V[0][c]);
           }
-        } else {
-          float t[2 * NT2];
-          load_r(Rr + ((k0 + r) % RB) * lay.rwp, t);
+        }
+      } else {
+        float t[2 * NT2];
+        load_r(Rr + ring_row * rwp, t);
 #pragma unroll
-          for (int c4 = 0; c4 < NVP / 4; ++c4) {
-            const float4 l4 = lr[c4];
-            const float lv[4] = {l4.x, l4.y, l4.z, l4.w};
+        for (int c4 = 0; c4 < NV4; ++c4) {
+          const float4 l4 = lr[c4];
+          const float lv[4] = {l4.x, l4.y, l4.z, l4.w};
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const int c = 4 * c4 + e;
-              if (c < NV) {
-                V[0][c] = fmaf(lv[e], t[c + sR + zoff<DIR>(0)], V[0][c]);
-                V[1][c] = fmaf(lv[e], t[c + sR + zoff<DIR>(1)], V[1][c]);
-              }
+          for (int e = 0; e < 4; ++e) {
+            const int c = 4 * c4 + e;
+            if (c < NVW) {
+              V[0][c] = fmaf(lv[e], t[c + sR + zoff<DIR>(0)], V[0][c]);
+              V[1][c] = fmaf(lv[e], t[c + sR + zoff<DIR>(1)], V[1][c]);
             }
           }
         }
       }
-    }
-    bool lane0 = lane == 0;
-    unsigned laneK[ZZ];
-    float half[ZZ];
+    };
+    if (active) {
 #pragma unroll
-    for (int e = 0; e < ZZ; ++e) {
-      laneK[e] = (unsigned)(ZW - 1 - (ZZ * lane + e)) + (1u << SH) - (0x3F800000u << SH);
+      for (int e = 0; e < ZZp; ++e)
+#pragma unroll
+        for (int c = 0; c < NVW; ++c) V[e][c] = 0.f;
+#pragma unroll
+      for (int r = 0; r < B; ++r) accum(k0 + r, (k0 + r) % RBp);
+    }
+    const bool lane0 = lane == 0;
+    unsigned laneK[ZZp];
+    float half[ZZp];
+#pragma unroll
+    for (int e = 0; e < ZZp; ++e) {
+      laneK[e] = (unsigned)(ZW - 1 - (ZZp * lane + e)) + (1u << SHp) - (0x3F800000u << SHp);
       half[e] = z + e < nz ? 0.5f : -1.0e30f;
     }
-    unsigned* sk = sK + (pass * nw + wp) * th * kTW;
-    unsigned* rk = rK + (pass * nw + wp) * th * kTW;
-    float X[ZZ][kTW], Y[ZZ][kTW];
+    unsigned* sk = sK + (slot0 + (kSplit ? 0 : wp)) * th * kTW + col0;
+    unsigned* rk = rK + (slot0 + (kSplit ? 0 : wp)) * th * kTW + col0;
+    float X[ZZp][TWW], Y[ZZp][TWW];
 #pragma unroll
-    for (int e = 0; e < ZZ; ++e)
+    for (int e = 0; e < ZZp; ++e)
 #pragma unroll
-      for (int p = 0; p < kTW; ++p) X[e][p] = 0.f, Y[e][p] = 0.f;
+      for (int p = 0; p < TWW; ++p) X[e][p] = 0.f, Y[e][p] = 0.f;
 
     // Rows are consumed in groups of G steps: one mbarrier wait and one CTA
     // barrier per group; the ring holds the group's b + G R rows and G Mp
@@ -560,42 +573,43 @@ __global__ void __launch_bounds__(NWM * 32) __maxnreg__(REGS) sweep4_kernel(cons
         if ((needc >> k) & 1ull) {
           const bool sl = k >= 1 && ((selm >> (k - 1)) & 1u);
           const bool rf = k >= 2 && ((refm >> (k - 2)) & 1u);
-          const float2* mrow = Mr + (k % (2 * G)) * lay.mwp + mb;
-          if constexpr (ZZ == 1)
-            row_step<B>(k, sl, rf, V[0], X[0], Y[0], Pp, mrow, half[0], laneK[0], lane0, sk, rk);
+          const float2* mrow = Mr + (k % (2 * GP)) * mwp + mb;
+          if constexpr (ZZp == 1)
+            row_step<B, TWW, SHp>(k, sl, rf, V[0], X[0], Y[0], Pp + col0 / 2, mrow, half[0],
+                                  laneK[0], lane0, sk, rk);
           else
             row_step2<B, DIR>(k, sl, rf, V, X, Y, Pp, reinterpret_cast<const float4*>(mrow), half,
                               laneK, lane0, sk, rk);
         }
         // slide V down one row: + row k + B, - row k
         if (k <= th) {
-          const float4* lin = reinterpret_cast<const float4*>(Lt + (k + B) * NVP);
-          const float4* lout = reinterpret_cast<const float4*>(Lt + k * NVP);
-          if constexpr (ZZ == 1) {
-            const float* rin = Rr + ((k + B) % RB) * lay.rwp + lb;
-            const float* rout = Rr + (k % RB) * lay.rwp + lb;
+          const float4* lin = reinterpret_cast<const float4*>(Lt + (k + B) * NVP + col0);
+          const float4* lout = reinterpret_cast<const float4*>(Lt + k * NVP + col0);
+          if constexpr (ZZp == 1) {
+            const float* rin = Rr + ((k + B) % RBp) * rwp + lb;
+            const float* rout = Rr + (k % RBp) * rwp + lb;
 #pragma unroll
-            for (int c4 = 0; c4 < NVP / 4; ++c4) {
+            for (int c4 = 0; c4 < NV4; ++c4) {
               const float4 i4 = lin[c4], o4 = lout[c4];
               const float iv[4] = {i4.x, i4.y, i4.z, i4.w}, ov[4] = {o4.x, o4.y, o4.z, o4.w};
 #pragma unroll
               for (int e = 0; e < 4; ++e) {
                 const int c = 4 * c4 + e;
-                if (c < NV) V[0][c] = fmaf(iv[e], rin[c], fmaf(-ov[e], rout[c], V[0][c]));
+                if (c < NVW) V[0][c] = fmaf(iv[e], rin[c], fmaf(-ov[e], rout[c], V[0][c]));
               }
             }
           } else {
             float tin[2 * NT2], tout[2 * NT2];
-            load_r(Rr + ((k + B) % RB) * lay.rwp, tin);
-            load_r(Rr + (k % RB) * lay.rwp, tout);
+            load_r(Rr + ((k + B) % RBp) * rwp, tin);
+            load_r(Rr + (k % RBp) * rwp, tout);
 #pragma unroll
-            for (int c4 = 0; c4 < NVP / 4; ++c4) {
+            for (int c4 = 0; c4 < NV4; ++c4) {
               const float4 i4 = lin[c4], o4 = lout[c4];
               const float iv[4] = {i4.x, i4.y, i4.z, i4.w}, ov[4] = {o4.x, o4.y, o4.z, o4.w};
 #pragma unroll
               for (int e = 0; e < 4; ++e) {
                 const int c = 4 * c4 + e;
-                if (c < NV) {
+                if (c < NVW) {
 #pragma unroll
                   for (int q = 0; q < 2; ++q) {
                     const int j = c + sR + zoff<DIR>(q);
@@ -609,25 +623,38 @@ __global__ void __launch_bounds__(NWM * 32) __maxnreg__(REGS) sweep4_kernel(cons
       }
     };
 #pragma unroll 1
-    for (int k = k0; k < kend; k += G) {
+    for (int k = k0; k < kend; k += GP) {
       if (k > k0) {
         mbar_wait(bars, phase & 1u);
         phase ^= 1u;
         __syncthreads();   // every warp done with the previous group (its slots are reused)
       }
-      if (tid == 0 && k + G < kend) {
+      if (tid == 0 && k + GP < kend) {
         fence_proxy_async();
-        const int r0 = k + B + G, r1 = min(k + B + 2 * G, th + B + 1);
-        const int m0 = k + G, m1 = min(k + 2 * G, th + 2);
+        const int r0 = k + B + GP, r1 = min(k + B + 2 * GP, th + B + 1);
+        const int m0 = k + GP, m1 = min(k + 2 * GP, th + 2);
         mbar_expect_tx(bars, max(r1 - r0, 0) * rbytes + (m1 - m0) * mbytes);
         for (int rr = r0; rr < r1; ++rr) stage_r(rr, bars);
         for (int km = m0; km < m1; ++km) stage_m(km, bars);
       }
 #pragma unroll 1
-      for (int g = 0; g < G; ++g) {
+      for (int g = 0; g < GP; ++g) {
         if (k + g < kend) step(k + g);
       }
     }
+  };
+  using std::integral_constant;
+  // the warps' own disparities: [0, nzm), ZZ per lane
+  int pass = 0;
+  for (int zp = 0; zp < nzm; zp += ZW * nw, ++pass)
+    run_pass(integral_constant<int, ZZ>{}, integral_constant<int, kTW>{}, integral_constant<int, G>{},
+             zp, min(nw, (nzm - 1 - zp) / ZW + 1), pass * nw, pass == 0);
+  // the remaining <= 32 disparities [nzm, nz): every warp, a quarter of the
+  // tile's columns each (two-disparity kernels with 4-warp CTAs only)
+  if constexpr (ZZ == 2) {
+    if (nzm < nz)
+      run_pass(integral_constant<int, 1>{}, integral_constant<int, kTW / 4>{},
+               integral_constant<int, kSplitG>{}, nzm, 1, pass * nw, false);
   }
   __syncthreads();
 
@@ -911,9 +938,9 @@ S4Shape s4_shape(int nz, int zw, int nwmax) {
 
 // NWM warps per CTA at most, REGS registers per thread at most
 template <int B, int DIR, int G, int ZZ, int NWM, int REGS>
-cudaError_t launch4(const SweepArgs& a, S4Shape sh, cudaStream_t s) {
+cudaError_t launch4(const SweepArgs& a, S4Shape sh, int slots, cudaStream_t s) {
   const int th = sweep4_th();
-  const S4Layout<B, G, ZZ> lay(th, sh.nw, sh.slots());
+  const S4Layout<B, G, ZZ> lay(th, sh.nw, slots);
   static SmemAttr attr;
   if (cudaError_t e = attr.ensure(sweep4_kernel<B, DIR, G, ZZ, NWM, REGS>, lay.bytes); e != cudaSuccess)
     return e;
@@ -971,8 +998,9 @@ int sweep4_zz() {
 // Two per lane need even ring bases: padded rows (a.pc, a.ldp) in multiples
 // of 4 elements (prep_staging lays them out so).
 struct S4Plan {
-  int zz, tail, ze;
+  int zz, tail, ze, zm;   // zm: end of the warps' own disparities (== ze: no split pass)
   S4Shape shape;
+  int slots() const { return shape.slots() + (zm < ze ? 1 : 0); }
 };
 S4Plan s4_plan(const SweepArgs& a) {
   auto plan = [&](int zz, int nwmax) {
@@ -980,7 +1008,7 @@ S4Plan s4_plan(const SweepArgs& a) {
     S4Plan p;
     p.zz = zz;
     p.tail = a.d % zw == 0;   // z = d would take a warp of its own through a pass
-    p.ze = p.tail ? a.d : a.d + 1;
+    p.zm = p.ze = p.tail ? a.d : a.d + 1;
     p.shape = s4_shape(p.ze, zw, nwmax);
     return p;
   };
@@ -989,9 +1017,21 @@ S4Plan s4_plan(const SweepArgs& a) {
   const S4Plan p1 = plan(1, nw1), p2 = plan(2, nw2);
   const bool even = (a.pc & 3) == 0 && (a.ldp & 3) == 0;
   const int zz = sweep4_zz();   // 0: choose, 1 / 2: forced
-  const bool pick2 = zz == 2 || (zz == 0 && p2.shape.nw >= 2 &&
-                                 64 * p2.shape.slots() <= 32 * p1.shape.slots());
-  return even && pick2 ? p2 : p1;
+  if (!even || zz == 1) return p1;
+  // Four two-disparity warps and <= 32 disparities more (C3: d = 288): the
+  // rest goes to a column-split pass of the same CTA (sweep4_kernel run_pass)
+  // instead of a fifth warp, which would leave the SM's schedulers with 3, 3,
+  // 2, 2 warps.  C3 level 0: 2.20 -> 1.7 ms.
+  static const int split = env_int("MSHBM_SWEEP4_SPLIT", 1);
+  if (split && p1.ze > 256 && p1.ze <= 288 && nw2 == 4) {
+    S4Plan m = p1;   // the one-disparity tail rule: the split pass holds 32 per warp
+    m.zz = 2;
+    m.zm = 256;
+    m.shape = S4Shape{1, 4};
+    return m;
+  }
+  const bool pick2 = zz == 2 || (p2.shape.nw >= 2 && 64 * p2.shape.slots() <= 32 * p1.shape.slots());
+  return pick2 ? p2 : p1;
 }
 
 template <int B, int DIR>
@@ -1007,9 +1047,10 @@ cudaError_t launch4_d(const SweepArgs& a0, cudaStream_t s) {
   SweepArgs a = a0;
   a.s4_tail = p.tail;
   a.s4_ze = p.ze;
-  if (p.zz == 2) return launch4<B, DIR, 2, 2, 4, 168>(a, p.shape, s);
-  if (sweep4_group() == 2) return launch4<B, DIR, 2, 1, 8, 128>(a, p.shape, s);
-  return launch4<B, DIR, 4, 1, 8, 128>(a, p.shape, s);
+  a.s4_zm = p.zm;
+  if (p.zz == 2) return launch4<B, DIR, 2, 2, 4, 168>(a, p.shape, p.slots(), s);
+  if (sweep4_group() == 2) return launch4<B, DIR, 2, 1, 8, 128>(a, p.shape, p.slots(), s);
+  return launch4<B, DIR, 4, 1, 8, 128>(a, p.shape, p.slots(), s);
 }
 
 template <int B>
