@@ -300,7 +300,8 @@ __device__ __forceinline__ void row_step2(
 }
 
 template <int B, int DIR, int G, int ZZ, int NWM, int REGS>
-__global__ void __launch_bounds__(NWM * 32) __maxnreg__(REGS) sweep4_kernel(const SweepArgs a, const int th_) {
+__global__ void __launch_bounds__(NWM * 32) __maxnreg__(REGS) sweep4_kernel(const SweepArgs a, const int th_,
+                                                                               const int ybase) {
   pdl_wait();
   const int th = th_;
   using SL = S4Layout<B, G, ZZ>;
@@ -334,7 +335,9 @@ __global__ void __launch_bounds__(NWM * 32) __maxnreg__(REGS) sweep4_kernel(cons
   const int tid = threadIdx.x, nt = blockDim.x;
   const int lane = tid & 31, wp = tid >> 5;
   const int x0 = blockIdx.x * kTW;
-  const int y0 = a.rows.lo + blockIdx.y * th;
+  // tile rows on the whole-image grid (ybase: the first one's top row, may be
+  // above the image or the stage's rows; a.rows are the rows to compute)
+  const int y0 = ybase + blockIdx.y * th;
   const int H = a.H, W = a.W;
   const float qnan = __int_as_float(0x7fc00000);
 
@@ -945,10 +948,10 @@ cudaError_t launch4(const SweepArgs& a, S4Shape sh, int slots, cudaStream_t s) {
   if (cudaError_t e = attr.ensure(sweep4_kernel<B, DIR, G, ZZ, NWM, REGS>, lay.bytes); e != cudaSuccess)
     return e;
   // CTA rows on the whole-image grid (row bands bit-identical to whole runs)
-  SweepArgs b = a;
-  b.rows.lo = tile_row(a.rows.lo, th) * th - kTileOff;
-  dim3 grid((a.W + kTW - 1) / kTW, (b.rows.hi - b.rows.lo + th - 1) / th);
-  return launch_pdl(sweep4_kernel<B, DIR, G, ZZ, NWM, REGS>, grid, dim3(32 * sh.nw), lay.bytes, s, b, th);
+  const int ybase = tile_row(a.rows.lo, th) * th - kTileOff;
+  dim3 grid((a.W + kTW - 1) / kTW, (a.rows.hi - ybase + th - 1) / th);
+  return launch_pdl(sweep4_kernel<B, DIR, G, ZZ, NWM, REGS>, grid, dim3(32 * sh.nw), lay.bytes, s, a, th,
+                    ybase);
 }
 
 }  // namespace

@@ -1,0 +1,103 @@
+"""sweep4 lane layouts (csrc/sweep4.cu s4_plan): one disparity per lane, two
+per lane (64 per warp), the z = d tail, and the column-split pass for the
+disparities beyond four two-disparity warps.
+
+Small wide images with wide search ranges, sweep4 forced on (MSHBM_SWEEP4=2,
+read once per process, hence the subprocesses), against the pinned C oracle;
+and the same cases with one disparity per lane forced (MSHBM_SWEEP4_ZZ=1):
+the two-per-lane layout evaluates every (pixel, z) with the same arithmetic
+in the same order, so without a split pass the outputs are bit-identical.
+"""
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+pytestmark = pytest.mark.gpu
+
+# (h, w, d_max, block, radius, sign, layout the default plan picks[, levels = 1])
+CASES = [
+    (80, 420, 127, 7, 2, "middlebury", "two per lane, 2 warps"),
+    (80, 420, 128, 7, 2, "paper", "two per lane, 2 warps + tail z = d"),
+    (72, 600, 280, 9, 3, "middlebury", "4 warps x 64 + split pass of 25"),
+    (72, 600, 287, 5, 1, "paper", "4 warps x 64 + split pass of 32"),
+    (72, 600, 288, 7, 2, "middlebury", "split pass + tail z = d"),
+    (72, 600, 270, 11, 2, "middlebury", "split pass, b = 11"),
+    (64, 700, 511, 7, 2, "middlebury", "two per lane, 2 passes of 4 warps"),
+    (64, 700, 200, 9, 2, "paper", "one per lane (7 warps)"),
+    # no pyramid: every pixel untrusted, no pixel states (the first tile row
+    # starts above the image: its rows -2, -1 must not be written)
+    (72, 600, 100, 7, 1, "middlebury", "K = 0, one per lane", 0),
+    (72, 600, 127, 11, 1, "middlebury", "K = 0, two per lane", 0),
+]
+
+
+def _levels(case):
+    return case[7] if len(case) > 7 else 1
+
+_RUN = r'''
+import sys, numpy as np
+sys.path.insert(0, ".")
+import paper_1901_09593_b200 as gpu
+from paper_1901_09593_b200.synthetic import CONFIGS, make_pair
+cases = eval(sys.argv[2])
+out = {}
+for i, case in enumerate(cases):
+    h, w, d_max, block, radius, sign = case[:6]
+    levels = case[7] if len(case) > 7 else 1
+    l, r, _gt = make_pair(CONFIGS["C4"], seed=100 + i, height=h, width=w)
+    cfg = gpu.MatchConfig(d_max=d_max, levels=levels, block=block, radius=radius, sign=sign)
+    d, c, t = gpu.run_pipeline(l, r, cfg)
+    out[f"d{i}"], out[f"c{i}"] = d, c
+np.savez(sys.argv[1], **out)
+'''
+
+
+def _run(env_extra, path):
+    env = dict(os.environ, MSHBM_SWEEP4="2", **env_extra)
+    r = subprocess.run([sys.executable, "-c", _RUN, path, repr(CASES)], cwd=ROOT, env=env,
+                       capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stderr[-3000:]
+    return np.load(path)
+
+
+@pytest.fixture(scope="module")
+def runs(tmp_path_factory):
+    tmp = tmp_path_factory.mktemp("s4layouts")
+    return (_run({}, str(tmp / "auto.npz")), _run({"MSHBM_SWEEP4_ZZ": "1"}, str(tmp / "zz1.npz")))
+
+
+@pytest.mark.parametrize("i", range(len(CASES)), ids=[c[6] for c in CASES])
+def test_layout_matches_oracle(runs, i):
+    from oracle import c_oracle as CO
+    from paper_1901_09593_b200.synthetic import CONFIGS, make_pair
+    h, w, d_max, block, radius, sign = CASES[i][:6]
+    l, r, _gt = make_pair(CONFIGS["C4"], seed=100 + i, height=h, width=w)
+    od, oc, _ = CO.run_pipeline(l, r, d_max, _levels(CASES[i]), block, radius=radius, sign=sign)
+    for name, run in zip(("auto", "one per lane"), runs):
+        d, c = run[f"d{i}"], run[f"c{i}"]
+        same = d == od
+        # budget: 0.05% of the image (BASELINE north_star), near ties only
+        assert (~same).sum() <= max(2, 5e-4 * d.size), (name, int((~same).sum()))
+        assert float(np.abs(c - oc)[same].max()) <= 1e-4, name
+
+
+@pytest.mark.parametrize("i", [0, 1, 6, 9], ids=[CASES[i][6] for i in (0, 1, 6, 9)])
+def test_two_per_lane_is_bit_identical_to_one_per_lane(runs, i):
+    auto, zz1 = runs
+    assert np.array_equal(auto[f"d{i}"], zz1[f"d{i}"])
+    assert np.array_equal(auto[f"c{i}"], zz1[f"c{i}"])
+
+
+@pytest.mark.parametrize("i", [2, 3, 4, 5], ids=[CASES[i][6] for i in (2, 3, 4, 5)])
+def test_split_pass_agrees_with_one_per_lane(runs, i):
+    """The split pass sums a window's columns in another order (two chains over
+    6 cost columns instead of 18): costs agree to fp32 rounding, winners can
+    differ at exact near ties only."""
+    auto, zz1 = runs
+    same = auto[f"d{i}"] == zz1[f"d{i}"]
+    assert (~same).sum() <= 2
+    assert float(np.abs(auto[f"c{i}"] - zz1[f"c{i}"])[same].max()) <= 2e-5
