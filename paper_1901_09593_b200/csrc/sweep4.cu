@@ -969,16 +969,6 @@ bool sweep4_supported(const SweepArgs& a, bool force) {
 
 namespace {
 
-int g_group = -1;
-int sweep4_group() {
-  if (g_group < 0) {
-    const char* v = getenv("MSHBM_SWEEP4_G");   // row steps per CTA barrier (2 or 4)
-    g_group = v ? atoi(v) : 2;   // 4 spills at the 128-register cap (measured slower)
-    if (g_group != 2 && g_group != 4) g_group = 2;
-  }
-  return g_group;
-}
-
 int g_zz = -1;
 int sweep4_zz() {
   if (g_zz < 0) {
@@ -1052,8 +1042,7 @@ cudaError_t launch4_d(const SweepArgs& a0, cudaStream_t s) {
   a.s4_ze = p.ze;
   a.s4_zm = p.zm;
   if (p.zz == 2) return launch4<B, DIR, 2, 2, 4, 168>(a, p.shape, p.slots(), s);
-  if (sweep4_group() == 2) return launch4<B, DIR, 2, 1, 8, 128>(a, p.shape, p.slots(), s);
-  return launch4<B, DIR, 4, 1, 8, 128>(a, p.shape, p.slots(), s);
+  return launch4<B, DIR, 2, 1, 8, 128>(a, p.shape, p.slots(), s);
 }
 
 template <int B>

@@ -24,10 +24,19 @@ for c in C2 C3 C5; do
   timeout 900 ncu --clock-control none --metrics $M --csv --log-file $OUT/stages_$c.csv \
     python tools/prof_once.py $c > $OUT/stages_$c.log 2>&1
 done
-timeout 900 ncu --set full --import-source on --clock-control none -k regex:sweep4_kernel -c 1 \
-  -o $OUT/sweep4_c3 python tools/prof_once.py C3 > $OUT/sweep4_c3.log 2>&1
-timeout 900 ncu --set full --import-source on --clock-control none -k regex:prior_select -c 1 \
-  -o $OUT/prior_select_c3 python tools/prof_once.py C3 > $OUT/prior_select_c3.log 2>&1
+# ncu --set full captures: the .ncu-rep stays in /tmp on the box (gpurun_out/ is capped at
+# 64 MiB); the raw-page summary + per-source-line breakdown come back as markdown
+cap() {  # cap <config> <kernel regex> <name>
+  timeout 900 ncu --set full --import-source on --clock-control none -k regex:$2 -c 1 -f \
+    -o /tmp/$3 python tools/prof_once.py $1 > $OUT/$3.log 2>&1
+  python tools/ncu_summary.py /tmp/$3.ncu-rep "$TAG $3: $2 on $1 (ncu --set full, one launch)" \
+    > $OUT/$3_ncu.md 2>> $OUT/$3.log
+  ncu -i /tmp/$3.ncu-rep --page source --csv > /tmp/$3_source.csv 2>/dev/null
+  python tools/sass_stalls.py /tmp/$3_source.csv 25 > $OUT/$3_sass_stalls.txt 2>> $OUT/$3.log
+}
+cap C3 sweep4_kernel sweep4_c3
+cap C5 sweep4_kernel sweep4_c5
+cap C3 prior_select prior_select_c3
 timeout 1500 python tools/flop_check.py capture $OUT/flops.json C1 C2 C3 C4 C5 > $OUT/flops.log 2>&1
 timeout 900 python tools/band_scaling.py C5 2 4 8 > $OUT/bands.log 2>&1
 echo done > $OUT/DONE
