@@ -43,7 +43,6 @@ namespace {
 constexpr unsigned kFull = 0xffffffffu;
 constexpr int kTW = 16;          // output columns per CTA
 constexpr int kNWMax = 8;        // warps (x 32 disparities) per CTA and pass
-constexpr int kSplitG = 8;       // row steps per CTA barrier of the column-split pass
 
 __device__ __forceinline__ float fma_sat(float a, float b, float c) {
   float r;
@@ -95,7 +94,10 @@ struct S4Layout {
   static constexpr int RB = B + 2 * G;          // R ring rows (b + G live + G in flight)
   int th, rwp, mwp, nzw;
   size_t o_bar, o_lt, o_pp, o_rr, o_mr, o_sk, o_rk, o_hs, bytes;
-  __host__ __device__ S4Layout(int th_, int nw, int nzw_) : th(th_), nzw(nzw_) {
+  // ring pitches of the row-split pass (32 disparities, sweep4_kernel run_rows)
+  static constexpr int RWS = (NV + 31 + 3 + 3 + 3) & ~3, MWS = (NC + 31 + 1 + 1 + 1) & ~1;
+  __host__ __device__ S4Layout(int th_, int nw, int nzw_, bool rows_pass = false)
+      : th(th_), nzw(nzw_) {
     // ring rows start 16-byte aligned in global memory: up to 3 (R) / 1 (Mp)
     // extra leading elements, and the copy is rounded up to 16 bytes
     // (ZZ = 2: lanes read whole pairs from the even element at or below
@@ -105,10 +107,13 @@ struct S4Layout {
     size_t o = 0;
     o_bar = o; o += 16;   // the tile's row masks (sel, ref) + the ring's mbarrier
     o_pp = o; o += sizeof(float4) * (th + 2) * (NC / 2);
-    o_mr = o; o += sizeof(float2) * 2 * G * mwp;
+    // (the row-split pass stages all its rows at once: th + 2 / th + B + 1 short rows)
+    const int mre = rows_pass && (th + 2) * MWS > 2 * G * mwp ? (th + 2) * MWS : 2 * G * mwp;
+    const int rre = rows_pass && (th + B + 1) * RWS > RB * rwp ? (th + B + 1) * RWS : RB * rwp;
+    o_mr = o; o += sizeof(float2) * mre;
     o = (o + 15) & ~(size_t)15;
     o_lt = o; o += sizeof(float) * (th + B + 1) * NVP;
-    o_rr = o; o += sizeof(float) * RB * rwp;
+    o_rr = o; o += sizeof(float) * rre;
     o = (o + 15) & ~(size_t)15;
     o_sk = o; o += sizeof(unsigned) * nzw * th * kTW;
     o_rk = o; o += sizeof(unsigned) * nzw * th * kTW;
@@ -124,9 +129,7 @@ struct S4Layout {
 // stores the warp's key per pixel into sk); REF: 3x3-summed winner of
 // output row k - 2 (into rk).  Rows whose pixels need neither skip the
 // reductions (the tile's row masks, see sweep4_kernel).
-// TWW: the warp's share of the tile's columns (kTW, or kTW / warps in a
-// column-split pass: the caller offsets Pp, mrow, sk, rk by the warp's first
-// column); SH: key bits holding the warp-local z.
+// TWW: tile columns (kTW); SH: key bits holding the warp-local z.
 template <int B, int TWW, int SH>
 __device__ __forceinline__ void row_step(
     const int k, const bool SEL, const bool REF, float (&V)[TWW + B + 1], float (&X)[TWW],
@@ -322,7 +325,7 @@ __global__ void __launch_bounds__(NWM * 32) __maxnreg__(REGS) sweep4_kernel(cons
   // column-split pass of all warps (run_pass below), one more key slot
   const int nzm = a.s4_zm;
   const int nslot = ((nzm + ZW * nw - 1) / (ZW * nw)) * nw + (nzm < nz ? 1 : 0);
-  const SL lay(th, nw, nslot);
+  const SL lay(th, nw, nslot, nzm < nz);
   unsigned long long* bars = reinterpret_cast<unsigned long long*>(smem + lay.o_bar) + 1;
   unsigned* sK = reinterpret_cast<unsigned*>(smem + lay.o_sk);
   unsigned* rK = reinterpret_cast<unsigned*>(smem + lay.o_rk);
@@ -429,31 +432,17 @@ __global__ void __launch_bounds__(NWM * 32) __maxnreg__(REGS) sweep4_kernel(cons
   const float* __restrict__ Rp = a.Rp + a.pc;
   const float2* __restrict__ Mp = a.Mp + a.pc;
   unsigned phase = 0;
-  // One pass over the tile's rows for the disparities [zp, zp + ZWp * nwp) on
-  // the lanes of nwp warps, ZZp per lane; winners into key slot `slot0 + wp`.
-  // TWW = kTW: every warp sweeps the whole tile width for its own 32 ZZp
-  // disparities.  TWW < kTW (column split, ZZp = 1, nwp = 1): all warps hold
-  // the same 32 disparities and each sweeps kTW / nw of the tile's columns:
-  // the rest of a search range that does not fill another warp, without an
-  // idle warp or a pass of one.
-  auto run_pass = [&](auto zz_c, auto tww_c, auto g_c, const int zp, const int nwp,
-                      const int slot0, const bool first) {
-    constexpr int ZZp = decltype(zz_c)::value, TWW = decltype(tww_c)::value;
-    // GP row steps per CTA barrier, ring rows RBp (the split pass's rows are short:
-    // more of them fit the same rings, so it synchronises less often)
-    constexpr int GP = decltype(g_c)::value, RBp = B + 2 * GP;
-    constexpr int ZWp = 32 * ZZp, SHp = SH;   // keys always in the kernel's format
-    constexpr bool kSplit = TWW < kTW;
-    constexpr int NVW = TWW + B + 1, NV4 = (NVW + 3) / 4;
-    const int col0 = kSplit ? TWW * wp : 0;   // the warp's first tile column
-    const int zlo = kSplit ? zp : zp + ZWp * wp;
-    const int z = zlo + ZZp * lane;   // the lane's (first) disparity
+  // One pass over the tile's rows for the disparities [zp, zp + ZW * nwp) on
+  // the lanes of nwp warps, ZZ per lane; winners into key slot `slot0 + wp`.
+  auto run_pass = [&](const int zp, const int nwp, const int slot0, const bool first) {
+    const int zlo = zp + ZW * wp;
+    const int z = zlo + ZZ * lane;   // the lane's (first) disparity
     // every z of the warp has its right centre outside the image for every
     // cost column of the tile: costs are all -1 there, and lower warps hold
     // smaller z with costs >= -1, so skipping the warp is exact (its key
     // slots stay 0 = no candidate)
-    const bool active = (kSplit || wp < nwp) && (DIR > 0 ? (zlo <= x0 + kTW) : (zlo <= W - x0));
-    const int span = ZWp * nwp - 1;
+    const bool active = wp < nwp && (DIR > 0 ? (zlo <= x0 + kTW) : (zlo <= W - x0));
+    const int span = ZW * nwp - 1;
     // image column of ring element 0 (R ring: tile V columns, Mp ring: cost
     // columns), moved down to a 16-byte boundary of the padded row
     int rc0 = DIR > 0 ? (x0 - 1 - H2 - zp - span) : (x0 - 1 - H2 + zp);
@@ -461,35 +450,33 @@ __global__ void __launch_bounds__(NWM * 32) __maxnreg__(REGS) sweep4_kernel(cons
     const int rmis = (a.pc + rc0) & 3, mmis = (a.pc + mc0) & 1;
     rc0 -= rmis;
     mc0 -= mmis;
-    // ring row pitches of this pass (the layout's for the warps' own passes)
-    const int rwp = kSplit ? ((NV + span + 3 + 3 + 3) & ~3) : lay.rwp;
-    const int mwp = kSplit ? ((NC + span + 1 + 1 + 1) & ~1) : lay.mwp;
+    const int rwp = lay.rwp, mwp = lay.mwp;
     const unsigned rbytes = (unsigned)(((NV + span + rmis + 3) & ~3) * sizeof(float));
     const unsigned mbytes = (unsigned)(((NC + span + mmis + 1) & ~1) * sizeof(float2));
     // lane base into the rings: element index of column c for this z.
-    // ZZp = 2: the lane's first element (that of z + 1 for DIR > 0) moved down
+    // ZZ = 2: the lane's first element (that of z + 1 for DIR > 0) moved down
     // to an even index, so whole pairs load with LDS.64 / LDS.128; the parity
     // pads sR, sM are compile-time constants because x0, zp and the padding
     // column a.pc are even
-    constexpr int sR = ZZp == 1 ? 0 : (DIR > 0 ? (H2 & 1) : ((H2 + 1) & 1));
-    constexpr int sM = ZZp == 1 ? 0 : (DIR > 0 ? 0 : 1);
-    const int lb = (DIR > 0 ? (span - (z - zp)) - (ZZp - 1) : (z - zp)) + rmis - sR + col0;
-    const int mb = (DIR > 0 ? (span - (z - zp)) - (ZZp - 1) : (z - zp)) + mmis - sM + col0;
-    if (ZZp > 1 && ((lb | mb) & 1)) __trap();
+    constexpr int sR = ZZ == 1 ? 0 : (DIR > 0 ? (H2 & 1) : ((H2 + 1) & 1));
+    constexpr int sM = ZZ == 1 ? 0 : (DIR > 0 ? 0 : 1);
+    const int lb = (DIR > 0 ? (span - (z - zp)) - (ZZ - 1) : (z - zp)) + rmis - sR;
+    const int mb = (DIR > 0 ? (span - (z - zp)) - (ZZ - 1) : (z - zp)) + mmis - sM;
+    if (ZZ > 1 && ((lb | mb) & 1)) __trap();
 
     auto stage_r = [&](int rr, unsigned long long* bar) {
       const int y = clampi(y0 - 1 - H2 + rr, 0, H - 1);
-      bulk_g2s(Rr + (rr % RBp) * rwp, Rp + ((int64_t)y * a.ldp + rc0), rbytes, bar);
+      bulk_g2s(Rr + (rr % RB) * rwp, Rp + ((int64_t)y * a.ldp + rc0), rbytes, bar);
     };
     auto stage_m = [&](int k, unsigned long long* bar) {
       const int y = clampi(y0 - 1 + k, 0, H - 1);
-      bulk_g2s(Mr + (k % (2 * GP)) * mwp, Mp + ((int64_t)y * a.ldp + mc0), mbytes, bar);
+      bulk_g2s(Mr + (k % (2 * G)) * mwp, Mp + ((int64_t)y * a.ldp + mc0), mbytes, bar);
     };
     if (!first) __syncthreads();   // previous pass done with the rings
 
     if (tid == 0) {
       fence_proxy_async();
-      const int nr0 = min(B + GP, th + B + 1 - k0), nm0 = min(GP, th + 2 - k0);
+      const int nr0 = min(B + G, th + B + 1 - k0), nm0 = min(G, th + 2 - k0);
       mbar_expect_tx(bars, nr0 * rbytes + nm0 * mbytes);
       for (int rr = k0; rr < k0 + nr0; ++rr) stage_r(rr, bars);
       for (int k = k0; k < k0 + nm0; ++k) stage_m(k, bars);
@@ -497,8 +484,8 @@ __global__ void __launch_bounds__(NWM * 32) __maxnreg__(REGS) sweep4_kernel(cons
     mbar_wait(bars, phase & 1u);
     phase ^= 1u;
 
-    float V[ZZp][NVW];
-    constexpr int NT2 = (NVW + 1 + sR + 1) / 2;   // ZZp = 2: float2 loads per ring row
+    float V[ZZ][NV];
+    constexpr int NT2 = (NV + 1 + sR + 1) / 2;   // ZZ = 2: float2 loads per ring row
     // ring row -> the lane's NV + 1 (+ pad) consecutive samples
     auto load_r = [&](const float* rowp, float (&t)[2 * NT2]) {
       const float2* rp = reinterpret_cast<const float2*>(rowp + lb);
@@ -511,30 +498,30 @@ __global__ void __launch_bounds__(NWM * 32) __maxnreg__(REGS) sweep4_kernel(cons
     };
     // V[.][c] += sign * L'(row, c) * R'(ring row, c -+ z) over the warp's columns
     auto accum = [&](int lrow, int ring_row) {
-      const float4* lr = reinterpret_cast<const float4*>(Lt + lrow * NVP + col0);
-      if constexpr (ZZp == 1) {
+      const float4* lr = reinterpret_cast<const float4*>(Lt + lrow * NVP);
+      if constexpr (ZZ == 1) {
         const float* rrow = Rr + ring_row * rwp + lb;
 #pragma unroll
-        for (int c4 = 0; c4 < NV4; ++c4) {
+        for (int c4 = 0; c4 < NVP / 4; ++c4) {
           const float4 l4 = lr[c4];
           const float lv[4] = {l4.x, l4.y, l4.z, l4.w};
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
             const int c = 4 * c4 + e;
-            if (c < NVW) V[0][c] = fmaf(lv[e], rrow[c], V[0][c]);
+            if (c < NV) V[0][c] = fmaf(lv[e], rrow[c], V[0][c]);
           }
         }
       } else {
         float t[2 * NT2];
         load_r(Rr + ring_row * rwp, t);
 #pragma unroll
-        for (int c4 = 0; c4 < NV4; ++c4) {
+        for (int c4 = 0; c4 < NVP / 4; ++c4) {
           const float4 l4 = lr[c4];
           const float lv[4] = {l4.x, l4.y, l4.z, l4.w};
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
             const int c = 4 * c4 + e;
-            if (c < NVW) {
+            if (c < NV) {
               V[0][c] = fmaf(lv[e], t[c + sR + zoff<DIR>(0)], V[0][c]);
               V[1][c] = fmaf(lv[e], t[c + sR + zoff<DIR>(1)], V[1][c]);
             }
@@ -544,27 +531,27 @@ __global__ void __launch_bounds__(NWM * 32) __maxnreg__(REGS) sweep4_kernel(cons
     };
     if (active) {
 #pragma unroll
-      for (int e = 0; e < ZZp; ++e)
+      for (int e = 0; e < ZZ; ++e)
 #pragma unroll
-        for (int c = 0; c < NVW; ++c) V[e][c] = 0.f;
+        for (int c = 0; c < NV; ++c) V[e][c] = 0.f;
 #pragma unroll
-      for (int r = 0; r < B; ++r) accum(k0 + r, (k0 + r) % RBp);
+      for (int r = 0; r < B; ++r) accum(k0 + r, (k0 + r) % RB);
     }
     const bool lane0 = lane == 0;
-    unsigned laneK[ZZp];
-    float half[ZZp];
+    unsigned laneK[ZZ];
+    float half[ZZ];
 #pragma unroll
-    for (int e = 0; e < ZZp; ++e) {
-      laneK[e] = (unsigned)(ZW - 1 - (ZZp * lane + e)) + (1u << SHp) - (0x3F800000u << SHp);
+    for (int e = 0; e < ZZ; ++e) {
+      laneK[e] = (unsigned)(ZW - 1 - (ZZ * lane + e)) + (1u << SH) - (0x3F800000u << SH);
       half[e] = z + e < nz ? 0.5f : -1.0e30f;
     }
-    unsigned* sk = sK + (slot0 + (kSplit ? 0 : wp)) * th * kTW + col0;
-    unsigned* rk = rK + (slot0 + (kSplit ? 0 : wp)) * th * kTW + col0;
-    float X[ZZp][TWW], Y[ZZp][TWW];
+    unsigned* sk = sK + (slot0 + wp) * th * kTW;
+    unsigned* rk = rK + (slot0 + wp) * th * kTW;
+    float X[ZZ][kTW], Y[ZZ][kTW];
 #pragma unroll
-    for (int e = 0; e < ZZp; ++e)
+    for (int e = 0; e < ZZ; ++e)
 #pragma unroll
-      for (int p = 0; p < TWW; ++p) X[e][p] = 0.f, Y[e][p] = 0.f;
+      for (int p = 0; p < kTW; ++p) X[e][p] = 0.f, Y[e][p] = 0.f;
 
     // Rows are consumed in groups of G steps: one mbarrier wait and one CTA
     // barrier per group; the ring holds the group's b + G R rows and G Mp
@@ -576,9 +563,9 @@ __global__ void __launch_bounds__(NWM * 32) __maxnreg__(REGS) sweep4_kernel(cons
         if ((needc >> k) & 1ull) {
           const bool sl = k >= 1 && ((selm >> (k - 1)) & 1u);
           const bool rf = k >= 2 && ((refm >> (k - 2)) & 1u);
-          const float2* mrow = Mr + (k % (2 * GP)) * mwp + mb;
-          if constexpr (ZZp == 1)
-            row_step<B, TWW, SHp>(k, sl, rf, V[0], X[0], Y[0], Pp + col0 / 2, mrow, half[0],
+          const float2* mrow = Mr + (k % (2 * G)) * mwp + mb;
+          if constexpr (ZZ == 1)
+            row_step<B, kTW, SH>(k, sl, rf, V[0], X[0], Y[0], Pp, mrow, half[0],
                                   laneK[0], lane0, sk, rk);
           else
             row_step2<B, DIR>(k, sl, rf, V, X, Y, Pp, reinterpret_cast<const float4*>(mrow), half,
@@ -586,33 +573,33 @@ __global__ void __launch_bounds__(NWM * 32) __maxnreg__(REGS) sweep4_kernel(cons
         }
         // slide V down one row: + row k + B, - row k
         if (k <= th) {
-          const float4* lin = reinterpret_cast<const float4*>(Lt + (k + B) * NVP + col0);
-          const float4* lout = reinterpret_cast<const float4*>(Lt + k * NVP + col0);
-          if constexpr (ZZp == 1) {
-            const float* rin = Rr + ((k + B) % RBp) * rwp + lb;
-            const float* rout = Rr + (k % RBp) * rwp + lb;
+          const float4* lin = reinterpret_cast<const float4*>(Lt + (k + B) * NVP);
+          const float4* lout = reinterpret_cast<const float4*>(Lt + k * NVP);
+          if constexpr (ZZ == 1) {
+            const float* rin = Rr + ((k + B) % RB) * rwp + lb;
+            const float* rout = Rr + (k % RB) * rwp + lb;
 #pragma unroll
-            for (int c4 = 0; c4 < NV4; ++c4) {
+            for (int c4 = 0; c4 < NVP / 4; ++c4) {
               const float4 i4 = lin[c4], o4 = lout[c4];
               const float iv[4] = {i4.x, i4.y, i4.z, i4.w}, ov[4] = {o4.x, o4.y, o4.z, o4.w};
 #pragma unroll
               for (int e = 0; e < 4; ++e) {
                 const int c = 4 * c4 + e;
-                if (c < NVW) V[0][c] = fmaf(iv[e], rin[c], fmaf(-ov[e], rout[c], V[0][c]));
+                if (c < NV) V[0][c] = fmaf(iv[e], rin[c], fmaf(-ov[e], rout[c], V[0][c]));
               }
             }
           } else {
             float tin[2 * NT2], tout[2 * NT2];
-            load_r(Rr + ((k + B) % RBp) * rwp, tin);
-            load_r(Rr + (k % RBp) * rwp, tout);
+            load_r(Rr + ((k + B) % RB) * rwp, tin);
+            load_r(Rr + (k % RB) * rwp, tout);
 #pragma unroll
-            for (int c4 = 0; c4 < NV4; ++c4) {
+            for (int c4 = 0; c4 < NVP / 4; ++c4) {
               const float4 i4 = lin[c4], o4 = lout[c4];
               const float iv[4] = {i4.x, i4.y, i4.z, i4.w}, ov[4] = {o4.x, o4.y, o4.z, o4.w};
 #pragma unroll
               for (int e = 0; e < 4; ++e) {
                 const int c = 4 * c4 + e;
-                if (c < NVW) {
+                if (c < NV) {
 #pragma unroll
                   for (int q = 0; q < 2; ++q) {
                     const int j = c + sR + zoff<DIR>(q);
@@ -626,38 +613,122 @@ __global__ void __launch_bounds__(NWM * 32) __maxnreg__(REGS) sweep4_kernel(cons
       }
     };
 #pragma unroll 1
-    for (int k = k0; k < kend; k += GP) {
+    for (int k = k0; k < kend; k += G) {
       if (k > k0) {
         mbar_wait(bars, phase & 1u);
         phase ^= 1u;
         __syncthreads();   // every warp done with the previous group (its slots are reused)
       }
-      if (tid == 0 && k + GP < kend) {
+      if (tid == 0 && k + G < kend) {
         fence_proxy_async();
-        const int r0 = k + B + GP, r1 = min(k + B + 2 * GP, th + B + 1);
-        const int m0 = k + GP, m1 = min(k + 2 * GP, th + 2);
+        const int r0 = k + B + G, r1 = min(k + B + 2 * G, th + B + 1);
+        const int m0 = k + G, m1 = min(k + 2 * G, th + 2);
         mbar_expect_tx(bars, max(r1 - r0, 0) * rbytes + (m1 - m0) * mbytes);
         for (int rr = r0; rr < r1; ++rr) stage_r(rr, bars);
         for (int km = m0; km < m1; ++km) stage_m(km, bars);
       }
 #pragma unroll 1
-      for (int g = 0; g < GP; ++g) {
+      for (int g = 0; g < G; ++g) {
         if (k + g < kend) step(k + g);
       }
     }
   };
-  using std::integral_constant;
   // the warps' own disparities: [0, nzm), ZZ per lane
   int pass = 0;
   for (int zp = 0; zp < nzm; zp += ZW * nw, ++pass)
-    run_pass(integral_constant<int, ZZ>{}, integral_constant<int, kTW>{}, integral_constant<int, G>{},
-             zp, min(nw, (nzm - 1 - zp) / ZW + 1), pass * nw, pass == 0);
-  // the remaining <= 32 disparities [nzm, nz): every warp, a quarter of the
-  // tile's columns each (two-disparity kernels with 4-warp CTAs only)
+    run_pass(zp, min(nw, (nzm - 1 - zp) / ZW + 1), pass * nw, pass == 0);
+  // The remaining <= 32 disparities [nzm, nz) (two-disparity kernels with
+  // 4-warp CTAs): instead of a fifth warp, which would leave the SM's four
+  // schedulers with 3, 3, 2, 2 warps, every warp holds the same 32
+  // disparities, one per lane, and sweeps a quarter of the tile's rows (its
+  // output rows + the 2 more cost rows their 3x3 sums read) with sliding
+  // sums started at its own first row.  The rows of so narrow a range are
+  // short, so all of them are staged at once: no barrier inside the pass.
   if constexpr (ZZ == 2) {
-    if (nzm < nz)
-      run_pass(integral_constant<int, 1>{}, integral_constant<int, kTW / 4>{},
-               integral_constant<int, kSplitG>{}, nzm, 1, pass * nw, false);
+    if (nzm < nz) {
+      constexpr int RWS = SL::RWS, MWS = SL::MWS, span = 31;
+      const int zp = nzm, z = zp + lane;
+      const bool active = DIR > 0 ? (zp <= x0 + kTW) : (zp <= W - x0);
+      int rc0 = DIR > 0 ? (x0 - 1 - H2 - zp - span) : (x0 - 1 - H2 + zp);
+      int mc0 = DIR > 0 ? (x0 - 1 - zp - span) : (x0 - 1 + zp);
+      const int rmis = (a.pc + rc0) & 3, mmis = (a.pc + mc0) & 1;
+      rc0 -= rmis;
+      mc0 -= mmis;
+      const unsigned rbytes = (unsigned)(((NV + span + rmis + 3) & ~3) * sizeof(float));
+      const unsigned mbytes = (unsigned)(((NC + span + mmis + 1) & ~1) * sizeof(float2));
+      const int lb = (DIR > 0 ? span - lane : lane) + rmis;
+      const int mb = (DIR > 0 ? span - lane : lane) + mmis;
+      __syncthreads();   // the warps' own passes are done with the rings
+      const int nrr = min(kend + B, th + B + 1), nmr = min(kend, th + 2);
+      if (tid == 0) {
+        fence_proxy_async();
+        mbar_expect_tx(bars, nrr * rbytes + nmr * mbytes);
+        for (int rr = 0; rr < nrr; ++rr)
+          bulk_g2s(Rr + rr * RWS, Rp + ((int64_t)clampi(y0 - 1 - H2 + rr, 0, H - 1) * a.ldp + rc0),
+                   rbytes, bars);
+        for (int k = 0; k < nmr; ++k)
+          bulk_g2s(Mr + k * MWS, Mp + ((int64_t)clampi(y0 - 1 + k, 0, H - 1) * a.ldp + mc0), mbytes,
+                   bars);
+      }
+      mbar_wait(bars, phase & 1u);
+      phase ^= 1u;
+      const int rows_w = (th + nw - 1) / nw;            // output rows per warp
+      const int klo = rows_w * wp, khi = min(klo + rows_w + 2, kend);
+      if (active && klo < khi) {
+        float V[NV], X[kTW], Y[kTW];
+#pragma unroll
+        for (int c = 0; c < NV; ++c) V[c] = 0.f;
+#pragma unroll
+        for (int p = 0; p < kTW; ++p) X[p] = 0.f, Y[p] = 0.f;
+        // V[c] += L'(lrow, c) * R'(lrow, c -+ z)
+        auto accum = [&](int lrow) {
+          const float4* lr = reinterpret_cast<const float4*>(Lt + lrow * NVP);
+          const float* rrow = Rr + lrow * RWS + lb;
+#pragma unroll
+          for (int c4 = 0; c4 < NVP / 4; ++c4) {
+            const float4 l4 = lr[c4];
+            const float lv[4] = {l4.x, l4.y, l4.z, l4.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const int c = 4 * c4 + e;
+              if (c < NV) V[c] = fmaf(lv[e], rrow[c], V[c]);
+            }
+          }
+        };
+#pragma unroll 1
+        for (int r = 0; r < B; ++r) accum(klo + r);
+        const unsigned laneK = (unsigned)(ZW - 1 - lane) + (1u << SH) - (0x3F800000u << SH);
+        const float half = z < nz ? 0.5f : -1.0e30f;
+        unsigned* sk = sK + (nslot - 1) * th * kTW;
+        unsigned* rk = rK + (nslot - 1) * th * kTW;
+#pragma unroll 1
+        for (int k = klo; k < khi; ++k) {
+          if ((needc >> k) & 1ull) {
+            // this warp's output rows only: [klo, klo + rows_w)
+            const bool sl = k >= klo + 1 && k <= klo + rows_w && ((selm >> (k - 1)) & 1u);
+            const bool rf = k >= klo + 2 && ((refm >> (k - 2)) & 1u);
+            row_step<B, kTW, SH>(k, sl, rf, V, X, Y, Pp, Mr + k * MWS + mb, half, laneK, lane == 0,
+                                 sk, rk);
+          }
+          if (k + 1 < khi) {   // slide V down one row: + row k + B, - row k
+            const float4* lin = reinterpret_cast<const float4*>(Lt + (k + B) * NVP);
+            const float4* lout = reinterpret_cast<const float4*>(Lt + k * NVP);
+            const float* rin = Rr + (k + B) * RWS + lb;
+            const float* rout = Rr + k * RWS + lb;
+#pragma unroll
+            for (int c4 = 0; c4 < NVP / 4; ++c4) {
+              const float4 i4 = lin[c4], o4 = lout[c4];
+              const float iv[4] = {i4.x, i4.y, i4.z, i4.w}, ov[4] = {o4.x, o4.y, o4.z, o4.w};
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const int c = 4 * c4 + e;
+                if (c < NV) V[c] = fmaf(iv[e], rin[c], fmaf(-ov[e], rout[c], V[c]));
+              }
+            }
+          }
+        }
+      }
+    }
   }
   __syncthreads();
 
@@ -943,7 +1014,7 @@ S4Shape s4_shape(int nz, int zw, int nwmax) {
 template <int B, int DIR, int G, int ZZ, int NWM, int REGS>
 cudaError_t launch4(const SweepArgs& a, S4Shape sh, int slots, cudaStream_t s) {
   const int th = sweep4_th();
-  const S4Layout<B, G, ZZ> lay(th, sh.nw, slots);
+  const S4Layout<B, G, ZZ> lay(th, sh.nw, slots, a.s4_zm < a.s4_ze);
   static SmemAttr attr;
   if (cudaError_t e = attr.ensure(sweep4_kernel<B, DIR, G, ZZ, NWM, REGS>, lay.bytes); e != cudaSuccess)
     return e;
