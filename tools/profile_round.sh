@@ -11,6 +11,9 @@ OUT=gpurun_out/$TAG
 mkdir -p $OUT
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.limit --format=csv > $OUT/smi.txt
 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.log 2>&1
+# implemented FLOP counts first: bench.py's roofline reads profiles/r02_flops.json
+timeout 1500 python tools/flop_check.py capture $OUT/flops.json C1 C2 C3 C4 C5 > $OUT/flops.log 2>&1
+cp $OUT/flops.json profiles/r02_flops.json
 for c in C1 C2 C3 C4 C5; do
   timeout 900 python bench.py --config $c > $OUT/bench_$c.json 2> $OUT/bench_$c.err
 done
@@ -37,6 +40,5 @@ cap() {  # cap <config> <kernel regex> <name>
 cap C3 sweep4_kernel sweep4_c3
 cap C5 sweep4_kernel sweep4_c5
 cap C3 prior_select prior_select_c3
-timeout 1500 python tools/flop_check.py capture $OUT/flops.json C1 C2 C3 C4 C5 > $OUT/flops.log 2>&1
 timeout 900 python tools/band_scaling.py C5 2 4 8 > $OUT/bands.log 2>&1
 echo done > $OUT/DONE
