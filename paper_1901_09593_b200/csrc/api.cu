@@ -100,6 +100,16 @@ struct Plan {
   cudaGraphExec_t exec = nullptr;         // plain graph
   cudaGraphExec_t exec_timed = nullptr;   // + the stage event-record nodes
   int launches = 0;
+  // host-output streaming (run_plan_io, launch_streamed): everything up to
+  // level 0's prior as one graph, then level 0's selection + median in row
+  // chunks, each chunk's rows copied to the host while the next one runs
+  cudaGraphExec_t exec_pre = nullptr;
+  std::vector<cudaGraphExec_t> exec_l0;
+  std::vector<int> l0_cut;                // chunk i = output rows [l0_cut[i], l0_cut[i + 1])
+  std::vector<cudaEvent_t> l0_ev;         // chunk i's median done
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t copy_done = nullptr;
+  int launches_streamed = 0;
   cudaStream_t stream = nullptr;   // batch slot stream (run_batch)
   // recorded after every use: a call on another stream waits for it before
   // touching the plan's buffers (inputs, pyramid, outputs are per plan)
@@ -346,11 +356,22 @@ cudaError_t rec(cudaEvent_t e, cudaStream_t s) {
 // costs also runs on the branch, beside level k's median (evs[K+2+k] =
 // sweep k done, evs[2K+3+(k-1)] = prefilter done, joined by prior k-1).
 // Every run records the plan's stage events (p.tev, t_begin/t_built/t_end).
+// part: kAll, or kPre = everything before level 0's selection (its prior
+// included), or kL0 = level 0's selection + median only, on the rows of
+// `chunk` (sweep rows, rows.lo..hi; median rows, cnt_lo..cnt_hi; first: the
+// chunk that also runs the whole image's guard fixup).
+enum { kAll = 0, kPre = 1, kL0 = 2 };
+struct L0Chunk {
+  RowBand sweep, median;
+  bool first;
+};
 int enqueue(mshbm_ctx* ctx, Plan& p, cudaStream_t s, cudaStream_t side = nullptr,
-            cudaEvent_t* evs = nullptr, cudaStream_t side2 = nullptr) {
+            cudaEvent_t* evs = nullptr, cudaStream_t side2 = nullptr, int part = kAll,
+            const L0Chunk* chunk = nullptr) {
   int n = 0;
   const mshbm_config& cfg = p.cfg;
   const int dir = cfg.sign == MSHBM_SIGN_PAPER ? -1 : 1;
+  if (part != kL0) {
   CK(rec(p.t_begin, s));
   CK(cudaMemsetAsync(p.counters, 0,
                      sizeof(unsigned long long) * (p.K + 1) * kCntSlots * kCntCopies, s));
@@ -439,12 +460,14 @@ int enqueue(mshbm_ctx* ctx, Plan& p, cudaStream_t s, cudaStream_t side = nullptr
     }
     if (fork && k < p.K) CK(cudaEventRecord(evs[k], side));
   }
-  for (int k = p.K; k >= 0; --k) {
+  }   // part != kL0
+  const bool fork = part != kL0 && side != nullptr && evs != nullptr && p.K > 0;
+  for (int k = part == kL0 ? 0 : p.K; k >= 0; --k) {
     LevelBuf& l = p.lv[k];
     unsigned long long* cnt = p.counters + (size_t)(p.K - k) * kCntSlots * kCntCopies;
     StageEvents* ev = &p.tev[p.K - k];
     CK(rec(ev->up0, s));
-    if (k < p.K) {
+    if (k < p.K && part != kL0) {
       LevelBuf& c = p.lv[k + 1];
       if (fork) {
         CK(cudaStreamWaitEvent(s, evs[2 * p.K + 3 + k], 0));   // prefilter of level k+1
@@ -475,10 +498,16 @@ int enqueue(mshbm_ctx* ctx, Plan& p, cudaStream_t s, cudaStream_t side = nullptr
     a.rows = l.rows;
     a.Rp = l.Rp; a.Mp = l.Mp; a.ldp = l.ldp; a.pc = l.pc;
     if (fork && k < p.K) CK(cudaStreamWaitEvent(s, evs[k], 0));
+    if (part == kPre && k == 0) break;   // level 0's selection + median: the kL0 chunks
     const bool s4 = sweep_uses_sweep4(a);
     CK(rec(ev->sel0, s));
+    if (part == kL0) a.rows = chunk->sweep;
     CK(launch_sweep(a, s, &n));
-    if (s4) {   // sweep2 on the tiles sweep4's precision guard left (usually none)
+    if (s4 && (part != kL0 || chunk->first)) {
+      // sweep2 on the tiles sweep4's precision guard left (usually none);
+      // chunked runs: once, for the whole level (the job list is the whole
+      // level's; it reads what sweep4 reads and writes only flagged tiles)
+      a.rows = l.rows;
       CK(launch_sweep4_fixup(a, s));
       ++n;
     }
@@ -498,13 +527,14 @@ int enqueue(mshbm_ctx* ctx, Plan& p, cudaStream_t s, cudaStream_t side = nullptr
       n += 1;
     }
     CK(rec(ev->med0, s));
-    CK(launch_median_pipeline(l.dsel, l.c, l.low, l.ld, l.h, l.w, cfg.alpha, l.dmed, cnt, l.rows,
-                              s));
+    CK(launch_median_pipeline(l.dsel, l.c, l.low, l.ld, l.h, l.w, cfg.alpha, l.dmed, cnt,
+                              part == kL0 ? chunk->median : l.rows, s));
     ++n;
     CK(rec(ev->med1, s));
   }
   CK(rec(p.t_end, s));
-  p.launches = n;
+  if (part == kAll) p.launches = n;
+  else p.launches_streamed += n;
   return MSHBM_OK;
 }
 
@@ -593,6 +623,110 @@ int launch_plan(mshbm_ctx* ctx, Plan& p, cudaStream_t s, int flags) {
     CK(cudaGraphLaunch(exec, s));
   }
   ctx->launches += p.launches;
+  return MSHBM_OK;
+}
+
+// Host-output streaming (MSHBM_IO_HOST, untimed, whole image): level 0's
+// selection + median run in row chunks after the rest of the pair, and each
+// chunk's disparity / cost rows go to the host on a copy stream while the
+// next chunk computes, so only the last chunk's copy is exposed.  Chunk
+// boundaries sit 4 rows above a sweep4 tile row (sweep rows [cut + 2, next
+// cut + 2) are whole tiles of the offset tile grid: no tile is swept twice),
+// chunks write disjoint rows, and every kernel keeps its whole-image tile
+// grid, so the outputs are bit-identical to the one-graph path (row bands'
+// property).
+bool stream_eligible(const Plan& p) {
+  static const int on = []() {
+    const char* v = getenv("MSHBM_STREAM_L0");
+    return v ? atoi(v) : 1;
+  }();
+  if (!on || p.user || p.K < 1) return false;
+  if (p.key.band_lo != 0 || p.key.band_hi < p.H) return false;
+  const LevelBuf& l0 = p.lv[0];
+  // a sweep4 level 0 tall enough that a chunk's tiles still fill the GPU
+  return l0.muL != nullptr && l0.h >= 1024;
+}
+
+int capture_part(mshbm_ctx* ctx, Plan& p, int part, const L0Chunk* chunk, cudaGraphExec_t* exec) {
+  cudaStream_t cs, side, side2;
+  CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&side2, cudaStreamNonBlocking));
+  std::vector<cudaEvent_t> evs(3 * p.K + 4);
+  for (auto& e : evs) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  cudaGraph_t g;
+  CK(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+  g_rec_events = false;
+  int st = part == kL0 ? enqueue(ctx, p, cs, nullptr, nullptr, nullptr, kL0, chunk)
+                       : enqueue(ctx, p, cs, side, evs.data(), side2, part, nullptr);
+  g_rec_events = true;
+  cudaError_t ce = cudaStreamEndCapture(cs, &g);
+  for (auto& e : evs) cudaEventDestroy(e);
+  cudaStreamDestroy(side);
+  cudaStreamDestroy(side2);
+  cudaStreamDestroy(cs);
+  if (st) return st;
+  CK(ce);
+  CK(cudaGraphInstantiate(exec, g, 0));
+  cudaGraphDestroy(g);
+  return MSHBM_OK;
+}
+
+int launch_streamed(mshbm_ctx* ctx, Plan& p, cudaStream_t s, int16_t* disparity, float* cost,
+                    int64_t ld_out) {
+  const LevelBuf& l0 = p.lv[0];
+  if (!p.exec_pre) {
+    // chunk cuts: multiples of the tile height minus 4 (see above)
+    const int th = sweep4_th();
+    static const int want = []() {
+      const char* v = getenv("MSHBM_STREAM_CHUNKS");
+      return v ? std::max(1, atoi(v)) : 4;
+    }();
+    std::vector<int> cut{0};
+    for (int i = 1; i < want; ++i) {
+      const int c = (int)(((int64_t)l0.h * i / want + th / 2) / th) * th - 4;
+      if (c > cut.back() + th && c < l0.h - th) cut.push_back(c);
+    }
+    cut.push_back(l0.h);
+    p.launches_streamed = 0;
+    int st = capture_part(ctx, p, kPre, nullptr, &p.exec_pre);
+    if (st) return st;
+    const int nc = (int)cut.size() - 1;
+    p.exec_l0.assign(nc, nullptr);
+    for (int i = 0; i < nc; ++i) {
+      L0Chunk ch;
+      const int lo = i == 0 ? 0 : cut[i] + 2, hi = i == nc - 1 ? l0.h : cut[i + 1] + 2;
+      ch.sweep = RowBand{lo, hi, lo, hi};
+      ch.median = RowBand{cut[i], cut[i + 1], cut[i], cut[i + 1]};
+      ch.first = i == 0;
+      st = capture_part(ctx, p, kL0, &ch, &p.exec_l0[i]);
+      if (st) return st;
+    }
+    p.l0_ev.resize(nc);
+    for (auto& e : p.l0_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&p.copy_done, cudaEventDisableTiming));
+    CK(cudaStreamCreateWithFlags(&p.copy_stream, cudaStreamNonBlocking));
+    p.l0_cut = cut;
+  }
+  CK(cudaGraphLaunch(p.exec_pre, s));
+  const int nc = (int)p.exec_l0.size();
+  for (int i = 0; i < nc; ++i) {
+    CK(cudaGraphLaunch(p.exec_l0[i], s));
+    CK(cudaEventRecord(p.l0_ev[i], s));
+    CK(cudaStreamWaitEvent(p.copy_stream, p.l0_ev[i], 0));
+    const int r0 = p.l0_cut[i], nr = p.l0_cut[i + 1] - r0;
+    if (disparity)
+      CK(cudaMemcpy2DAsync(disparity + (int64_t)r0 * ld_out, ld_out * 2,
+                           l0.dmed + (int64_t)r0 * l0.ld, l0.ld * 2, (size_t)l0.w * 2, nr,
+                           cudaMemcpyDeviceToHost, p.copy_stream));
+    if (cost)
+      CK(cudaMemcpy2DAsync(cost + (int64_t)r0 * ld_out, ld_out * 4, l0.c + (int64_t)r0 * l0.ld,
+                           l0.ld * 4, (size_t)l0.w * 4, nr, cudaMemcpyDeviceToHost,
+                           p.copy_stream));
+  }
+  CK(cudaEventRecord(p.copy_done, p.copy_stream));
+  CK(cudaStreamWaitEvent(s, p.copy_done, 0));
+  ctx->launches += p.launches_streamed;
   return MSHBM_OK;
 }
 
@@ -702,6 +836,15 @@ int run_plan_io(mshbm_ctx* ctx, Plan* p, const float* left, const float* right, 
     CK(cudaMemcpy2DAsync(p->in_l, p->ld_in * 4, left, ld * 4, (size_t)p->W * 4, p->H, kin, s));
     CK(cudaMemcpy2DAsync(p->in_r, p->ld_in * 4, right, ld * 4, (size_t)p->W * 4, p->H, kin, s));
   }
+  if (host && allow_sync && flags == 0 && trace == nullptr && (disparity || cost) &&
+      stream_eligible(*p)) {
+    st = launch_streamed(ctx, *p, s, disparity, cost, ld_out);
+    if (st) return st;
+    st = plan_release(ctx, *p, s);
+    if (st) return st;
+    CK(cudaStreamSynchronize(s));
+    return MSHBM_OK;
+  }
   st = launch_plan(ctx, *p, s, flags);
   if (st) return st;
   const LevelBuf& l0 = p->lv[0];
@@ -775,6 +918,13 @@ int mshbm_destroy(mshbm_ctx* ctx) {
   for (auto& kv : ctx->plans) {
     if (kv.second->exec) cudaGraphExecDestroy(kv.second->exec);
     if (kv.second->exec_timed) cudaGraphExecDestroy(kv.second->exec_timed);
+    if (kv.second->exec_pre) cudaGraphExecDestroy(kv.second->exec_pre);
+    for (cudaGraphExec_t e : kv.second->exec_l0)
+      if (e) cudaGraphExecDestroy(e);
+    for (cudaEvent_t e : kv.second->l0_ev)
+      if (e) cudaEventDestroy(e);
+    if (kv.second->copy_done) cudaEventDestroy(kv.second->copy_done);
+    if (kv.second->copy_stream) cudaStreamDestroy(kv.second->copy_stream);
     if (kv.second->stream) cudaStreamDestroy(kv.second->stream);
     if (kv.second->done) cudaEventDestroy(kv.second->done);
     destroy_events(kv.second->tev);
