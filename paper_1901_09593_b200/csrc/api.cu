@@ -710,9 +710,13 @@ int launch_streamed(mshbm_ctx* ctx, Plan& p, cudaStream_t s, int16_t* disparity,
   }
   CK(cudaGraphLaunch(p.exec_pre, s));
   const int nc = (int)p.exec_l0.size();
+  // every chunk is enqueued before the first copy: a copy into pageable host
+  // memory blocks the calling thread, and must not hold back the launches
   for (int i = 0; i < nc; ++i) {
     CK(cudaGraphLaunch(p.exec_l0[i], s));
     CK(cudaEventRecord(p.l0_ev[i], s));
+  }
+  for (int i = 0; i < nc; ++i) {
     CK(cudaStreamWaitEvent(p.copy_stream, p.l0_ev[i], 0));
     const int r0 = p.l0_cut[i], nr = p.l0_cut[i + 1] - r0;
     if (disparity)
