@@ -21,6 +21,14 @@
 // registers, reduced the same way.  The prior window (trusted pixels) masks
 // the keys of lanes outside [c - r, c + r]; untrusted pixels use [0, d].
 //
+// Lane layouts (s4_plan): one disparity per lane (32 per warp, 128
+// registers) or two adjacent ones (64 per warp, 168 registers: LDS.64 /
+// LDS.128 of the right samples and normalisers feed both, one REDUX for the
+// lane's two keys; same arithmetic per (pixel, z), bit-identical outputs),
+// plus, for a search range of four two-disparity warps and <= 32 more, a
+// row-split pass in which every warp sweeps a quarter of the tile's rows for
+// the same 32 disparities.  DESIGN.md section 6.
+//
 // Also: R' / (muR - c, 0.5/sigmaR) rows stream through a shared-memory ring
 // by 1-D bulk copies (one thread, mbarrier completion); z = d for d a
 // multiple of 32 is evaluated once per tile after the sweep (no warp with a
