@@ -1091,9 +1091,11 @@ S4Plan s4_plan(const SweepArgs& a) {
   const int zz = sweep4_zz();   // 0: choose, 1 / 2: forced
   if (!even || zz == 1) return p1;
   // Four two-disparity warps and <= 32 disparities more (C3: d = 288): the
-  // rest goes to a column-split pass of the same CTA (sweep4_kernel run_pass)
-  // instead of a fifth warp, which would leave the SM's schedulers with 3, 3,
-  // 2, 2 warps.  C3 level 0: 2.20 -> 1.7 ms.
+  // rest goes to a row-split pass of the same CTA (sweep4_kernel) instead of
+  // a fifth warp, which would leave the SM's schedulers with 3, 3, 2, 2
+  // warps.  C3 level 0: 2.20 -> 1.84 ms.  (Two full warps + a row-split
+  // pass, C2's d = 144: slower than one per lane, 0.41 vs 0.35 ms: the
+  // staged rows leave room for 4 CTAs = 8 warps per SM only.)
   static const int split = env_int("MSHBM_SWEEP4_SPLIT", 1);
   if (split && p1.ze > 256 && p1.ze <= 288 && nw2 == 4) {
     S4Plan m = p1;   // the one-disparity tail rule: the split pass holds 32 per warp
