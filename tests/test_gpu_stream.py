@@ -11,7 +11,8 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("name,shape", [("C3", (1984, 1056)), ("C2", (1472, 992))])
+@pytest.mark.parametrize("name,shape", [("C3", (1984, 1056)), ("C2", (1472, 992)),
+                                        ("C2", (1101, 611)), ("C4", (1027, 450))])
 def test_streamed_outputs_equal_one_graph_outputs(name, shape):
     import torch
     if not torch.cuda.is_available():
@@ -21,7 +22,7 @@ def test_streamed_outputs_equal_one_graph_outputs(name, shape):
     from paper_1901_09593_b200.synthetic import CONFIGS, make_pair
 
     cfg = CONFIGS[name]
-    h, w = shape          # >= 1024 rows: the streamed path (C2 transposed canvas: 1472 rows)
+    h, w = shape          # >= 1024 rows: the streamed path; odd sizes: partial tiles / chunks
     left, right, _ = make_pair(cfg, height=h, width=w)
     mc = gpu.MatchConfig(d_max=cfg.d_max, levels=cfg.levels, block=cfg.block, radius=cfg.radius)
     d_ref, c_ref, trace = gpu.run_pipeline(left, right, mc)       # traced: one graph
