@@ -330,7 +330,7 @@ __global__ void __launch_bounds__(NWM * 32) __maxnreg__(REGS) sweep4_kernel(cons
   const bool tail = a.s4_tail != 0;
   const int nz = a.s4_ze;    // disparities on lanes: [0, nz)
   // [0, nzm) on the warps' own lanes (ZZ each); the rest, if any, in a
-  // column-split pass of all warps (run_pass below), one more key slot
+  // row-split pass of all warps (below), one more key slot
   const int nzm = a.s4_zm;
   const int nslot = ((nzm + ZW * nw - 1) / (ZW * nw)) * nw + (nzm < nz ? 1 : 0);
   const SL lay(th, nw, nslot, nzm < nz);
