@@ -230,8 +230,10 @@ __global__ void __launch_bounds__(256) bspline_fir_kernel(const T* cin, int ch, 
                                                           int64_t ldc, int ty0) {
   extern __shared__ double smem_d[];
   T (*S)[kFE + 1] = reinterpret_cast<T (*)[kFE + 1]>(smem_d);        // [kFE][kFE+1] input
-  double (*Tm)[kFE + 1] = reinterpret_cast<double (*)[kFE + 1]>(
-      smem_d + (sizeof(T) * kFE * (kFE + 1) + 7) / 8);                 // [kFT][kFE+1] axis-0 pass
+  // axis-0 pass [kFT][kFE]: a pitch of 88 doubles (= 16 words mod 32) puts the
+  // axis-1 reads of a warp (4 rows x 8 consecutive doubles) on 2 x 32 banks
+  double (*Tm)[kFE] = reinterpret_cast<double (*)[kFE]>(
+      smem_d + (sizeof(T) * kFE * (kFE + 1) + 7) / 8);
   const int nh = ch + 2 * kNpad, nw = cw + 2 * kNpad;
   // tile rows ty0.. (row bands: only the coefficient rows their prior reads)
   const int y0 = (ty0 + blockIdx.y) * kFT, x0 = blockIdx.x * kFT;
@@ -276,16 +278,27 @@ __global__ void __launch_bounds__(256) bspline_fir_kernel(const T* cin, int ch, 
     for (int o = 0; o < 4; ++o) Tm[ty + 8 * o][c] = acc[o];
   }
   __syncthreads();
-  // axis 1
+  // axis 1: thread (row r, q) computes columns q, q + 8, q + 16, q + 24 of
+  // its row from the 81 row samples they share (the same tap order per
+  // output as a 57-tap loop: m ascending)
+  {
+    const int r = threadIdx.x >> 3, q = threadIdx.x & 7;
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-  for (int o = 0; o < 4; ++o) {
-    const int r = ty + 8 * o;
-    double acc = 0.0;
+    for (int k = 0; k < 2 * kFirR + 1 + 24; ++k) {
+      const double v = Tm[r][q + k];
 #pragma unroll
-    for (int m = -kFirR; m <= kFirR; ++m)
-      acc = fma(fir_tap(m < 0 ? -m : m), Tm[r][lane + kFirR + m], acc);
-    const int gy = y0 + r, gx = x0 + lane;
-    if (gy < nh && gx < nw) coef[(int64_t)gy * ldc + gx] = acc;
+      for (int o = 0; o < 4; ++o) {
+        const int m = k - 8 * o - kFirR;
+        if (m >= -kFirR && m <= kFirR) acc[o] = fma(fir_tap(m < 0 ? -m : m), v, acc[o]);
+      }
+    }
+    const int gy = y0 + r;
+#pragma unroll
+    for (int o = 0; o < 4; ++o) {
+      const int gx = x0 + q + 8 * o;
+      if (gy < nh && gx < nw) coef[(int64_t)gy * ldc + gx] = acc[o];
+    }
   }
 }
 
