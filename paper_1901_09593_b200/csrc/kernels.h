@@ -73,7 +73,7 @@ struct SweepArgs {
   // raw outputs (dense H x W): full, window, 3x3-summed winners
   int16_t* fz; float* fc; int16_t* wz; float* wcst; int16_t* nz; float* nc;
   // set by launch_sweep4 (s4_plan): the lanes hold z in [0, s4_ze), the
-  // warps' own lanes [0, s4_zm) and a column-split pass the rest; s4_tail:
+  // warps' own lanes [0, s4_zm) and a row-split pass the rest; s4_tail:
   // z = d is evaluated once per tile after the sweep
   int s4_ze, s4_zm, s4_tail;
 };

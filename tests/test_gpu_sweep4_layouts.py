@@ -1,5 +1,5 @@
 """sweep4 lane layouts (csrc/sweep4.cu s4_plan): one disparity per lane, two
-per lane (64 per warp), the z = d tail, and the column-split pass for the
+per lane (64 per warp), the z = d tail, and the row-split pass for the
 disparities beyond four two-disparity warps.
 
 Small wide images with wide search ranges, sweep4 forced on (MSHBM_SWEEP4=2,
@@ -94,8 +94,8 @@ def test_two_per_lane_is_bit_identical_to_one_per_lane(runs, i):
 
 @pytest.mark.parametrize("i", [2, 3, 4, 5], ids=[CASES[i][6] for i in (2, 3, 4, 5)])
 def test_split_pass_agrees_with_one_per_lane(runs, i):
-    """The split pass sums a window's columns in another order (two chains over
-    6 cost columns instead of 18): costs agree to fp32 rounding, winners can
+    """The row-split pass starts each warp's sliding sums at the warp's own
+    first row instead of the tile's: costs agree to fp32 rounding, winners can
     differ at exact near ties only."""
     auto, zz1 = runs
     same = auto[f"d{i}"] == zz1[f"d{i}"]
